@@ -1,0 +1,593 @@
+/*
+ * camelot_oracle.c -- plain, slow CPU oracle for the Camelot allocation search.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  It shares no code,
+ * header, table or constant with the CUDA path (paper_2005_02088_b200/csrc/).
+ *
+ * What it computes (PAPER.md = /root/reference/PAPER.md, line numbers):
+ *   - the candidate space: one batch size per application (PAPER.md L858,
+ *     "batch size should also be considered as a variable"), and per stage i a
+ *     replica count N_i and an SM quota p_i shared by its replicas (the SA state
+ *     vector V = [n1..nN, p1..pN]), all on given grids;
+ *   - the deployment scheme of PAPER.md L916-945 (sort GPUs by remaining
+ *     resources, global memory first, fewest resources first; all replicas of a
+ *     stage on one GPU if possible; listing PAPER.md) -- DESIGN.md
+ *     readings R14-R16;
+ *   - the constraints of Eq. 1 / Eq. 3 per GPU
+ *     after placement (prose PAPER.md L774-777: bandwidth "on a GPU") -- R3,R4;
+ *   - the contention-aware predictor: co-located stages' bandwidth pressure
+ *     inflates their latency -- reading R17;
+ *   - objectives: Eq. 1 max of min_i N_i f(p_i) and the
+ *     min-resource policy "first minimizes the number of GPUs ... then the
+ *     resource usage" (Eq. 3) with a load floor -- R10,R11;
+ *   - Eq. 2 GPU-count estimate -- reading R9.
+ * Arithmetic: IEEE binary32, round-to-nearest-even, no FMA contraction
+ * (compiled with -ffp-contract=off), every operation in the order written
+ * below.  The paper fixes no precision; binary32 is the kernel's precision and
+ * every output of the search is an integer decision (verdict, argmax), which
+ * both sides therefore take in the same precision (R21).
+ * A float64 re-evaluation of the latencies of a given placement is provided to
+ * bound the binary32 rounding error (north_star: latencies within 1e-5 rel).
+ *
+ * Pins: tests/test_oracle_*.py (worked examples, closed forms, invariants,
+ * brute force); see DESIGN.md "Oracle pins".
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define OC_MAX_STAGES 8
+#define OC_MAX_APPS 2
+#define OC_MAX_GPUS 16
+#define OC_MAX_REPL 16
+#define OC_MAX_LOADS 64
+
+/* flags */
+#define OC_NO_BW_CAP 1u
+#define OC_NO_CONTENTION 2u
+#define OC_SAT 4u
+#define OC_PAPER_GLOBAL 8u
+#define OC_EQ2_BUDGET 16u
+
+/* first-failing-check bits */
+#define OC_V_QUOTA 1u
+#define OC_V_INST 2u
+#define OC_V_MEM 4u
+#define OC_V_BW 8u
+#define OC_V_QOS 16u
+#define OC_V_LOAD 32u
+#define OC_V_EQ2 64u
+
+typedef struct {
+    int32_t A, n;
+    const int32_t *app;   /* [n] application of each stage, app-major order */
+    const float *qos;     /* [A] QoS target (ms) */
+    int32_t nQ;
+    const int32_t *Q;     /* SM-quota grid (%) */
+    int32_t nS;
+    const int32_t *S;     /* batch grid */
+    int32_t Rmax;         /* replicas N_i in 1..Rmax */
+    const float *tab;     /* [n][nS][nQ][4] = dur_ms, thr_qps, bw_gbs, unused */
+    const uint32_t *W;    /* [n] weights footprint (MiB) */
+    const uint32_t *Am;   /* [n] activation footprint per batch item (MiB) */
+    const float *cflop;   /* [n] GFLOP per item */
+    const float *gamma;   /* [n] bandwidth sensitivity */
+    uint32_t flags;
+    int32_t C, R, I;      /* GPUs, quota per GPU (%), max instances per GPU */
+    float BW;             /* GB/s per GPU */
+    uint32_t FM;          /* MiB per GPU */
+    float G;              /* GFLOPS per GPU */
+} oc_problem;
+
+typedef struct {
+    uint32_t verdict;         /* first failing check of the max-load policy (0 = feasible) */
+    uint32_t place_viol;      /* placement failure bits (0 = placed) */
+    float T;                  /* min over apps of Tmin_a */
+    int32_t u, U;             /* GPUs used, sum N_i p_i */
+    float Tmin[OC_MAX_APPS];
+    float Lsum[OC_MAX_APPS];
+    float L[OC_MAX_STAGES], Ti[OC_MAX_STAGES], kappa[OC_MAX_STAGES];
+    double L64[OC_MAX_STAGES], T64[OC_MAX_STAGES], Lsum64[OC_MAX_APPS];
+    int8_t gpu_of_instance[OC_MAX_STAGES * OC_MAX_REPL];  /* -1 = unused */
+    float dem[OC_MAX_GPUS];
+    uint32_t level_verdict[OC_MAX_LOADS];  /* min-resource: first failing check per load level */
+    int32_t eq2_y[OC_MAX_LOADS];
+} oc_score_t;
+
+typedef struct {
+    uint64_t index;       /* UINT64_MAX if no feasible candidate */
+    float T;              /* objective (max-load) of the winner */
+    int32_t u, U;
+    uint64_t n_feasible;
+    uint64_t n_scanned;
+    uint64_t hist[7];     /* first-failing-check histogram: QUOTA..EQ2 (placement bits counted per bit) */
+} oc_best_t;
+
+/* ---------------------------------------------------------------- validation */
+static int fin(float v) { return isfinite(v); }
+
+int oc_validate(const oc_problem *P) {
+    if (P->n < 1 || P->n > OC_MAX_STAGES) return -1;
+    if (P->A < 1 || P->A > OC_MAX_APPS) return -1;
+    if (P->C < 1 || P->C > OC_MAX_GPUS) return -2;
+    if (P->R < 1 || P->R > 127 || P->I < 1) return -1;
+    if (!(P->BW > 0.0f) || !fin(P->BW) || !(P->G > 0.0f) || P->FM < 1) return -1;
+    if (P->Rmax < 1 || P->Rmax > OC_MAX_REPL) return -1;
+    if (P->nQ < 1 || P->nS < 1) return -1;
+    for (int k = 0; k < P->nQ; k++) {
+        if (P->Q[k] < 1 || P->Q[k] > P->R) return -1;
+        if (k > 0 && P->Q[k] <= P->Q[k - 1]) return -1;
+    }
+    for (int k = 0; k < P->nS; k++) {
+        if (P->S[k] < 1) return -1;
+        if (k > 0 && P->S[k] <= P->S[k - 1]) return -1;
+    }
+    for (int i = 0; i < P->n; i++) {
+        if (P->app[i] < 0 || P->app[i] >= P->A) return -1;
+        if (i > 0 && P->app[i] < P->app[i - 1]) return -1;
+        if (!(P->gamma[i] >= 0.0f) || !fin(P->gamma[i])) return -1;
+        if (!fin(P->cflop[i]) || P->cflop[i] < 0.0f) return -1;
+    }
+    if (P->app[0] != 0 || P->app[P->n - 1] != P->A - 1) return -1;
+    for (int a = 0; a < P->A; a++)
+        if (!(P->qos[a] > 0.0f) || !fin(P->qos[a])) return -1;
+    for (long e = 0; e < (long)P->n * P->nS * P->nQ; e++) {
+        const float *t = P->tab + 4 * e;
+        if (!fin(t[0]) || !fin(t[1]) || !fin(t[2])) return -1;
+        if (!(t[0] > 0.0f) || !(t[1] > 0.0f) || !(t[2] >= 0.0f)) return -1;
+    }
+    return 0;
+}
+
+/* Ntot = |S|^A * (Rmax*|Q|)^n ; 0 if >= 2^63 */
+uint64_t oc_ntot(const oc_problem *P) {
+    unsigned __int128 t = 1;
+    for (int a = 0; a < P->A; a++) t *= (unsigned)P->nS;
+    for (int i = 0; i < P->n; i++) t *= (unsigned)(P->Rmax * P->nQ);
+    if (t >= ((unsigned __int128)1 << 63)) return 0;
+    return (uint64_t)t;
+}
+
+/* Candidate digits, most significant first: beta_1..beta_A, rho_1, theta_1, ...,
+ * rho_n, theta_n (DESIGN.md R-enum).  N_i = rho_i + 1, p_i = Q[theta_i],
+ * s_a = S[beta_a]. */
+void oc_decode(const oc_problem *P, uint64_t x, int32_t *beta, int32_t *rho, int32_t *theta) {
+    for (int i = P->n - 1; i >= 0; i--) {
+        theta[i] = (int32_t)(x % (uint64_t)P->nQ);
+        x /= (uint64_t)P->nQ;
+        rho[i] = (int32_t)(x % (uint64_t)P->Rmax);
+        x /= (uint64_t)P->Rmax;
+    }
+    for (int a = P->A - 1; a >= 0; a--) {
+        beta[a] = (int32_t)(x % (uint64_t)P->nS);
+        x /= (uint64_t)P->nS;
+    }
+}
+
+uint64_t oc_encode(const oc_problem *P, const int32_t *beta, const int32_t *rho, const int32_t *theta) {
+    uint64_t x = 0;
+    for (int a = 0; a < P->A; a++) x = x * (uint64_t)P->nS + (uint64_t)beta[a];
+    for (int i = 0; i < P->n; i++) {
+        x = x * (uint64_t)P->Rmax + (uint64_t)rho[i];
+        x = x * (uint64_t)P->nQ + (uint64_t)theta[i];
+    }
+    return x;
+}
+
+static const float *entry(const oc_problem *P, int i, int b, int q) {
+    return P->tab + 4 * (((long)i * P->nS + b) * P->nQ + q);
+}
+
+/* ------------------------------------------------------------------ placement
+ * PAPER.md L929-945 + listing L955-979, readings R14-R16. */
+typedef struct {
+    int32_t rq[OC_MAX_GPUS];     /* remaining quota (%) */
+    int32_t cnt[OC_MAX_GPUS];    /* instances hosted */
+    int64_t rm[OC_MAX_GPUS];     /* remaining memory (MiB) */
+    float dem[OC_MAX_GPUS];      /* accumulated bandwidth demand (GB/s) */
+    int32_t host[OC_MAX_STAGES][OC_MAX_GPUS];
+} oc_state;
+
+/* can GPU g take k more replicas of stage i?  returns 0 if yes, else the
+ * failing dimension bits */
+static uint32_t fit_bits(const oc_problem *P, const oc_state *st, int i, int g, int k,
+                         int32_t p, int64_t s, float bw) {
+    uint32_t v = 0;
+    if ((int64_t)k * p > st->rq[g]) v |= OC_V_QUOTA;
+    if (st->cnt[g] + k > P->I) v |= OC_V_INST;
+    int64_t need = (st->host[i][g] == 0 ? (int64_t)P->W[i] : 0) + (int64_t)k * (int64_t)P->Am[i] * s;
+    if (need > st->rm[g]) v |= OC_V_MEM;
+    if (!(P->flags & OC_NO_BW_CAP)) {
+        float add = (float)k * bw;
+        float tot = st->dem[g] + add;
+        if (tot > P->BW) v |= OC_V_BW;
+    }
+    return v;
+}
+
+static int can_hold(const oc_problem *P, const oc_state *st, int i, int g, int m,
+                    int32_t p, int64_t s, float bw) {
+    for (int k = m; k >= 1; k--)
+        if (fit_bits(P, st, i, g, k, p, s, bw) == 0) return k;
+    return 0;
+}
+
+static void deploy(const oc_problem *P, oc_state *st, int i, int g, int k, int32_t p,
+                   int64_t s, float bw) {
+    st->rq[g] -= k * p;
+    st->cnt[g] += k;
+    st->rm[g] -= (st->host[i][g] == 0 ? (int64_t)P->W[i] : 0) + (int64_t)k * (int64_t)P->Am[i] * s;
+    float add = (float)k * bw;
+    st->dem[g] = st->dem[g] + add;
+    st->host[i][g] += k;
+}
+
+/* returns 0 if every stage was placed, else the placement-failure bits */
+static uint32_t place_all(const oc_problem *P, const int32_t *beta, const int32_t *rho,
+                          const int32_t *theta, oc_state *st) {
+    for (int g = 0; g < P->C; g++) {
+        st->rq[g] = P->R;
+        st->cnt[g] = 0;
+        st->rm[g] = (int64_t)P->FM;
+        st->dem[g] = 0.0f;
+        for (int i = 0; i < P->n; i++) st->host[i][g] = 0;
+    }
+    for (int i = 0; i < P->n; i++) {
+        int b = beta[P->app[i]];
+        int64_t s = P->S[b];
+        int32_t p = P->Q[theta[i]];
+        int N = rho[i] + 1;
+        float bw = entry(P, i, b, theta[i])[2];
+        /* 1. snapshot order: GPUs by (remaining memory, remaining quota, index) ascending */
+        int order[OC_MAX_GPUS];
+        for (int g = 0; g < P->C; g++) order[g] = g;
+        for (int a = 1; a < P->C; a++) {           /* insertion sort */
+            int g = order[a], j = a - 1;
+            while (j >= 0) {
+                int h = order[j];
+                int less = (st->rm[g] < st->rm[h]) ||
+                           (st->rm[g] == st->rm[h] && st->rq[g] < st->rq[h]) ||
+                           (st->rm[g] == st->rm[h] && st->rq[g] == st->rq[h] && g < h);
+                if (!less) break;
+                order[j + 1] = h;
+                j--;
+            }
+            order[j + 1] = g;
+        }
+        /* 2. pass 1: all N_i replicas on the first GPU that holds them */
+        int placed = 0;
+        for (int j = 0; j < P->C && !placed; j++) {
+            int g = order[j];
+            if (can_hold(P, st, i, g, N, p, s, bw) == N) {
+                deploy(P, st, i, g, N, p, s, bw);
+                placed = 1;
+            }
+        }
+        if (placed) continue;
+        /* 3. pass 2: fill greedily in the same order */
+        int rem = N;
+        for (int j = 0; j < P->C && rem > 0; j++) {
+            int g = order[j];
+            int k = can_hold(P, st, i, g, rem, p, s, bw);
+            if (k > 0) {
+                deploy(P, st, i, g, k, p, s, bw);
+                rem -= k;
+            }
+        }
+        if (rem > 0) {
+            uint32_t v = 0;
+            for (int j = 0; j < P->C; j++) v |= fit_bits(P, st, i, order[j], 1, p, s, bw);
+            return v ? v : OC_V_QUOTA;   /* (v == 0 cannot happen: some g failed k=1) */
+        }
+    }
+    return 0;
+}
+
+/* Eq. 2, rate reading R9:
+ * y = clamp(max(ceil(sum_a lambda_a * sum_{i in a} c_i / G), ceil(sum_i M(i,s)/F)), 1, C)
+ * with M(i,s) = W_i + A_i*s; computed in float64. */
+static int32_t eq2_y(const oc_problem *P, const int32_t *beta, const float *lam) {
+    double comp = 0.0, mem = 0.0;
+    for (int i = 0; i < P->n; i++) {
+        comp += (double)lam[P->app[i]] * (double)P->cflop[i];
+        mem += (double)P->W[i] + (double)P->Am[i] * (double)P->S[beta[P->app[i]]];
+    }
+    double y1 = ceil(comp / (double)P->G), y2 = ceil(mem / (double)P->FM);
+    double y = y1 > y2 ? y1 : y2;
+    if (y < 1.0) y = 1.0;
+    if (y > (double)P->C) y = (double)P->C;
+    return (int32_t)y;
+}
+
+/* ---------------------------------------------------------------- scoring
+ * Score one candidate (all checks, no short-cuts).  loads: [L][A] (may be NULL
+ * when L == 0).  Returns 0. */
+int oc_score(const oc_problem *P, const int32_t *beta, const int32_t *rho, const int32_t *theta,
+             const float *loads, int L, oc_score_t *out) {
+    memset(out, 0, sizeof(*out));
+    for (int k = 0; k < OC_MAX_STAGES * OC_MAX_REPL; k++) out->gpu_of_instance[k] = -1;
+    const int n = P->n;
+    float dur[OC_MAX_STAGES], thr[OC_MAX_STAGES], bwv[OC_MAX_STAGES];
+    int32_t Nn[OC_MAX_STAGES];
+    int32_t U = 0;
+    for (int i = 0; i < n; i++) {
+        const float *e = entry(P, i, beta[P->app[i]], theta[i]);
+        dur[i] = e[0];
+        thr[i] = e[1];
+        bwv[i] = e[2];
+        Nn[i] = rho[i] + 1;
+        U += Nn[i] * P->Q[theta[i]];
+    }
+    out->U = U;
+    float kmax[OC_MAX_STAGES];
+    uint32_t pv = 0;
+    static const oc_state zero_state;
+    oc_state st = zero_state;
+    if (P->flags & OC_PAPER_GLOBAL) {
+        /* literal Eq. 1 Constraints 1-4 as global sums (reading R3 flag) */
+        int64_t q = 0, ni = 0, mem = 0;
+        float bsum = 0.0f;
+        for (int i = 0; i < n; i++) {
+            int64_t s = P->S[beta[P->app[i]]];
+            q += (int64_t)Nn[i] * P->Q[theta[i]];
+            ni += Nn[i];
+            float t = (float)Nn[i] * bwv[i];
+            bsum = bsum + t;
+            mem += (int64_t)Nn[i] * ((int64_t)P->W[i] + (int64_t)P->Am[i] * s);
+        }
+        if (q > (int64_t)P->C * P->R) pv |= OC_V_QUOTA;
+        if (ni > (int64_t)P->C * P->I) pv |= OC_V_INST;
+        float cap = (float)P->C * P->BW;
+        if (!(P->flags & OC_NO_BW_CAP) && bsum > cap) pv |= OC_V_BW;
+        if (mem > (int64_t)P->C * (int64_t)P->FM) pv |= OC_V_MEM;
+        out->u = 0;
+        for (int i = 0; i < n; i++) kmax[i] = 1.0f;
+    } else {
+        pv = place_all(P, beta, rho, theta, &st);
+        int u = 0;
+        for (int g = 0; g < P->C; g++) {
+            if (st.cnt[g] > 0) u++;
+            out->dem[g] = st.dem[g];
+        }
+        out->u = u;
+        /* instance -> GPU map (replica order: by GPU index) */
+        for (int i = 0; i < n; i++) {
+            int r = 0;
+            for (int g = 0; g < P->C; g++)
+                for (int k = 0; k < st.host[i][g]; k++) out->gpu_of_instance[i * OC_MAX_REPL + r++] = (int8_t)g;
+        }
+        /* contention (reading R17): kappa_{i,g} = 1 + gamma_i * (dem_g - bw_i) / BW,
+         * x max(1, dem_g/BW) under SAT; worst GPU hosting the stage */
+        float invBW = 1.0f / P->BW;
+        for (int i = 0; i < n; i++) {
+            kmax[i] = 1.0f;
+            if (P->flags & OC_NO_CONTENTION) continue;
+            for (int g = 0; g < P->C; g++) {
+                if (st.host[i][g] == 0) continue;
+                float d = st.dem[g] - bwv[i];
+                float t = d * invBW;
+                float t2 = P->gamma[i] * t;
+                float kap = 1.0f + t2;
+                if (P->flags & OC_SAT) {
+                    float r = st.dem[g] * invBW;
+                    if (r > 1.0f) kap = kap * r;
+                }
+                if (kap > kmax[i]) kmax[i] = kap;
+            }
+        }
+    }
+    out->place_viol = pv;
+    /* predictions (Table 2: f(p_i) throughput, duration) with contention */
+    for (int i = 0; i < n; i++) {
+        out->kappa[i] = kmax[i];
+        out->L[i] = dur[i] * kmax[i];
+        float nt = (float)Nn[i] * thr[i];
+        out->Ti[i] = nt / kmax[i];
+        out->L64[i] = (double)dur[i] * (double)kmax[i];
+        out->T64[i] = (double)Nn[i] * (double)thr[i] / (double)kmax[i];
+    }
+    /* float64 kappa from float64 demand sums of the same placement */
+    if (!(P->flags & OC_PAPER_GLOBAL) && !(P->flags & OC_NO_CONTENTION)) {
+        double dem64[OC_MAX_GPUS];
+        for (int g = 0; g < P->C; g++) {
+            dem64[g] = 0.0;
+            for (int i = 0; i < n; i++) dem64[g] += (double)st.host[i][g] * (double)bwv[i];
+        }
+        for (int i = 0; i < n; i++) {
+            double km = 1.0;
+            for (int g = 0; g < P->C; g++) {
+                if (st.host[i][g] == 0) continue;
+                double kap = 1.0 + (double)P->gamma[i] * (dem64[g] - (double)bwv[i]) / (double)P->BW;
+                if ((P->flags & OC_SAT) && dem64[g] / (double)P->BW > 1.0) kap *= dem64[g] / (double)P->BW;
+                if (kap > km) km = kap;
+            }
+            out->L64[i] = (double)dur[i] * km;
+            out->T64[i] = (double)Nn[i] * (double)thr[i] / km;
+        }
+    }
+    /* per app: ordered latency sum vs QoS (Constraint-5, reading R1) and Tmin */
+    uint32_t qos_fail = 0;
+    float T = 0.0f;
+    for (int a = 0; a < P->A; a++) {
+        int first = 1;
+        float ls = 0.0f, tm = 0.0f;
+        double ls64 = 0.0;
+        for (int i = 0; i < n; i++) {
+            if (P->app[i] != a) continue;
+            if (first) {
+                ls = out->L[i];
+                tm = out->Ti[i];
+                first = 0;
+            } else {
+                ls = ls + out->L[i];
+                if (out->Ti[i] < tm) tm = out->Ti[i];
+            }
+            ls64 += out->L64[i];
+        }
+        out->Lsum[a] = ls;
+        out->Lsum64[a] = ls64;
+        out->Tmin[a] = tm;
+        if (ls > P->qos[a]) qos_fail = 1;
+        if (a == 0 || tm < T) T = tm;
+    }
+    out->T = T;
+    out->verdict = pv ? pv : (qos_fail ? OC_V_QOS : 0u);
+    for (int k = 0; k < L && k < OC_MAX_LOADS; k++) {
+        const float *lam = loads + (long)k * P->A;
+        int32_t y = eq2_y(P, beta, lam);
+        out->eq2_y[k] = y;
+        uint32_t v = out->verdict;
+        if (v == 0) {
+            for (int a = 0; a < P->A; a++)
+                if (out->Tmin[a] < lam[a]) v = OC_V_LOAD;
+        }
+        if (v == 0 && (P->flags & OC_EQ2_BUDGET) && out->u > y) v = OC_V_EQ2;
+        out->level_verdict[k] = v;
+    }
+    return 0;
+}
+
+int oc_score_index(const oc_problem *P, uint64_t x, const float *loads, int L, oc_score_t *out) {
+    int32_t beta[OC_MAX_APPS], rho[OC_MAX_STAGES], theta[OC_MAX_STAGES];
+    oc_decode(P, x, beta, rho, theta);
+    return oc_score(P, beta, rho, theta, loads, L, out);
+}
+
+/* Verdict/objective vectors over [lo,hi): verdict (max-load), T bits, u, U. */
+int oc_score_range(const oc_problem *P, uint64_t lo, uint64_t hi, uint8_t *verdict,
+                   float *T, int32_t *u, int32_t *U) {
+    oc_score_t sc;
+    for (uint64_t x = lo; x < hi; x++) {
+        oc_score_index(P, x, NULL, 0, &sc);
+        verdict[x - lo] = (uint8_t)sc.verdict;
+        T[x - lo] = sc.T;
+        u[x - lo] = sc.u;
+        U[x - lo] = sc.U;
+    }
+    return 0;
+}
+
+/* ---------------------------------------------------------------- search
+ * Plain exhaustive scan in increasing canonical index; keep the best with a
+ * STRICT improvement test, so the smallest index wins among ties (R20).
+ * policy 0 = max-load (maximise T); 1 = min-resource (minimise (u, U)
+ * lexicographically, per load level). */
+static void hist_add(uint64_t *h, uint32_t v) {
+    for (int b = 0; b < 7; b++)
+        if (v & (1u << b)) h[b]++;
+}
+
+static void search_range(const oc_problem *P, int policy, const float *loads, int L,
+                         uint64_t lo, uint64_t hi, oc_best_t *best) {
+    int nb = policy == 0 ? 1 : L;
+    for (int k = 0; k < nb; k++) {
+        memset(&best[k], 0, sizeof(best[k]));
+        best[k].index = UINT64_MAX;
+    }
+    oc_score_t sc;
+    for (uint64_t x = lo; x < hi; x++) {
+        oc_score_index(P, x, loads, policy == 0 ? 0 : L, &sc);
+        if (policy == 0) {
+            best[0].n_scanned++;
+            if (sc.verdict) {
+                hist_add(best[0].hist, sc.verdict);
+                continue;
+            }
+            best[0].n_feasible++;
+            if (best[0].index == UINT64_MAX || sc.T > best[0].T) {
+                best[0].index = x;
+                best[0].T = sc.T;
+                best[0].u = sc.u;
+                best[0].U = sc.U;
+            }
+        } else {
+            for (int k = 0; k < L; k++) {
+                best[k].n_scanned++;
+                uint32_t v = sc.level_verdict[k];
+                if (v) {
+                    hist_add(best[k].hist, v);
+                    continue;
+                }
+                best[k].n_feasible++;
+                int better = best[k].index == UINT64_MAX || sc.u < best[k].u ||
+                             (sc.u == best[k].u && sc.U < best[k].U);
+                if (better) {
+                    best[k].index = x;
+                    best[k].T = sc.T;
+                    best[k].u = sc.u;
+                    best[k].U = sc.U;
+                }
+            }
+        }
+    }
+}
+
+static int better_than(int policy, const oc_best_t *a, const oc_best_t *b) {
+    /* is a strictly better than b (ties -> smaller index) */
+    if (a->index == UINT64_MAX) return 0;
+    if (b->index == UINT64_MAX) return 1;
+    if (policy == 0) {
+        if (a->T != b->T) return a->T > b->T;
+    } else {
+        if (a->u != b->u) return a->u < b->u;
+        if (a->U != b->U) return a->U < b->U;
+    }
+    return a->index < b->index;
+}
+
+/* threads > 1: the range is cut into contiguous pieces scanned independently
+ * and merged by (objective, index) -- the same result as one scan. */
+int oc_search(const oc_problem *P, int policy, const float *loads, int L, uint64_t lo, uint64_t hi,
+              int threads, oc_best_t *best) {
+    if (oc_validate(P) != 0) return -1;
+    if (policy != 0 && (L < 1 || L > OC_MAX_LOADS)) return -1;
+    if (policy != 0)
+        for (int k = 0; k < L * P->A; k++)
+            if (!(loads[k] > 0.0f) || !isfinite(loads[k])) return -1;
+    uint64_t nt = oc_ntot(P);
+    if (nt == 0) return -2;
+    if (hi > nt) hi = nt;
+    if (lo > hi) lo = hi;
+    int nb = policy == 0 ? 1 : L;
+    if (threads < 1) threads = 1;
+    if (threads == 1 || hi - lo < (uint64_t)threads * 64) {
+        search_range(P, policy, loads, L, lo, hi, best);
+        return 0;
+    }
+    oc_best_t *part = (oc_best_t *)calloc((size_t)threads * nb, sizeof(oc_best_t));
+    if (!part) return -3;
+    uint64_t len = hi - lo;
+#pragma omp parallel for num_threads(threads) schedule(static, 1)
+    for (int t = 0; t < threads; t++) {
+        uint64_t a = lo + (uint64_t)((unsigned __int128)len * t / threads);
+        uint64_t b = lo + (uint64_t)((unsigned __int128)len * (t + 1) / threads);
+        search_range(P, policy, loads, L, a, b, part + (size_t)t * nb);
+    }
+    for (int k = 0; k < nb; k++) {
+        oc_best_t acc;
+        memset(&acc, 0, sizeof(acc));
+        acc.index = UINT64_MAX;
+        for (int t = 0; t < threads; t++) {
+            const oc_best_t *q = part + (size_t)t * nb + k;
+            acc.n_feasible += q->n_feasible;
+            acc.n_scanned += q->n_scanned;
+            for (int b = 0; b < 7; b++) acc.hist[b] += q->hist[b];
+            if (better_than(policy, q, &acc)) {
+                acc.index = q->index;
+                acc.T = q->T;
+                acc.u = q->u;
+                acc.U = q->U;
+            }
+        }
+        best[k] = acc;
+    }
+    free(part);
+    return 0;
+}
+
+int oc_eq2_y(const oc_problem *P, const int32_t *beta, const float *lam) { return eq2_y(P, beta, lam); }
+
+int oc_sizeof_score(void) { return (int)sizeof(oc_score_t); }
+int oc_sizeof_best(void) { return (int)sizeof(oc_best_t); }
