@@ -1,0 +1,315 @@
+"""Benchmark of the contention-aware allocation search (BASELINE.json metric:
+"allocation candidates/sec and time-to-optimal-plan at 1/2/4/8 B200").
+
+One step = one full plan of BASELINE config C4 (5-stage pipeline, 8 modeled
+GPUs, 1% SM-quota grid, batch 1..128, up to 4 replicas/stage: 8.192e13
+candidates per policy) for BOTH policies: max peak load (Eq. 1), then minimum
+resource at 30% of that peak (Eq. 3).  Each policy is an exact
+search of the whole space; value = candidates covered per second
+(2 x 8.192e13 / step time), whole job.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+N > 1: launched by torchrun, one rank per GPU; every rank searches its shard
+(chunk c -> rank c mod N) and ONE all_reduce(MIN) of packed int64 keys per
+policy goes over NCCL.  --impl reference times the CPU oracle (oracle/) on a
+bounded slice of the same workload on the host cores.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "allocation candidates/sec (time-to-optimal-plan, both policies)"
+UNIT = "candidates/s"
+WORKLOAD = "C4: 5-stage p1-c2-m2-c3-m1 pipeline, 8 modeled V100 (BW 897 GB/s), 1% quota grid, " \
+           "batch 1..128 (pow2), <=4 replicas/stage; max-load then min-resource at 0.3*T*"
+LOW_LOAD = 0.3   # low load = 30% of the peak
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons DURING the timed region."""
+
+    def __init__(self, dev):
+        self.dev, self.samples, self.proc = dev, [], None
+
+    def __enter__(self):
+        q = "clocks.sm,clocks.max.sm,clocks_event_reasons.active," \
+            "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
+            "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([v.strip() for v in line.split(",")])
+
+    def __exit__(self, *a):
+        time.sleep(0.15)
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4)
+                          if len(s) > 3 + k and s[3 + k].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def cpu_reference_leg(prob, args, rank, world, as_main):
+    """The CPU oracle (plain exhaustive scan, as it stands) on a bounded slice of
+    the workload, on the host cores.  Returns the JSON fields."""
+    from oracle import oracle as O
+    threads = os.cpu_count() or 1
+    nt = O.ntot(prob)
+    # size a slice for ~2 s per step (probe the rate first)
+    lo = nt // 3
+    t0 = time.perf_counter()
+    O.search(prob, lo=lo, hi=lo + 200_000, threads=threads)
+    rate0 = 200_000 / max(1e-6, time.perf_counter() - t0)
+    per_step = args.ref_seconds if as_main else args.cpu_seconds
+    n = int(max(100_000, min(5e9, rate0 * per_step)))
+    times = []
+    steps = args.steps if as_main else 1
+    warm = args.warmup if as_main else 0
+    for s in range(warm + steps):
+        a = lo + s * n
+        t0 = time.perf_counter()
+        b_ = O.search(prob, lo=a, hi=a + n, threads=threads)[0]
+        dt = time.perf_counter() - t0
+        if s >= warm:
+            times.append(dt)
+    rate = n * len(times) / sum(times)
+    sample = f"max-load exhaustive scan of {n} consecutive C4 candidates per step from index {lo} " \
+             f"(one policy; full C4 = 2 x {nt:.4g} candidates)"
+    return dict(value=rate, unit=UNIT, cores=threads, kind="oracle", sample=sample,
+                ms_per_step=1000 * statistics.mean(times), n_per_step=n)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="camelot", choices=["camelot", "reference"])
+    ap.add_argument("--config", type=int, default=4, help="BASELINE config (default 4 = C4)")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="cpu_baseline sample budget")
+    ap.add_argument("--ref-seconds", type=float, default=8.0, help="--impl reference seconds per step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    assert args.warmup >= 3 or args.impl == "reference", "timing rules: >= 3 warm-up steps"
+
+    from gen import problems as G
+    prob = G.config_problems(args.config)[0]
+    rank, world, local = dist_env()
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        r = cpu_reference_leg(prob, args, rank, world, as_main=True)
+        line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT,
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": WORKLOAD, "problem": prob.name, "sha256": prob.sha256(),
+                           "l2": "n/a (CPU)"},
+                "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "oracle",
+                                 "sample": r["sample"]},
+                "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2005_02088_b200 import _lib as L
+    from paper_2005_02088_b200 import api
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.current_stream(dev)
+    sess = api.Session(prob, device=local, n_loads=1)
+    sess.upload()
+    torch.cuda.synchronize()
+    ntot = 1
+    for _ in range(prob.n_apps):
+        ntot *= len(prob.batch)
+    for _ in range(prob.n_stages):
+        ntot *= prob.max_replicas * len(prob.quota_pct)
+
+    def all_reduce_min(keys):
+        if world > 1:
+            dist.all_reduce(keys, op=dist.ReduceOp.MIN)
+
+    def step(resident=True):
+        """Both policies, whole hot path: search shard -> allreduce -> finalize."""
+        k1 = sess.search_local(L.POLICY_MAX_LOAD, rank=rank, world=world, resident=resident)
+        all_reduce_min(k1)
+        pm = sess.finalize(L.POLICY_MAX_LOAD, k1, rank=rank, world=world)[0]
+        st1 = sess.last_stats()
+        lam = [[LOW_LOAD * pm.objective] * prob.n_apps]
+        k2 = sess.search_local(L.POLICY_MIN_RESOURCE, lam, rank=rank, world=world, resident=True)
+        all_reduce_min(k2)
+        pr = sess.finalize(L.POLICY_MIN_RESOURCE, k2, lam, rank=rank, world=world)[0]
+        st2 = sess.last_stats()
+        return pm, pr, st1, st2
+
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    kt = []
+    launches0 = L.lib().camelot_kernel_launches()
+    plans = []
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        for s in range(args.steps):
+            flush.fill_(s & 0xFF)            # L2 flush between timed steps (not timed)
+            ev[s][0].record(stream)
+            pm, pr, st1, st2 = step()
+            ev[s][1].record(stream)
+            plans.append((pm, pr))
+            kt.append((st1, st2))
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    launches = (L.lib().camelot_kernel_launches() - launches0) / args.steps
+    ms = [a.elapsed_time(b) for a, b in ev]
+    ms_step = statistics.mean(ms)
+    t_local = torch.tensor([ms_step], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+    ms_step = float(t_local.item())
+    covered = 2 * ntot
+    value = covered / (ms_step / 1000.0)
+
+    # e2e: through the public API with the problem copied from pinned host
+    # memory every step (not resident) and the plans read back to the host
+    e2e = None
+    if not args.no_e2e:
+        for _ in range(2):
+            step(resident=False)
+        torch.cuda.synchronize()
+        ee = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        for s in range(args.steps):
+            flush.fill_(s & 0xFF)
+            ee[s][0].record(stream)
+            step(resident=False)
+            ee[s][1].record(stream)
+        torch.cuda.synchronize()
+        e_ms = statistics.mean(a.elapsed_time(b) for a, b in ee)
+        t_e = torch.tensor([e_ms], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
+        e_ms = float(t_e.item())
+        h2d = prob.table.nbytes + prob.quota_pct.nbytes + prob.batch.nbytes + 4 * prob.n_apps
+        d2h = 2 * C_sizeof_plan()
+        e2e = {"value": covered / (e_ms / 1000.0), "unit": UNIT, "ms_per_step": e_ms,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+    # roofline of the dominant kernel (the main search kernel): ALU/issue bound
+    peaks = load_peaks()
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    clocks = clk.summary()
+    ops_per_eval = algorithmic_ops_per_eval(prob)
+    evals = sum(s1["n_scored"] + s1["n_nodes"] + s2["n_scored"] + s2["n_nodes"] for s1, s2 in kt) / args.steps
+    k_ns = sum(s1["t_ns"] + s2["t_ns"] for s1, s2 in kt) / args.steps
+    achieved = ops_per_eval * evals / (k_ns * 1e-9) / 1e12 if k_ns else None
+    peak = n_sm * 4 * 32 * sm_max * 1e6 / 1e12          # lane-instructions/s (issue bound)
+    roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s",
+            "frac": (achieved / peak) if achieved else None, "traffic": None,
+            "kernel": "search_kernel (main pass, both policies)",
+            "ops_per_eval": ops_per_eval, "evals_per_step": evals,
+            "kernel_ms_per_step": k_ns / 1e6,
+            "kernel_share_of_step": (k_ns / 1e6) / ms_step if ms_step else None,
+            "peak_note": f"{n_sm} SMs x 4 SMSP x 32 lanes x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        r = cpu_reference_leg(prob, args, rank, world, as_main=False)
+        cpu = {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "oracle", "sample": r["sample"]}
+
+    pm, pr = plans[-1]
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": WORKLOAD, "problem": prob.name, "sha256": prob.sha256(),
+                           "candidates_per_policy": ntot, "policies": 2, "parallelism": f"shard{world}",
+                           "l2": "flushed between timed steps (256 MiB write)"},
+                "time_to_plan_ms": ms_step,
+                "plans": {"max_load": {"index": pm.index, "T": pm.objective, "replicas": pm.replicas,
+                                       "quota_pct": pm.quota_pct, "batch": pm.batch},
+                          "min_resource": {"index": pr.index, "gpus_used": pr.gpus_used,
+                                           "quota_used": pr.quota_used, "load": LOW_LOAD * pm.objective}},
+                "scored_per_step": evals, "gpu_launches": launches, "roofline": roof, "clocks": clocks,
+                "e2e": e2e, "cpu_baseline": cpu}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def C_sizeof_plan():
+    import ctypes
+    from paper_2005_02088_b200 import _lib as L
+    return ctypes.sizeof(L.Plan)
+
+
+def algorithmic_ops_per_eval(prob):
+    """Algorithmic operations of one tree-node / leaf evaluation (DESIGN.md
+    "Roofline"): first-fit placement test 4 ops x C GPUs, demand update 2,
+    host-max update (n-1), contention factor 4 per stage, latency 1 per stage,
+    ordered sum (n-1), QoS compare A, throughput bound 2, key compare 2."""
+    n, C, A = prob.n_stages, prob.cluster.n_gpus, prob.n_apps
+    return 4 * C + 2 + (n - 1) + 4 * n + n + (n - 1) + A + 2 + 2
+
+
+if __name__ == "__main__":
+    main()

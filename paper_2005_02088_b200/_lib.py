@@ -1,0 +1,128 @@
+"""ctypes declarations of include/camelot.h and the loader of libcamelot.so.
+
+Argument marshalling only: every step of the search runs in the CUDA kernels of
+libcamelot.so.  If the library is missing the import of the compute entry
+points raises -- there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+LIB = os.path.join(HERE, "libcamelot.so")
+HEADER = os.path.join(ROOT, "include", "camelot.h")
+
+MAX_STAGES, MAX_APPS, MAX_GPUS, MAX_REPLICAS, MAX_LOADS = 8, 2, 16, 16, 64
+OK, INFEASIBLE, EINVAL, ERANGE, ECUDA, ENODEV, ENOMEM = 0, 1, -1, -2, -3, -4, -5
+F_NO_BW_CAP, F_NO_CONTENTION, F_SAT, F_PAPER_GLOBAL, F_EQ2_BUDGET, F_NO_FILTER = 1, 2, 4, 8, 16, 32
+V_QUOTA, V_INST, V_MEM, V_BW, V_QOS, V_LOAD, V_EQ2 = 1, 2, 4, 8, 16, 32, 64
+POLICY_MAX_LOAD, POLICY_MIN_RESOURCE = 0, 1
+EXEC_RESIDENT = 1
+
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+              "-fmad=false", "-Xcompiler", "-fPIC", "-shared", "-cudart", "static"]
+
+
+def sources():
+    return [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC))
+            if f.endswith((".cu", ".cuh"))] + [HEADER]
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile libcamelot.so for sm_100a (in-tree)."""
+    newest = max(os.path.getmtime(s) for s in sources())
+    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < newest:
+        cmd = ["nvcc"] + NVCC_FLAGS + (["-Xptxas", "-v"] if verbose else []) + \
+              ["-o", LIB, os.path.join(CSRC, "camelot_api.cu")]
+        subprocess.check_call(cmd)
+    return LIB
+
+
+class Cluster(C.Structure):
+    _fields_ = [("n_gpus", C.c_int32), ("quota_per_gpu", C.c_int32), ("max_instances", C.c_int32),
+                ("bw_gbs", C.c_float), ("mem_mib", C.c_uint32), ("gflops", C.c_float)]
+
+
+class Problem(C.Structure):
+    _fields_ = [("n_apps", C.c_int32), ("n_stages", C.c_int32),
+                ("app_of_stage", C.POINTER(C.c_int32)), ("qos_ms", C.POINTER(C.c_float)),
+                ("n_quota", C.c_int32), ("quota_pct", C.POINTER(C.c_int32)),
+                ("n_batch", C.c_int32), ("batch", C.POINTER(C.c_int32)),
+                ("max_replicas", C.c_int32), ("table", C.POINTER(C.c_float)),
+                ("weights_mib", C.POINTER(C.c_uint32)), ("act_mib_per_item", C.POINTER(C.c_uint32)),
+                ("gflop_per_item", C.POINTER(C.c_float)), ("bw_sensitivity", C.POINTER(C.c_float)),
+                ("flags", C.c_uint32)]
+
+
+class Exec(C.Structure):
+    _fields_ = [("device", C.c_int32), ("stream", C.c_void_p), ("rank", C.c_int32), ("world", C.c_int32),
+                ("index_lo", C.c_uint64), ("index_hi", C.c_uint64), ("workspace", C.c_void_p),
+                ("workspace_bytes", C.c_size_t), ("exec_flags", C.c_uint32)]
+
+
+class Plan(C.Structure):
+    _fields_ = [("index", C.c_uint64), ("status", C.c_int32),
+                ("batch", C.c_int32 * MAX_APPS),
+                ("replicas", C.c_int32 * MAX_STAGES), ("quota_pct", C.c_int32 * MAX_STAGES),
+                ("gpu_of_instance", C.c_int8 * (MAX_STAGES * MAX_REPLICAS)),
+                ("stage_latency_ms", C.c_float * MAX_STAGES),
+                ("stage_throughput_qps", C.c_float * MAX_STAGES),
+                ("kappa", C.c_float * MAX_STAGES),
+                ("e2e_latency_ms", C.c_float * MAX_APPS), ("throughput_qps", C.c_float * MAX_APPS),
+                ("objective", C.c_float), ("quota_used", C.c_int32), ("gpus_used", C.c_int32),
+                ("eq2_gpus", C.c_int32), ("violations", C.c_uint32),
+                ("n_feasible", C.c_uint64), ("n_scored", C.c_uint64), ("n_covered", C.c_uint64)]
+
+
+EXPORTS = ["camelot_last_error", "camelot_version", "camelot_workspace_bytes", "camelot_upload",
+           "camelot_plan_max_load", "camelot_plan_min_resource", "camelot_predict",
+           "camelot_score_range", "camelot_search_local", "camelot_finalize", "camelot_last_stats",
+           "camelot_kernel_launches"]
+
+_lib = None
+
+
+class CamelotError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"camelot error {code}: {msg}")
+        self.code = code
+
+
+def lib():
+    """Load libcamelot.so (raises if it is missing: no CPU fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB):
+            raise ImportError(f"{LIB} is missing: run __graft_entry__.build() (there is no CPU fallback)")
+        L = C.CDLL(LIB)
+        L.camelot_last_error.restype = C.c_char_p
+        L.camelot_version.restype = C.c_char_p
+        L.camelot_workspace_bytes.restype = C.c_size_t
+        L.camelot_workspace_bytes.argtypes = [C.POINTER(Problem), C.POINTER(Cluster), C.c_int]
+        P, Cl, E, Pl = C.POINTER(Problem), C.POINTER(Cluster), C.POINTER(Exec), C.POINTER(Plan)
+        fp = C.POINTER(C.c_float)
+        L.camelot_upload.argtypes = [P, Cl, E]
+        L.camelot_plan_max_load.argtypes = [P, Cl, E, Pl]
+        L.camelot_plan_min_resource.argtypes = [P, Cl, fp, C.c_int, E, Pl]
+        ip = C.POINTER(C.c_int32)
+        L.camelot_predict.argtypes = [P, Cl, ip, ip, ip, fp, C.c_int, E, Pl]
+        L.camelot_score_range.argtypes = [P, Cl, C.c_uint64, C.c_uint64, E, C.c_void_p, C.c_void_p,
+                                          C.c_void_p, C.c_void_p]
+        L.camelot_search_local.argtypes = [P, Cl, C.c_int, fp, C.c_int, E, C.c_void_p]
+        L.camelot_finalize.argtypes = [P, Cl, C.c_int, fp, C.c_int, C.c_void_p, E, Pl]
+        L.camelot_last_stats.argtypes = [E, C.POINTER(C.c_uint64)]
+        L.camelot_kernel_launches.restype = C.c_uint64
+        for f in EXPORTS:
+            getattr(L, f)
+        _lib = L
+    return _lib
+
+
+def check(rc: int, allow_infeasible: bool = True) -> int:
+    if rc == OK or (allow_infeasible and rc == INFEASIBLE):
+        return rc
+    raise CamelotError(rc, lib().camelot_last_error().decode())

@@ -1,0 +1,274 @@
+"""Python API over the C ABI (include/camelot.h): argument marshalling only.
+
+PyTorch provides the device workspace, the stream and (for N > 1 GPUs) the
+process group; every step of the allocation search runs in libcamelot.so's
+kernels.  A problem is any object with the attributes of gen.problems.Problem
+(Table 2 variables of the paper).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+from typing import List, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib as L
+
+
+@dataclasses.dataclass
+class PlanResult:
+    """One optimal plan (camelot_plan)."""
+    status: int
+    index: Optional[int]
+    batch: List[int]
+    replicas: List[int]
+    quota_pct: List[int]
+    gpu_of_instance: List[List[int]]
+    stage_latency_ms: List[float]
+    stage_throughput_qps: List[float]
+    kappa: List[float]
+    e2e_latency_ms: List[float]
+    throughput_qps: List[float]
+    objective: float
+    quota_used: int
+    gpus_used: int
+    eq2_gpus: int
+    violations: int
+    n_feasible: int
+    n_scored: int
+    n_covered: int
+
+    @property
+    def feasible(self) -> bool:
+        return self.status == L.OK
+
+
+def _plan(p: L.Plan, n: int, A: int) -> PlanResult:
+    none = p.index == (1 << 64) - 1
+    goi = [[g for g in p.gpu_of_instance[i * L.MAX_REPLICAS:(i + 1) * L.MAX_REPLICAS] if g >= 0]
+           for i in range(n)]
+    return PlanResult(p.status, None if none else int(p.index), list(p.batch[:A]),
+                      list(p.replicas[:n]), list(p.quota_pct[:n]), goi,
+                      list(p.stage_latency_ms[:n]), list(p.stage_throughput_qps[:n]),
+                      list(p.kappa[:n]), list(p.e2e_latency_ms[:A]), list(p.throughput_qps[:A]),
+                      p.objective, p.quota_used, p.gpus_used, p.eq2_gpus, p.violations,
+                      int(p.n_feasible), int(p.n_scored), int(p.n_covered))
+
+
+class Session:
+    """One problem bound to a device workspace (torch uint8 tensor) and a stream."""
+
+    def __init__(self, problem, device: Optional[int] = None, n_loads: int = 0,
+                 flags: Optional[int] = None, stream: Optional[torch.cuda.Stream] = None):
+        L.lib()
+        if not torch.cuda.is_available():
+            raise L.CamelotError(L.ENODEV, "no CUDA device (there is no CPU fallback)")
+        self.device = torch.cuda.current_device() if device is None else device
+        self.stream = stream
+        self.problem = problem
+        self.n, self.A = int(problem.n_stages), int(problem.n_apps)
+        pin = True
+        self._keep = dict(
+            app=np.ascontiguousarray(problem.app_of_stage, np.int32),
+            qos=np.ascontiguousarray(problem.qos_ms, np.float32),
+            Q=np.ascontiguousarray(problem.quota_pct, np.int32),
+            S=np.ascontiguousarray(problem.batch, np.int32),
+            W=np.ascontiguousarray(problem.weights_mib, np.uint32),
+            Am=np.ascontiguousarray(problem.act_mib_per_item, np.uint32),
+            cf=np.ascontiguousarray(problem.gflop_per_item, np.float32),
+            gm=np.ascontiguousarray(problem.bw_sensitivity, np.float32),
+        )
+        tab = np.ascontiguousarray(problem.table, np.float32)
+        # pinned host copy of the predictor tables (the only sizeable input)
+        self._tab = torch.from_numpy(tab.copy()).pin_memory() if pin else torch.from_numpy(tab)
+        k = self._keep
+        ptr = lambda a, t: a.ctypes.data_as(C.POINTER(t))
+        self.cprob = L.Problem(
+            n_apps=self.A, n_stages=self.n, app_of_stage=ptr(k["app"], C.c_int32),
+            qos_ms=ptr(k["qos"], C.c_float), n_quota=len(k["Q"]), quota_pct=ptr(k["Q"], C.c_int32),
+            n_batch=len(k["S"]), batch=ptr(k["S"], C.c_int32), max_replicas=int(problem.max_replicas),
+            table=C.cast(self._tab.data_ptr(), C.POINTER(C.c_float)),
+            weights_mib=ptr(k["W"], C.c_uint32), act_mib_per_item=ptr(k["Am"], C.c_uint32),
+            gflop_per_item=ptr(k["cf"], C.c_float), bw_sensitivity=ptr(k["gm"], C.c_float),
+            flags=int(problem.flags if flags is None else flags))
+        c = problem.cluster
+        self.ccl = L.Cluster(n_gpus=int(c.n_gpus), quota_per_gpu=int(c.quota_per_gpu),
+                             max_instances=int(c.max_instances), bw_gbs=float(c.bw_gbs),
+                             mem_mib=int(c.mem_mib), gflops=float(c.gflops))
+        self.ws = None
+        self._ensure(n_loads)
+
+    # ------------------------------------------------------------------ plumbing
+    def _ensure(self, n_loads: int):
+        nb = L.lib().camelot_workspace_bytes(C.byref(self.cprob), C.byref(self.ccl), int(n_loads))
+        if nb == 0:
+            raise L.CamelotError(L.EINVAL, L.lib().camelot_last_error().decode())
+        if self.ws is None or self.ws.numel() < nb:
+            self.ws = torch.empty(nb, dtype=torch.uint8, device=f"cuda:{self.device}")
+
+    def _stream_ptr(self):
+        s = self.stream if self.stream is not None else torch.cuda.current_stream(self.device)
+        return s.cuda_stream
+
+    def exec(self, rank: int = 0, world: int = 1, lo: int = 0, hi: int = 0, resident: bool = False) -> L.Exec:
+        return L.Exec(device=self.device, stream=self._stream_ptr(), rank=rank, world=world,
+                      index_lo=lo, index_hi=hi, workspace=self.ws.data_ptr(),
+                      workspace_bytes=self.ws.numel(), exec_flags=L.EXEC_RESIDENT if resident else 0)
+
+    def _loads(self, loads):
+        arr = np.ascontiguousarray(np.asarray(loads, np.float32).reshape(-1, self.A))
+        return arr, arr.shape[0]
+
+    # ------------------------------------------------------------------ entry points
+    def upload(self):
+        ex = self.exec()
+        L.check(L.lib().camelot_upload(C.byref(self.cprob), C.byref(self.ccl), C.byref(ex)), False)
+
+    def plan_max_load(self, lo: int = 0, hi: int = 0, resident: bool = False) -> PlanResult:
+        out = L.Plan()
+        ex = self.exec(lo=lo, hi=hi, resident=resident)
+        L.check(L.lib().camelot_plan_max_load(C.byref(self.cprob), C.byref(self.ccl), C.byref(ex), C.byref(out)))
+        return _plan(out, self.n, self.A)
+
+    def plan_min_resource(self, loads, lo: int = 0, hi: int = 0, resident: bool = False) -> List[PlanResult]:
+        arr, nl = self._loads(loads)
+        self._ensure(nl)
+        out = (L.Plan * nl)()
+        ex = self.exec(lo=lo, hi=hi, resident=resident)
+        L.check(L.lib().camelot_plan_min_resource(C.byref(self.cprob), C.byref(self.ccl),
+                                                  arr.ctypes.data_as(C.POINTER(C.c_float)), nl,
+                                                  C.byref(ex), out))
+        return [_plan(o, self.n, self.A) for o in out]
+
+    def predict(self, batch: Sequence[int], replicas: Sequence[int], quota_pct: Sequence[int],
+                loads=None) -> PlanResult:
+        b = (C.c_int32 * L.MAX_APPS)(*batch)
+        r = (C.c_int32 * L.MAX_STAGES)(*replicas)
+        q = (C.c_int32 * L.MAX_STAGES)(*quota_pct)
+        out = L.Plan()
+        if loads is not None:
+            arr, nl = self._loads(loads)
+            lp, nl = arr.ctypes.data_as(C.POINTER(C.c_float)), 1
+        else:
+            lp, nl = None, 0
+        ex = self.exec()
+        L.check(L.lib().camelot_predict(C.byref(self.cprob), C.byref(self.ccl), b, r, q, lp, nl,
+                                        C.byref(ex), C.byref(out)))
+        return _plan(out, self.n, self.A)
+
+    def predict_index(self, x: int, loads=None) -> PlanResult:
+        """camelot_predict of the candidate with canonical index x (digits decoded here)."""
+        p = self.problem
+        nQ, nS, R = len(p.quota_pct), len(p.batch), int(p.max_replicas)
+        theta, rho = [0] * self.n, [0] * self.n
+        for i in range(self.n - 1, -1, -1):
+            theta[i] = x % nQ
+            x //= nQ
+            rho[i] = x % R
+            x //= R
+        beta = [0] * self.A
+        for a in range(self.A - 1, -1, -1):
+            beta[a] = x % nS
+            x //= nS
+        return self.predict([int(p.batch[b]) for b in beta], [r + 1 for r in rho],
+                            [int(p.quota_pct[t]) for t in theta], loads)
+
+    def score_range(self, lo: int, hi: int):
+        """Device vectors (verdict u8, T f32, u i32, U i32) of every candidate in [lo, hi)."""
+        m = hi - lo
+        dev = f"cuda:{self.device}"
+        v = torch.empty(m, dtype=torch.uint8, device=dev)
+        T = torch.empty(m, dtype=torch.float32, device=dev)
+        u = torch.empty(m, dtype=torch.int32, device=dev)
+        U = torch.empty(m, dtype=torch.int32, device=dev)
+        ex = self.exec()
+        L.check(L.lib().camelot_score_range(C.byref(self.cprob), C.byref(self.ccl), lo, hi, C.byref(ex),
+                                            v.data_ptr(), T.data_ptr(), u.data_ptr(), U.data_ptr()), False)
+        return v, T, u, U
+
+    def search_local(self, policy: int, loads=None, rank: int = 0, world: int = 1, lo: int = 0,
+                     hi: int = 0, resident: bool = False, keys: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """This rank's shard -> device int64 keys (sign-mapped; all_reduce MIN them)."""
+        if policy == L.POLICY_MIN_RESOURCE:
+            arr, nl = self._loads(loads)
+            lp = arr.ctypes.data_as(C.POINTER(C.c_float))
+            self._ensure(nl)
+        else:
+            lp, nl = None, 0
+        nk = max(1, nl)
+        if keys is None:
+            keys = torch.empty(nk, dtype=torch.int64, device=f"cuda:{self.device}")
+        ex = self.exec(rank=rank, world=world, lo=lo, hi=hi, resident=resident)
+        L.check(L.lib().camelot_search_local(C.byref(self.cprob), C.byref(self.ccl), policy, lp, nl,
+                                             C.byref(ex), keys.data_ptr()), False)
+        self._last_loads = (lp, nl, arr if policy else None)
+        return keys
+
+    def finalize(self, policy: int, keys: torch.Tensor, loads=None, rank: int = 0, world: int = 1,
+                 lo: int = 0, hi: int = 0) -> List[PlanResult]:
+        if policy == L.POLICY_MIN_RESOURCE:
+            arr, nl = self._loads(loads)
+            lp = arr.ctypes.data_as(C.POINTER(C.c_float))
+        else:
+            lp, nl = None, 0
+        nk = max(1, nl)
+        out = (L.Plan * nk)()
+        ex = self.exec(rank=rank, world=world, lo=lo, hi=hi)
+        L.check(L.lib().camelot_finalize(C.byref(self.cprob), C.byref(self.ccl), policy, lp, nl,
+                                         keys.data_ptr(), C.byref(ex), out))
+        return [_plan(o, self.n, self.A) for o in out]
+
+    def last_stats(self):
+        out = (C.c_uint64 * 6)()
+        ex = self.exec()
+        L.check(L.lib().camelot_last_stats(C.byref(ex), out), False)
+        return dict(n_scored=out[0], n_nodes=out[1], n_feasible=out[2], t_ns=out[3], items=out[4],
+                    inc_passes=out[5])
+
+
+# ---------------------------------------------------------------------- functional API
+def plan_max_load(problem, **kw) -> PlanResult:
+    return Session(problem, device=kw.pop("device", None)).plan_max_load(**kw)
+
+
+def plan_min_resource(problem, loads, **kw) -> List[PlanResult]:
+    s = Session(problem, device=kw.pop("device", None), n_loads=np.asarray(loads).reshape(-1, problem.n_apps).shape[0])
+    return s.plan_min_resource(loads, **kw)
+
+
+def predict(problem, batch, replicas, quota_pct, loads=None, device=None) -> PlanResult:
+    return Session(problem, device=device).predict(batch, replicas, quota_pct, loads)
+
+
+def plan_distributed(session: Session, policy: int, loads=None, group=None, lo: int = 0, hi: int = 0,
+                     resident: bool = False) -> List[PlanResult]:
+    """Multi-GPU plan: this rank searches chunks c = rank (mod world); ONE
+    all_reduce(MIN) of the packed int64 keys over the process group (NCCL over
+    NVLink); every rank then resolves and scores the winner locally."""
+    import torch.distributed as dist
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    keys = session.search_local(policy, loads, rank=rank, world=world, lo=lo, hi=hi, resident=resident)
+    if world > 1:
+        dist.all_reduce(keys, op=dist.ReduceOp.MIN, group=group)
+    return session.finalize(policy, keys, loads, rank=rank, world=world, lo=lo, hi=hi)
+
+
+# ---------------------------------------------------------------------- key helpers
+SIGN = 1 << 63
+
+
+def pack_key(objkey: int, low: int) -> int:
+    """Packed 64-bit key as camelot_search_local writes it: (objective key << 32 |
+    chunk-or-index), XOR 2^63 so that a signed int64 MIN equals the unsigned min
+    (include/camelot.h).  objkey 0xFFFFFFFF with low 0xFFFFFFFF = no candidate."""
+    u = ((objkey & 0xFFFFFFFF) << 32) | (low & 0xFFFFFFFF)
+    v = u ^ SIGN
+    return v - (1 << 64) if v >= SIGN else v
+
+
+def unpack_key(k: int):
+    u = (k + (1 << 64) if k < 0 else k) ^ SIGN
+    return u >> 32, u & 0xFFFFFFFF

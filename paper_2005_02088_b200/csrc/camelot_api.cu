@@ -1,0 +1,814 @@
+// camelot_api.cu -- host side of libcamelot.so: validation, workspace layout,
+// launches and the C ABI declared in include/camelot.h.  All compute runs in
+// the kernels of camelot_kernels.cuh / camelot_search.cuh; there is no CPU
+// fallback (no device -> CAMELOT_ENODEV).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <atomic>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/camelot.h"
+#include "camelot_kernels.cuh"
+
+using namespace cam;
+
+namespace {
+
+thread_local std::string g_err = "";
+std::atomic<unsigned long long> g_launches{0};
+thread_local unsigned long long t_call_launches = 0;
+// CUDA events around the main search kernel of the last call on this thread
+struct EvPair {
+    int dev = -1;
+    cudaEvent_t a = nullptr, b = nullptr;
+    bool armed = false;
+};
+thread_local EvPair t_ev;
+
+int fail(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define COUNT_LAUNCH()               \
+    do {                             \
+        g_launches.fetch_add(1);     \
+        ++t_call_launches;           \
+    } while (0)
+
+#define CU(call)                                                                              \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess) return fail(CAMELOT_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+    } while (0)
+
+constexpr int MAXSLOTS = 4096;      // persistent CTAs (>= 148 SMs x resident CTAs)
+constexpr int CHUNK_ITEMS = 64;
+
+size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct Layout {
+    size_t hdr, hdr2, tab, Q, S, rec, sb, item_off, lam, y, inc, result, keys, winner, rescan, plans, slots,
+        front0, front1, total;
+    int nlev;
+    unsigned long long fcap;   // frontier capacity (nodes) of each ping-pong buffer
+};
+
+struct Dims {
+    int A, n, nQ, nS, Rmax, C, O, nbc;
+    unsigned long long ntot;
+};
+
+int check_problem(const camelot_problem *p, const camelot_cluster *c, Dims &d) {
+    if (!p || !c) return fail(CAMELOT_EINVAL, "null problem or cluster");
+    if (p->n_apps < 1 || p->n_apps > CAMELOT_MAX_APPS) return fail(CAMELOT_EINVAL, "n_apps must be 1 or 2");
+    if (p->n_stages < 1 || p->n_stages > CAMELOT_MAX_STAGES) return fail(CAMELOT_EINVAL, "n_stages must be in 1..8");
+    if (c->n_gpus < 1) return fail(CAMELOT_EINVAL, "n_gpus < 1");
+    if (c->n_gpus > CAMELOT_MAX_GPUS) return fail(CAMELOT_ERANGE, "n_gpus > %d", CAMELOT_MAX_GPUS);
+    if (c->quota_per_gpu < 1 || c->quota_per_gpu > 127) return fail(CAMELOT_EINVAL, "quota_per_gpu must be in 1..127");
+    if (c->max_instances < 1) return fail(CAMELOT_EINVAL, "max_instances < 1");
+    if (!(c->bw_gbs > 0.0f) || !std::isfinite(c->bw_gbs)) return fail(CAMELOT_EINVAL, "bw_gbs must be > 0");
+    if (!(c->gflops > 0.0f) || !std::isfinite(c->gflops)) return fail(CAMELOT_EINVAL, "gflops must be > 0");
+    if (c->mem_mib < 1 || c->mem_mib >= (1u << 21)) return fail(CAMELOT_ERANGE, "mem_mib must be in 1..2^21-1");
+    if (p->max_replicas < 1 || p->max_replicas > CAMELOT_MAX_REPLICAS) return fail(CAMELOT_EINVAL, "max_replicas must be in 1..16");
+    if (p->n_quota < 1 || p->n_quota > CAMELOT_MAX_QUOTAS) return fail(CAMELOT_EINVAL, "n_quota must be in 1..128");
+    if (p->n_batch < 1 || p->n_batch > CAMELOT_MAX_BATCHES) return fail(CAMELOT_EINVAL, "n_batch must be in 1..64");
+    if (!p->app_of_stage || !p->qos_ms || !p->quota_pct || !p->batch || !p->table || !p->weights_mib ||
+        !p->act_mib_per_item || !p->gflop_per_item || !p->bw_sensitivity)
+        return fail(CAMELOT_EINVAL, "null array in problem");
+    for (int k = 0; k < p->n_quota; ++k) {
+        if (p->quota_pct[k] < 1 || p->quota_pct[k] > c->quota_per_gpu) return fail(CAMELOT_EINVAL, "quota_pct[%d] not in [1,R]", k);
+        if (k && p->quota_pct[k] <= p->quota_pct[k - 1]) return fail(CAMELOT_EINVAL, "quota grid not strictly ascending");
+    }
+    for (int k = 0; k < p->n_batch; ++k) {
+        if (p->batch[k] < 1) return fail(CAMELOT_EINVAL, "batch[%d] < 1", k);
+        if (k && p->batch[k] <= p->batch[k - 1]) return fail(CAMELOT_EINVAL, "batch grid not strictly ascending");
+    }
+    for (int i = 0; i < p->n_stages; ++i) {
+        const int a = p->app_of_stage[i];
+        if (a < 0 || a >= p->n_apps) return fail(CAMELOT_EINVAL, "app_of_stage[%d] out of range", i);
+        if (i && a < p->app_of_stage[i - 1]) return fail(CAMELOT_EINVAL, "app_of_stage not non-decreasing");
+        if (!(p->bw_sensitivity[i] >= 0.0f) || !std::isfinite(p->bw_sensitivity[i])) return fail(CAMELOT_EINVAL, "bw_sensitivity[%d] < 0", i);
+        if (!(p->gflop_per_item[i] >= 0.0f) || !std::isfinite(p->gflop_per_item[i])) return fail(CAMELOT_EINVAL, "gflop_per_item[%d] < 0", i);
+        const unsigned long long need = (unsigned long long)p->weights_mib[i] +
+            (unsigned long long)p->max_replicas * p->act_mib_per_item[i] * (unsigned long long)p->batch[p->n_batch - 1];
+        if (need >= (1ull << 31)) return fail(CAMELOT_ERANGE, "stage %d memory footprint overflows 2^31 MiB", i);
+    }
+    if (p->app_of_stage[0] != 0 || p->app_of_stage[p->n_stages - 1] != p->n_apps - 1)
+        return fail(CAMELOT_EINVAL, "every application needs at least one stage");
+    for (int a = 0; a < p->n_apps; ++a)
+        if (!(p->qos_ms[a] > 0.0f) || !std::isfinite(p->qos_ms[a])) return fail(CAMELOT_EINVAL, "qos_ms[%d] must be > 0", a);
+    const size_t ne = (size_t)p->n_stages * p->n_batch * p->n_quota;
+    for (size_t e = 0; e < ne; ++e) {
+        const float *t = p->table + 4 * e;
+        if (!std::isfinite(t[0]) || !std::isfinite(t[1]) || !std::isfinite(t[2]))
+            return fail(CAMELOT_EINVAL, "non-finite table entry %zu", e);
+        if (!(t[0] > 0.0f) || !(t[1] > 0.0f) || !(t[2] >= 0.0f))
+            return fail(CAMELOT_EINVAL, "table entry %zu: need dur > 0, thr > 0, bw >= 0", e);
+    }
+    if ((unsigned long long)p->max_replicas * p->n_stages * c->quota_per_gpu >= (1ull << 24))
+        return fail(CAMELOT_ERANGE, "quota sum exceeds the 24-bit key field");
+    d.A = p->n_apps;
+    d.n = p->n_stages;
+    d.nQ = p->n_quota;
+    d.nS = p->n_batch;
+    d.Rmax = p->max_replicas;
+    d.C = c->n_gpus;
+    d.O = d.Rmax * d.nQ;
+    d.nbc = 1;
+    for (int a = 0; a < d.A; ++a) d.nbc *= d.nS;
+    long double t = 1;
+    for (int a = 0; a < d.A; ++a) t *= d.nS;
+    for (int i = 0; i < d.n; ++i) t *= d.O;
+    if (t >= 9.2e18L) return fail(CAMELOT_ERANGE, "candidate space >= 2^63");
+    unsigned long long nt = 1;
+    for (int a = 0; a < d.A; ++a) nt *= (unsigned long long)d.nS;
+    for (int i = 0; i < d.n; ++i) nt *= (unsigned long long)d.O;
+    d.ntot = nt;
+    return CAMELOT_OK;
+}
+
+int check_loads(const camelot_problem *p, const float *loads, int n_loads) {
+    if (n_loads < 1 || n_loads > CAMELOT_MAX_LOADS) return fail(CAMELOT_EINVAL, "n_loads must be in 1..64");
+    if (!loads) return fail(CAMELOT_EINVAL, "null load_qps");
+    for (int k = 0; k < n_loads * p->n_apps; ++k)
+        if (!(loads[k] > 0.0f) || !std::isfinite(loads[k])) return fail(CAMELOT_EINVAL, "load_qps[%d] must be > 0", k);
+    return CAMELOT_OK;
+}
+
+Layout make_layout(const Dims &d, int nlev) {
+    Layout L;
+    L.nlev = nlev < 1 ? 1 : nlev;
+    size_t o = 0;
+    auto put = [&](size_t bytes) {
+        size_t at = o;
+        o += al(bytes);
+        return at;
+    };
+    L.hdr = put(sizeof(DevHeader));
+    L.hdr2 = put(sizeof(DevHeader));
+    L.tab = put((size_t)d.n * d.nS * d.nQ * sizeof(float4));
+    L.Q = put((size_t)d.nQ * sizeof(int));
+    L.S = put((size_t)d.nS * sizeof(int));
+    L.rec = put((size_t)d.n * d.nS * d.O * sizeof(OptRec));
+    L.sb = put((size_t)d.n * d.nS * sizeof(StageBound));
+    L.item_off = put((size_t)(d.nbc + 1) * sizeof(unsigned long long));
+    L.lam = put((size_t)CAMELOT_MAX_LOADS * CAMELOT_MAX_APPS * sizeof(float));
+    L.y = put((size_t)d.nbc * L.nlev * sizeof(int));
+    L.inc = put((size_t)L.nlev * sizeof(Slot));
+    L.result = put((size_t)L.nlev * sizeof(Slot));
+    L.keys = put((size_t)L.nlev * sizeof(long long));
+    L.winner = put((size_t)L.nlev * sizeof(Slot));
+    L.rescan = put((size_t)L.nlev * sizeof(unsigned long long));
+    L.plans = put((size_t)L.nlev * sizeof(camelot_plan));
+    L.slots = put((size_t)MAXSLOTS * L.nlev * sizeof(Slot));
+    // frontier of placement-state nodes: as many as there are leaf parents in the
+    // whole space, clamped to [256, 2^20] (overflow falls back to inline DFS)
+    const size_t nb = d.C > 8 ? sizeof(Node<16>) : sizeof(Node<8>);
+    long double parents = (long double)d.ntot / (long double)d.O;
+    L.fcap = (unsigned long long)std::max(256.0L, std::min((long double)(1u << 20), parents));
+    // testing knob: force a small frontier to exercise the inline-descent fallback
+    if (const char *cap = getenv("CAMELOT_FRONTIER_CAP")) {
+        const unsigned long long v = strtoull(cap, nullptr, 10);
+        if (v >= 1 && v < L.fcap) L.fcap = v;
+    }
+    L.front0 = put((size_t)L.fcap * nb);
+    L.front1 = put((size_t)L.fcap * nb);
+    L.total = o;
+    return L;
+}
+size_t slots_off(const Layout &L) { return L.slots; }
+
+int device_ok(const camelot_exec *ex) {
+    if (!ex) return fail(CAMELOT_EINVAL, "null exec");
+    int nd = 0;
+    cudaError_t e = cudaGetDeviceCount(&nd);
+    if (e != cudaSuccess || nd == 0) {
+        cudaGetLastError();
+        return fail(CAMELOT_ENODEV, "no CUDA device (there is no CPU fallback)");
+    }
+    if (ex->device < 0 || ex->device >= nd) return fail(CAMELOT_EINVAL, "bad device ordinal %d", ex->device);
+    CU(cudaSetDevice(ex->device));
+    if (ex->world < 1 || ex->rank < 0 || ex->rank >= ex->world) return fail(CAMELOT_EINVAL, "bad rank/world");
+    if (!ex->workspace) return fail(CAMELOT_EINVAL, "null workspace");
+    return CAMELOT_OK;
+}
+
+DevProb make_devprob(const camelot_problem *p, const camelot_cluster *c, const Dims &d, char *ws, const Layout &L) {
+    DevProb P;
+    memset(&P, 0, sizeof(P));
+    P.A = d.A;
+    P.n = d.n;
+    P.nQ = d.nQ;
+    P.nS = d.nS;
+    P.Rmax = d.Rmax;
+    P.C = d.C;
+    P.R = c->quota_per_gpu;
+    P.I = c->max_instances;
+    P.O = d.O;
+    P.nbc = d.nbc;
+    P.FM = c->mem_mib;
+    P.flags = p->flags;
+    P.BW = c->bw_gbs;
+    volatile float one = 1.0f;
+    P.invBW = one / c->bw_gbs;   // IEEE binary32 division, as the oracle
+    P.G = c->gflops;
+    for (int a = 0; a < d.A; ++a) {
+        P.qos[a] = p->qos_ms[a];
+        P.first_of_app[a] = -1;
+    }
+    for (int i = 0; i < d.n; ++i) {
+        const int a = p->app_of_stage[i];
+        P.app[i] = a;
+        if (P.first_of_app[a] < 0) P.first_of_app[a] = i;
+        P.last_of_app[a] = i;
+        P.W[i] = p->weights_mib[i];
+        P.Am[i] = p->act_mib_per_item[i];
+        P.gamma[i] = p->bw_sensitivity[i];
+        P.cflop[i] = p->gflop_per_item[i];
+    }
+    P.ntot = d.ntot;
+    P.opow[0] = 1;
+    for (int k = 1; k <= NMAX; ++k) P.opow[k] = P.opow[k - 1] * (unsigned long long)d.O;
+    P.tab = reinterpret_cast<const float4 *>(ws + L.tab);
+    P.Q = reinterpret_cast<const int *>(ws + L.Q);
+    P.S = reinterpret_cast<const int *>(ws + L.S);
+    return P;
+}
+
+struct Ctx {
+    Dims d;
+    Layout L;
+    DevProb P;
+    char *ws;
+    cudaStream_t st;
+    int nslots[2][2];   // [cm16][policy]
+    int d0;
+    int cm16;
+    bool naive;
+};
+
+template <int CM, int POL>
+size_t search_smem() {
+    return (size_t)SEARCH_WARPS * NMAX * sizeof(Node<CM>) + SEARCH_WARPS * sizeof(WarpCtl) +
+           SEARCH_WARPS * sizeof(WarpBest);
+}
+
+std::mutex g_attr_mu;
+int g_slots_cache[64][2][2];
+bool g_slots_ready[64][2][2];
+
+template <int CM, int POL>
+int grid_for(int dev, int &grid) {
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    const int ci = CM == 16 ? 1 : 0;
+    if (dev < 64 && g_slots_ready[dev][ci][POL]) {
+        grid = g_slots_cache[dev][ci][POL];
+        return CAMELOT_OK;
+    }
+    const size_t sm = search_smem<CM, POL>();
+    CU(cudaFuncSetAttribute(search_kernel<CM, POL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    int per = 0, nsm = 0;
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, search_kernel<CM, POL>, SEARCH_THREADS, sm));
+    CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    grid = std::max(1, std::min(MAXSLOTS, per * nsm));
+    if (dev < 64) {
+        g_slots_cache[dev][ci][POL] = grid;
+        g_slots_ready[dev][ci][POL] = true;
+    }
+    return CAMELOT_OK;
+}
+
+int choose_d0(const Dims &d) {
+    if (d.n < 2) return 0;   // single-stage problems: items are whole candidates (handled by flat path)
+    int d0 = 1;
+    long double items = (long double)d.nbc * d.O;
+    while (d0 < d.n - 1 && items < 16384.0L) {
+        ++d0;
+        items *= d.O;
+    }
+    return d0;
+}
+
+int setup(const camelot_problem *p, const camelot_cluster *c, const camelot_exec *ex, int nlev, Ctx &X, bool upload) {
+    int rc = check_problem(p, c, X.d);
+    if (rc) return rc;
+    rc = device_ok(ex);
+    if (rc) return rc;
+    X.L = make_layout(X.d, nlev);
+    if (ex->workspace_bytes < X.L.total)
+        return fail(CAMELOT_ENOMEM, "workspace too small: %zu < %zu bytes", ex->workspace_bytes, X.L.total);
+    X.ws = static_cast<char *>(ex->workspace);
+    X.st = static_cast<cudaStream_t>(ex->stream);
+    X.P = make_devprob(p, c, X.d, X.ws, X.L);
+    X.d0 = choose_d0(X.d);
+    X.cm16 = X.d.C > 8;
+    X.naive = (p->flags & F_PAPER_GLOBAL) || X.d.n < 2 || (ex->exec_flags & CAMELOT_EXEC_NAIVE);
+    if (upload && !(ex->exec_flags & CAMELOT_EXEC_RESIDENT)) {
+        CU(cudaMemcpyAsync(X.ws + X.L.tab, p->table, (size_t)X.d.n * X.d.nS * X.d.nQ * 16, cudaMemcpyHostToDevice, X.st));
+        CU(cudaMemcpyAsync(X.ws + X.L.Q, p->quota_pct, (size_t)X.d.nQ * 4, cudaMemcpyHostToDevice, X.st));
+        CU(cudaMemcpyAsync(X.ws + X.L.S, p->batch, (size_t)X.d.nS * 4, cudaMemcpyHostToDevice, X.st));
+    }
+    return CAMELOT_OK;
+}
+
+template <int CM, int POL>
+int launch_search(const Ctx &X, const SearchArgs &S, int grid) {
+    const size_t sm = search_smem<CM, POL>();
+    search_kernel<CM, POL><<<grid, SEARCH_THREADS, sm, X.st>>>(X.P, S);
+    COUNT_LAUNCH();
+    CU(cudaGetLastError());
+    return CAMELOT_OK;
+}
+
+int launch_search_any(const Ctx &X, int policy, const SearchArgs &S, int grid) {
+    if (X.cm16) return policy ? launch_search<16, 1>(X, S, grid) : launch_search<16, 0>(X, S, grid);
+    return policy ? launch_search<8, 1>(X, S, grid) : launch_search<8, 0>(X, S, grid);
+}
+
+int grid_any(const Ctx &X, int policy, int dev, int &grid) {
+    if (X.cm16) return policy ? grid_for<16, 1>(dev, grid) : grid_for<16, 0>(dev, grid);
+    return policy ? grid_for<8, 1>(dev, grid) : grid_for<8, 0>(dev, grid);
+}
+
+// One search pass: filter -> offsets -> search -> reduce.
+//   inc: device incumbents [nlev]; result: device [nlev]; keys: device [nlev]
+int flat_grid(int dev, int &grid) {
+    static int cache[64] = {0};
+    if (dev < 64 && cache[dev]) {
+        grid = cache[dev];
+        return CAMELOT_OK;
+    }
+    int per = 0, nsm = 0;
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, flat_search_kernel, FLAT_THREADS, 0));
+    CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    grid = std::max(1, std::min(MAXSLOTS, per * nsm));
+    if (dev < 64) cache[dev] = grid;
+    return CAMELOT_OK;
+}
+
+// naive pass: thread per candidate over [lo, hi) (chunks of 2^15 dealt round-robin to ranks)
+int flat_pass(const Ctx &X, int dev, int policy, int nlev, int ystride, int yoff, const float *lam, const Slot *inc,
+              Slot *result, long long *keys, int rank, int world, unsigned long long lo, unsigned long long hi) {
+    char *ws = X.ws;
+    DevHeader *hdr = reinterpret_cast<DevHeader *>(ws + X.L.hdr);
+    CU(cudaMemsetAsync(hdr, 0, sizeof(DevHeader), X.st));
+    int grid = 0;
+    int rc = flat_grid(dev, grid);
+    if (rc) return rc;
+    FlatArgs F;
+    F.policy = policy;
+    F.nlev = nlev;
+    F.rank = rank;
+    F.world = world;
+    F.lo = lo;
+    F.hi = hi;
+    F.lam = lam;
+    F.y = reinterpret_cast<const int *>(ws + X.L.y);
+    F.ystride = ystride;
+    F.yoff = yoff;
+    F.inc = inc;
+    F.slots = reinterpret_cast<Slot *>(ws + slots_off(X.L));
+    F.hdr = hdr;
+    flat_search_kernel<<<grid, FLAT_THREADS, 0, X.st>>>(X.P, F);
+    COUNT_LAUNCH();
+    CU(cudaGetLastError());
+    reduce_kernel<<<1, 256, 0, X.st>>>(X.P, F.slots, grid, nlev, result, keys, nullptr, nullptr, nullptr, 0, 1,
+                                       FLAT_SHIFT);
+    COUNT_LAUNCH();
+    CU(cudaGetLastError());
+    return CAMELOT_OK;
+}
+
+// the level-synchronous passes of one search (parents at depth 0..n-1)
+int run_passes(const Ctx &X, int dev, int policy, SearchArgs S, bool timed) {
+    char *ws = X.ws;
+    DevHeader *hdr = S.hdr;
+    int grid = 0;
+    int rc = grid_any(X, policy, dev, grid);
+    if (rc) return rc;
+    CU(cudaMemsetAsync(hdr->head, 0, sizeof(hdr->head) + sizeof(hdr->tail), X.st));
+    if (timed) {
+        if (t_ev.dev != dev) {
+            if (t_ev.a) {
+                cudaEventDestroy(t_ev.a);
+                cudaEventDestroy(t_ev.b);
+            }
+            CU(cudaEventCreate(&t_ev.a));
+            CU(cudaEventCreate(&t_ev.b));
+            t_ev.dev = dev;
+        }
+        CU(cudaEventRecord(t_ev.a, X.st));
+    }
+    init_slots_kernel<<<(grid * S.nlev + 255) / 256, 256, 0, X.st>>>(S.slots, grid * S.nlev);
+    COUNT_LAUNCH();
+    CU(cudaGetLastError());
+    void *buf[2] = {ws + X.L.front0, ws + X.L.front1};
+    const int n = X.d.n;
+    for (int j = 0; j < n; ++j) {
+        S.level = j;
+        S.flevel = (j + 1 <= n - 1) ? j + 1 : -1;
+        S.in_nodes = j == 0 ? nullptr : buf[j & 1];
+        S.in_count = &hdr->tail[j];
+        S.in_cap = X.L.fcap;
+        S.out_nodes = buf[(j + 1) & 1];
+        S.out_tail = &hdr->tail[j + 1];
+        S.out_cap = X.L.fcap;
+        S.head = &hdr->head[j];
+        S.grab = 1;
+        rc = launch_search_any(X, policy, S, grid);
+        if (rc) return rc;
+    }
+    if (timed) {
+        CU(cudaEventRecord(t_ev.b, X.st));
+        t_ev.armed = true;
+    }
+    return CAMELOT_OK;
+}
+
+int search_pass(const Ctx &X, int dev, int policy, int nlev, bool prune, int stride, const Slot *inc,
+                Slot *result, long long *keys, int rank, int world, unsigned long long lo, unsigned long long hi,
+                bool timed) {
+    char *ws = X.ws;
+    if (X.naive)
+        return flat_pass(X, dev, policy, nlev, nlev, 0, reinterpret_cast<const float *>(ws + X.L.lam), inc, result,
+                         keys, rank, world, lo, hi);
+    DevHeader *hdr = reinterpret_cast<DevHeader *>(ws + X.L.hdr);
+    CU(cudaMemsetAsync(hdr, 0, sizeof(DevHeader), X.st));
+    CU(cudaMemsetAsync(&hdr->best_obj, 0xFF, sizeof(unsigned int), X.st));
+    FilterArgs F;
+    F.policy = policy;
+    F.prune = prune;
+    F.stride = stride;
+    F.nlev = nlev;
+    F.inc = inc;
+    F.lam = reinterpret_cast<const float *>(ws + X.L.lam);
+    F.rec = reinterpret_cast<OptRec *>(ws + X.L.rec);
+    F.sb = reinterpret_cast<StageBound *>(ws + X.L.sb);
+    filter_kernel<<<X.d.nS, FILTER_THREADS, 0, X.st>>>(X.P, F);
+    COUNT_LAUNCH();
+    CU(cudaGetLastError());
+    offsets_kernel<<<1, 32, 0, X.st>>>(X.P, F.sb, X.d0, reinterpret_cast<unsigned long long *>(ws + X.L.item_off), hdr);
+    COUNT_LAUNCH();
+    CU(cudaGetLastError());
+    SearchArgs S;
+    memset(&S, 0, sizeof(S));
+    S.policy = policy;
+    S.nlev = nlev;
+    S.d0 = X.d0;
+    S.chunk_items = CHUNK_ITEMS;
+    S.rank = rank;
+    S.world = world;
+    S.prune = prune;
+    S.lo = lo;
+    S.hi = hi;
+    S.rec = F.rec;
+    S.sb = F.sb;
+    S.item_off = reinterpret_cast<const unsigned long long *>(ws + X.L.item_off);
+    S.lam = F.lam;
+    S.y = reinterpret_cast<const int *>(ws + X.L.y);
+    S.ystride = nlev;
+    S.yoff = 0;
+    S.inc = inc;
+    S.hdr = hdr;
+    S.slots = reinterpret_cast<Slot *>(ws + slots_off(X.L));
+    int rc = run_passes(X, dev, policy, S, timed);
+    if (rc) return rc;
+    int grid = 0;
+    rc = grid_any(X, policy, dev, grid);
+    if (rc) return rc;
+    reduce_kernel<<<1, 256, 0, X.st>>>(X.P, S.slots, grid, nlev, result, keys, S.sb, S.rec, S.item_off, X.d0,
+                                       CHUNK_ITEMS, -1);
+    COUNT_LAUNCH();
+    CU(cudaGetLastError());
+    return CAMELOT_OK;
+}
+
+// re-scan chunk `chunk` for level k after the cross-rank reduction (same filter state)
+int rescan_pass(const Ctx &X, int dev, int policy, int nlev, bool prune, int k, Slot *winner_k,
+                const unsigned long long chunk, unsigned long long lo, unsigned long long hi) {
+    char *ws = X.ws;
+    if (X.naive) {
+        const unsigned long long a0 = std::max(lo, chunk << FLAT_SHIFT);
+        const unsigned long long b0 = std::min(hi, (chunk + 1) << FLAT_SHIFT);
+        long long *dummy = reinterpret_cast<long long *>(ws + X.L.keys) + k;
+        return flat_pass(X, dev, policy, 1, nlev, k, reinterpret_cast<const float *>(ws + X.L.lam) + k * X.d.A,
+                         winner_k, winner_k, dummy, 0, 1, a0, b0);
+    }
+    DevHeader *hdr = reinterpret_cast<DevHeader *>(ws + X.L.hdr);
+    SearchArgs S;
+    memset(&S, 0, sizeof(S));
+    S.policy = policy;
+    S.nlev = 1;
+    S.d0 = X.d0;
+    S.chunk_items = CHUNK_ITEMS;
+    S.rank = 0;
+    S.world = 1;
+    S.prune = prune;
+    S.lo = lo;
+    S.hi = hi;
+    S.rec = reinterpret_cast<const OptRec *>(ws + X.L.rec);
+    S.sb = reinterpret_cast<const StageBound *>(ws + X.L.sb);
+    S.item_off = reinterpret_cast<const unsigned long long *>(ws + X.L.item_off);
+    S.lam = reinterpret_cast<const float *>(ws + X.L.lam) + k * X.d.A;
+    S.y = reinterpret_cast<const int *>(ws + X.L.y);
+    S.ystride = nlev;
+    S.yoff = k;
+    S.inc = winner_k;
+    S.hdr = hdr;
+    S.slots = reinterpret_cast<Slot *>(ws + slots_off(X.L));
+    S.chunk_lo = chunk;
+    S.chunk_hi = chunk + 1;
+    CU(cudaMemsetAsync(&hdr->best_obj, 0xFF, sizeof(unsigned int), X.st));
+    int rc = run_passes(X, dev, policy, S, false);
+    if (rc) return rc;
+    int grid = 0;
+    rc = grid_any(X, policy, dev, grid);
+    if (rc) return rc;
+    long long *dummy = reinterpret_cast<long long *>(ws + X.L.keys) + k;
+    reduce_kernel<<<1, 256, 0, X.st>>>(X.P, S.slots, grid, 1, winner_k, dummy, S.sb, S.rec, S.item_off, X.d0,
+                                       CHUNK_ITEMS, -1);
+    COUNT_LAUNCH();
+    CU(cudaGetLastError());
+    return CAMELOT_OK;
+}
+
+void range_of(const Ctx &X, const camelot_exec *ex, unsigned long long &lo, unsigned long long &hi) {
+    lo = ex->index_lo;
+    hi = ex->index_hi;
+    if (lo == 0 && hi == 0) hi = X.d.ntot;
+    if (hi > X.d.ntot) hi = X.d.ntot;
+    if (lo > hi) lo = hi;
+}
+
+bool use_coarse(const Ctx &X, bool prune) { return prune && !X.naive && X.d.nQ >= 20 && X.d.ntot > 4000000ull; }
+int coarse_stride(const Ctx &X) { return std::max(2, X.d.nQ / 10); }
+
+// local search (incumbent pass + main pass); leaves keys in X.L.keys (or d_keys) and the
+// exact local best in X.L.result
+int local_search(const Ctx &X, const camelot_exec *ex, int policy, int nlev, long long *d_keys) {
+    const bool prune = !(X.P.flags & F_NO_FILTER);
+    char *ws = X.ws;
+    Slot *inc = reinterpret_cast<Slot *>(ws + X.L.inc);
+    Slot *result = reinterpret_cast<Slot *>(ws + X.L.result);
+    long long *keys = d_keys ? d_keys : reinterpret_cast<long long *>(ws + X.L.keys);
+    // incumbent = none: key 0xFFFFFFFF, x = ~0
+    init_slots_kernel<<<1, 64, 0, X.st>>>(inc, nlev);
+    COUNT_LAUNCH();
+    CU(cudaGetLastError());
+    if (policy == 1) {
+        const int nb = X.d.nbc * nlev;
+        eq2_kernel<<<(nb + 127) / 128, 128, 0, X.st>>>(X.P, reinterpret_cast<const float *>(ws + X.L.lam), nlev,
+                                                      reinterpret_cast<int *>(ws + X.L.y));
+        COUNT_LAUNCH();
+        CU(cudaGetLastError());
+    }
+    unsigned long long lo, hi;
+    range_of(X, ex, lo, hi);
+    int dev = ex->device;
+    int rc;
+    if (use_coarse(X, prune)) {
+        // incumbent: exact optimum of the coarse quota sub-grid (replicated on every rank)
+        rc = search_pass(X, dev, policy, nlev, true, coarse_stride(X), inc, result,
+                         reinterpret_cast<long long *>(ws + X.L.keys), 0, 1, lo, hi, false);
+        if (rc) return rc;
+        CU(cudaMemcpyAsync(inc, result, nlev * sizeof(Slot), cudaMemcpyDeviceToDevice, X.st));
+    }
+    rc = search_pass(X, dev, policy, nlev, prune, 1, inc, result, keys, ex->rank, ex->world, lo, hi, true);
+    if (rc) return rc;
+    CU(cudaMemcpyAsync(ws + X.L.hdr2, ws + X.L.hdr, sizeof(DevHeader), cudaMemcpyDeviceToDevice, X.st));
+    return CAMELOT_OK;
+}
+
+int finalize_impl(const Ctx &X, const camelot_exec *ex, int policy, int nlev, const long long *d_keys,
+                  camelot_plan *out) {
+    const bool prune = !(X.P.flags & F_NO_FILTER);
+    char *ws = X.ws;
+    Slot *winner = reinterpret_cast<Slot *>(ws + X.L.winner);
+    unsigned long long *rescan = reinterpret_cast<unsigned long long *>(ws + X.L.rescan);
+    FinalArgs F;
+    F.policy = policy;
+    F.nlev = nlev;
+    F.world = ex->world;
+    F.keys = d_keys;
+    F.local = reinterpret_cast<const Slot *>(ws + X.L.result);
+    F.winner = winner;
+    F.rescan = rescan;
+    resolve_kernel<<<1, 64, 0, X.st>>>(X.P, F);
+    COUNT_LAUNCH();
+    CU(cudaGetLastError());
+    if (ex->world > 1 && X.d.ntot > (1ull << 32)) {
+        std::vector<unsigned long long> rs(nlev);
+        CU(cudaMemcpyAsync(rs.data(), rescan, nlev * sizeof(unsigned long long), cudaMemcpyDeviceToHost, X.st));
+        CU(cudaStreamSynchronize(X.st));
+        unsigned long long lo, hi;
+        range_of(X, ex, lo, hi);
+        for (int k = 0; k < nlev; ++k) {
+            if (rs[k] == ~0ull) continue;
+            int rc = rescan_pass(X, ex->device, policy, nlev, prune, k, winner + k, rs[k], lo, hi);
+            if (rc) return rc;
+        }
+    }
+    camelot_plan *dplans = reinterpret_cast<camelot_plan *>(ws + X.L.plans);
+    plan_kernel<<<(nlev + 63) / 64, 64, 0, X.st>>>(X.P, policy, nlev, winner, reinterpret_cast<const float *>(ws + X.L.lam),
+                                                   reinterpret_cast<const DevHeader *>(ws + X.L.hdr2), dplans);
+    COUNT_LAUNCH();
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(out, dplans, nlev * sizeof(camelot_plan), cudaMemcpyDeviceToHost, X.st));
+    CU(cudaStreamSynchronize(X.st));
+    unsigned long long lo, hi;
+    range_of(X, ex, lo, hi);
+    bool any = false;
+    for (int k = 0; k < nlev; ++k) {
+        out[k].n_covered = hi - lo;
+        any |= out[k].status == CAMELOT_OK;
+    }
+    return any ? CAMELOT_OK : CAMELOT_INFEASIBLE;
+}
+
+int upload_loads(const Ctx &X, const float *loads, int n_loads) {
+    if (n_loads <= 0) return CAMELOT_OK;
+    CU(cudaMemcpyAsync(X.ws + X.L.lam, loads, (size_t)n_loads * X.d.A * sizeof(float), cudaMemcpyHostToDevice, X.st));
+    return CAMELOT_OK;
+}
+
+}  // namespace
+
+// ============================================================================ C ABI
+extern "C" {
+
+const char *camelot_last_error(void) { return g_err.c_str(); }
+const char *camelot_version(void) { return "camelot-b200 0.1 (sm_100a)"; }
+
+size_t camelot_workspace_bytes(const camelot_problem *p, const camelot_cluster *c, int n_loads) {
+    Dims d;
+    if (check_problem(p, c, d)) return 0;
+    if (n_loads < 0 || n_loads > CAMELOT_MAX_LOADS) {
+        fail(CAMELOT_EINVAL, "n_loads must be in 0..64");
+        return 0;
+    }
+    return make_layout(d, n_loads).total;
+}
+
+int camelot_upload(const camelot_problem *p, const camelot_cluster *c, const camelot_exec *ex) {
+    t_call_launches = 0;
+    Ctx X;
+    camelot_exec e2 = ex ? *ex : camelot_exec{};
+    e2.exec_flags &= ~CAMELOT_EXEC_RESIDENT;
+    return setup(p, c, &e2, 1, X, true);
+}
+
+int camelot_search_local(const camelot_problem *p, const camelot_cluster *c, int policy, const float *load_qps,
+                         int n_loads, const camelot_exec *ex, int64_t *d_keys) {
+    t_call_launches = 0;
+    if (policy != 0 && policy != 1) return fail(CAMELOT_EINVAL, "bad policy");
+    const int nlev = policy == 0 ? 1 : n_loads;
+    if (policy == 1) {
+        int rc = p ? check_loads(p, load_qps, n_loads) : fail(CAMELOT_EINVAL, "null problem");
+        if (rc) return rc;
+    }
+    Ctx X;
+    int rc = setup(p, c, ex, nlev, X, true);
+    if (rc) return rc;
+    rc = upload_loads(X, load_qps, policy == 1 ? n_loads : 0);
+    if (rc) return rc;
+    return local_search(X, ex, policy, nlev, reinterpret_cast<long long *>(d_keys));
+}
+
+int camelot_finalize(const camelot_problem *p, const camelot_cluster *c, int policy, const float *load_qps,
+                     int n_loads, const int64_t *d_keys, const camelot_exec *ex, camelot_plan *out) {
+    t_call_launches = 0;
+    if (policy != 0 && policy != 1) return fail(CAMELOT_EINVAL, "bad policy");
+    if (!out || !d_keys) return fail(CAMELOT_EINVAL, "null out or keys");
+    const int nlev = policy == 0 ? 1 : n_loads;
+    Ctx X;
+    int rc = setup(p, c, ex, nlev, X, false);
+    if (rc) return rc;
+    return finalize_impl(X, ex, policy, nlev, reinterpret_cast<const long long *>(d_keys), out);
+}
+
+int camelot_plan_max_load(const camelot_problem *p, const camelot_cluster *c, const camelot_exec *ex,
+                          camelot_plan *out) {
+    t_call_launches = 0;
+    if (!out) return fail(CAMELOT_EINVAL, "null out");
+    if (ex && ex->world != 1) return fail(CAMELOT_EINVAL, "plan_* is single-process: use search_local + finalize for world > 1");
+    Ctx X;
+    int rc = setup(p, c, ex, 1, X, true);
+    if (rc) return rc;
+    rc = local_search(X, ex, 0, 1, nullptr);
+    if (rc) return rc;
+    return finalize_impl(X, ex, 0, 1, reinterpret_cast<const long long *>(X.ws + X.L.keys), out);
+}
+
+int camelot_plan_min_resource(const camelot_problem *p, const camelot_cluster *c, const float *load_qps, int n_loads,
+                              const camelot_exec *ex, camelot_plan *out) {
+    t_call_launches = 0;
+    if (!out) return fail(CAMELOT_EINVAL, "null out");
+    if (ex && ex->world != 1) return fail(CAMELOT_EINVAL, "plan_* is single-process: use search_local + finalize for world > 1");
+    int rc = p ? check_loads(p, load_qps, n_loads) : fail(CAMELOT_EINVAL, "null problem");
+    if (rc) return rc;
+    Ctx X;
+    rc = setup(p, c, ex, n_loads, X, true);
+    if (rc) return rc;
+    rc = upload_loads(X, load_qps, n_loads);
+    if (rc) return rc;
+    rc = local_search(X, ex, 1, n_loads, nullptr);
+    if (rc) return rc;
+    return finalize_impl(X, ex, 1, n_loads, reinterpret_cast<const long long *>(X.ws + X.L.keys), out);
+}
+
+int camelot_predict(const camelot_problem *p, const camelot_cluster *c, const int32_t *batch, const int32_t *replicas,
+                    const int32_t *quota_pct, const float *load_qps, int n_loads, const camelot_exec *ex,
+                    camelot_plan *out) {
+    t_call_launches = 0;
+    if (!out || !batch || !replicas || !quota_pct) return fail(CAMELOT_EINVAL, "null argument");
+    Ctx X;
+    int rc = setup(p, c, ex, 1, X, true);
+    if (rc) return rc;
+    if (n_loads > 0) {
+        rc = check_loads(p, load_qps, 1);
+        if (rc) return rc;
+        rc = upload_loads(X, load_qps, 1);
+        if (rc) return rc;
+    }
+    unsigned long long x = 0;
+    for (int a = 0; a < X.d.A; ++a) {
+        int b = -1;
+        for (int k = 0; k < X.d.nS; ++k)
+            if (p->batch[k] == batch[a]) b = k;
+        if (b < 0) return fail(CAMELOT_EINVAL, "batch %d of app %d is not on the batch grid", batch[a], a);
+        x = x * X.d.nS + b;
+    }
+    for (int i = 0; i < X.d.n; ++i) {
+        if (replicas[i] < 1 || replicas[i] > X.d.Rmax) return fail(CAMELOT_EINVAL, "replicas[%d] not in 1..Rmax", i);
+        int t = -1;
+        for (int k = 0; k < X.d.nQ; ++k)
+            if (p->quota_pct[k] == quota_pct[i]) t = k;
+        if (t < 0) return fail(CAMELOT_EINVAL, "quota %d of stage %d is not on the quota grid", quota_pct[i], i);
+        x = x * X.d.Rmax + (replicas[i] - 1);
+        x = x * X.d.nQ + t;
+    }
+    camelot_plan *dplans = reinterpret_cast<camelot_plan *>(X.ws + X.L.plans);
+    predict_kernel<<<1, 1, 0, X.st>>>(X.P, x, n_loads > 0 ? reinterpret_cast<const float *>(X.ws + X.L.lam) : nullptr,
+                                      n_loads > 0 ? 1 : 0, dplans);
+    COUNT_LAUNCH();
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(out, dplans, sizeof(camelot_plan), cudaMemcpyDeviceToHost, X.st));
+    CU(cudaStreamSynchronize(X.st));
+    return out->status;
+}
+
+int camelot_score_range(const camelot_problem *p, const camelot_cluster *c, uint64_t lo, uint64_t hi,
+                        const camelot_exec *ex, uint8_t *d_verdict, float *d_T, int32_t *d_u, int32_t *d_U) {
+    t_call_launches = 0;
+    Ctx X;
+    int rc = setup(p, c, ex, 1, X, true);
+    if (rc) return rc;
+    if (hi > X.d.ntot) hi = X.d.ntot;
+    if (lo > hi) return fail(CAMELOT_EINVAL, "lo > hi");
+    const unsigned long long cnt = hi - lo;
+    if (cnt > (1ull << 31)) return fail(CAMELOT_ERANGE, "range longer than 2^31");
+    if (cnt == 0) return CAMELOT_OK;
+    const unsigned blocks = (unsigned)((cnt + 255) / 256);
+    score_range_kernel<<<blocks, 256, 0, X.st>>>(X.P, lo, cnt, d_verdict, d_T, d_u, d_U);
+    COUNT_LAUNCH();
+    CU(cudaGetLastError());
+    return CAMELOT_OK;
+}
+
+uint64_t camelot_kernel_launches(void) { return g_launches.load(); }
+
+int camelot_last_stats(const camelot_exec *ex, uint64_t *out6) {
+    if (!ex || !out6 || !ex->workspace) return fail(CAMELOT_EINVAL, "null argument");
+    float ms = 0.0f;
+    if (t_ev.armed) {
+        CU(cudaEventSynchronize(t_ev.b));
+        CU(cudaEventElapsedTime(&ms, t_ev.a, t_ev.b));
+    }
+    // the saved header sits right after the live one (layout is problem independent here)
+    DevHeader h;
+    cudaStream_t st = static_cast<cudaStream_t>(ex->stream);
+    CU(cudaMemcpyAsync(&h, static_cast<char *>(ex->workspace) + al(sizeof(DevHeader)), sizeof(h), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    out6[0] = h.n_scored;
+    out6[1] = h.n_nodes;
+    out6[2] = h.n_feasible;
+    out6[3] = (uint64_t)((double)ms * 1e6);
+    out6[4] = h.items_total;
+    out6[5] = t_call_launches;
+    return CAMELOT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,110 @@
+// camelot_device.cuh -- device-side data structures and the scoring arithmetic
+// of the allocation search (sm_100a).  Everything here follows DESIGN.md
+// "Scoring definition" (placement PAPER.md L929-945; constraints Eq. 1 / Eq. 3
+// L825-836, L859-869; contention reading R17).  Floating point uses explicit
+// round-to-nearest intrinsics so that no FMA contraction can happen.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace cam {
+
+constexpr int NMAX = 8;      // stages
+constexpr int AMAX = 2;      // applications
+constexpr int LMAX = 64;     // load levels
+
+constexpr uint32_t F_NO_BW_CAP = 1u, F_NO_CONTENTION = 2u, F_SAT = 4u, F_PAPER_GLOBAL = 8u,
+                   F_EQ2_BUDGET = 16u, F_NO_FILTER = 32u;
+constexpr uint32_t V_QUOTA = 1u, V_INST = 2u, V_MEM = 4u, V_BW = 8u, V_QOS = 16u,
+                   V_LOAD = 32u, V_EQ2 = 64u;
+
+// Problem image passed BY VALUE to every kernel (lives in the constant bank).
+struct DevProb {
+    int A, n, nQ, nS, Rmax, C, R, I, O, nbc;   // O = Rmax*nQ options per stage, nbc = nS^A
+    uint32_t FM, flags;
+    float BW, invBW, G;
+    float qos[AMAX];
+    int app[NMAX];
+    int first_of_app[AMAX], last_of_app[AMAX];
+    uint32_t W[NMAX], Am[NMAX];
+    float gamma[NMAX], cflop[NMAX];
+    unsigned long long ntot;
+    unsigned long long opow[NMAX + 1];       // O^k
+    const float4 *tab;                       // [n][nS][nQ] (dur, thr, bw, 0)
+    const int *Q, *S;                        // grids
+};
+
+// One option (N, theta) of stage i at batch index b, precomputed by the filter kernel.
+struct __align__(16) OptRec {
+    uint32_t code;     // option code o = rho*nQ + theta
+    uint32_t NP;       // N * p
+    uint32_t N;        // replicas
+    uint32_t MEM;      // W_i + N*A_i*s  (MiB)
+    float NB;          // fl(N * bw)
+    float NT;          // fl(N * thr)
+    float bw;          // bw of one replica
+    float dur;         // duration (ms)
+    uint32_t p;        // quota (%)
+    uint32_t pmul;     // ceil(2^16 / p): floor(a/p) = (a*pmul)>>16 for a <= 127
+    uint32_t As;       // A_i * s
+    uint32_t W;        // W_i
+};
+
+// Per (stage, batch) bounds over the surviving options.
+struct __align__(16) StageBound {
+    float mindur;      // min duration over surviving options
+    float maxNT;       // max fl(N*thr) over surviving options
+    uint32_t minNP;    // min N*p over surviving options
+    uint32_t cnt;      // surviving options
+};
+
+// Device header at the start of the workspace.
+struct DevHeader {
+    unsigned long long chunk_counter;
+    unsigned long long n_scored, n_feasible, n_nodes;
+    unsigned int best_obj;          // dynamic incumbent objective key (32-bit, smaller better)
+    unsigned int viol_or;
+    unsigned int done_ctas;
+    unsigned int overflow;
+    unsigned long long items_total; // number of depth-d0 items of the (filtered) space
+    unsigned long long nchunks;
+    unsigned long long t_search_ns;
+    unsigned int inc_passes;
+    unsigned int pad[7];
+    unsigned long long head[NMAX + 1];   // pop counter of pass j
+    unsigned long long tail[NMAX + 1];   // size of the frontier at depth j (may exceed capacity)
+};
+
+struct Slot {                      // (objective key, canonical index), smaller is better
+    unsigned long long key, x;
+};
+
+__device__ __forceinline__ bool slot_less(unsigned long long ka, unsigned long long xa,
+                                          unsigned long long kb, unsigned long long xb) {
+    return ka < kb || (ka == kb && xa < xb);
+}
+
+__device__ __forceinline__ unsigned int objkey_maxload(float T) {
+    return 0xFFFFFFFFu - __float_as_uint(T);
+}
+__device__ __forceinline__ unsigned int objkey_minres(int u, int U) {
+    return ((unsigned)u << 24) | (unsigned)U;
+}
+
+// contention inflation for a stage with one-replica bandwidth bw, sensitivity
+// gamma, on GPUs whose largest accumulated demand is dmax (reading R17; the max
+// over hosting GPUs of a monotone function = the function of the max demand).
+__device__ __forceinline__ float kappa_of(float dmax, float bw, float gamma, float invBW, uint32_t flags) {
+    if (flags & F_NO_CONTENTION) return 1.0f;
+    float d = __fsub_rn(dmax, bw);
+    float t = __fmul_rn(d, invBW);
+    float t2 = __fmul_rn(gamma, t);
+    float k = __fadd_rn(1.0f, t2);
+    if (flags & F_SAT) {
+        float r = __fmul_rn(dmax, invBW);
+        if (r > 1.0f) k = __fmul_rn(k, r);
+    }
+    return k;
+}
+
+}  // namespace cam

@@ -1,0 +1,535 @@
+// camelot_kernels.cuh -- the small kernels around the search (sm_100a):
+//   filter_kernel   (N3) per (batch, stage) option filtering + compaction,
+//   offsets_kernel       item-space prefix offsets per batch combo,
+//   eq2_kernel           Eq. 2 GPU-count estimate per (batch combo, load level),
+//   reduce_kernel        per-CTA slots -> rank-local best + packed 64-bit keys,
+//   finalize_kernel (N4/N5) keys -> exact index (chunk rescan result) -> plan,
+//   score_range_kernel   (N5) one thread per candidate, full recompute.
+#pragma once
+#include "../../include/camelot.h"
+#include "camelot_device.cuh"
+#include "camelot_score.cuh"
+#include "camelot_search.cuh"
+
+namespace cam {
+
+constexpr int FILTER_THREADS = 256;
+constexpr int OMAX = 16 * 128;   // Rmax * nQ upper bound
+
+struct FilterArgs {
+    int policy, prune, stride, nlev;
+    const Slot *inc;       // [nlev] incumbent (may be all-none)
+    const float *lam;      // [nlev][A]
+    OptRec *rec;           // [n][nS][O]
+    StageBound *sb;        // [n][nS]
+};
+
+// One CTA per batch index b: filters the options of every stage at batch b.
+// An option survives unless it provably cannot be part of a feasible
+// candidate at least as good as the incumbent.
+__global__ void __launch_bounds__(FILTER_THREADS) filter_kernel(const DevProb P, const FilterArgs F) {
+    __shared__ unsigned char keep[NMAX][OMAX];
+    __shared__ float mindur[NMAX];
+    __shared__ int minNP[NMAX];
+    const int b = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int n = P.n, O = P.O, nQ = P.nQ;
+    const bool cap = !(P.flags & F_NO_BW_CAP);
+    // incumbent
+    unsigned long long ikey = 0xFFFFFFFFull;
+    for (int k = 0; k < F.nlev; ++k) ikey = (k == 0) ? F.inc[k].key : max(ikey, F.inc[k].key);
+    const bool has_inc = ikey < 0xFFFFFFFFull;
+    const float Tinc = has_inc ? __uint_as_float(0xFFFFFFFFu - (unsigned)ikey) : 0.0f;
+    const int uinc = (int)(ikey >> 24), Uinc = (int)(ikey & 0xFFFFFFu);
+    float lam_min[AMAX] = {0.0f, 0.0f};
+    if (F.policy == 1)
+        for (int a = 0; a < P.A; ++a) {
+            float m = F.lam[a];
+            for (int k = 1; k < F.nlev; ++k) m = fminf(m, F.lam[k * P.A + a]);
+            lam_min[a] = m;
+        }
+    // static conditions
+    for (int idx = tid; idx < n * O; idx += blockDim.x) {
+        const int i = idx / O, o = idx % O;
+        const int th = o % nQ, N = o / nQ + 1;
+        const float4 e = P.tab[((size_t)i * P.nS + b) * nQ + th];
+        const uint32_t As = P.Am[i] * (uint32_t)P.S[b];
+        bool k = true;
+        if (F.stride > 1 && ((nQ - 1 - th) % F.stride) != 0) k = false;
+        if (F.prune) {
+            if (P.W[i] + As > P.FM) k = false;                 // one replica fits no GPU
+            if (cap && e.z > P.BW) k = false;
+            if (N > P.C * P.I) k = false;
+            const float NT = __fmul_rn((float)N, e.y);
+            if (F.policy == 0 && has_inc && NT < Tinc) k = false;   // T <= fl(N thr) < T_inc
+            if (F.policy == 1 && NT < lam_min[P.app[i]]) k = false; // load floor at every level
+        }
+        keep[i][o] = k;
+    }
+    __syncthreads();
+    const int rounds = F.prune ? 3 : 0;
+    for (int it = 0; it <= rounds; ++it) {
+        // per-stage minima over surviving options (warp w: stage w)
+        for (int i = wid; i < n; i += FILTER_THREADS / 32) {
+            float md = __int_as_float(0x7f800000);
+            int mn = 0x7fffffff;
+            for (int o = lane; o < O; o += 32)
+                if (keep[i][o]) {
+                    const int th = o % nQ, N = o / nQ + 1;
+                    md = fminf(md, P.tab[((size_t)i * P.nS + b) * nQ + th].x);
+                    mn = min(mn, N * P.Q[th]);
+                }
+            for (int off = 16; off; off >>= 1) {
+                md = fminf(md, __shfl_xor_sync(0xffffffffu, md, off));
+                mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, off));
+            }
+            if (lane == 0) {
+                mindur[i] = md;
+                minNP[i] = mn;
+            }
+        }
+        __syncthreads();
+        if (it == rounds) break;
+        for (int idx = tid; idx < n * O; idx += blockDim.x) {
+            const int i = idx / O, o = idx % O;
+            if (!keep[i][o]) continue;
+            const int th = o % nQ, N = o / nQ + 1;
+            const int a = P.app[i];
+            const float dur = P.tab[((size_t)i * P.nS + b) * nQ + th].x;
+            // QoS: ordered fp32 sum with this option's duration and the others' minima
+            float ls = 0.0f;
+            for (int k2 = P.first_of_app[a]; k2 <= P.last_of_app[a]; ++k2) {
+                const float t = (k2 == i) ? dur : mindur[k2];
+                ls = (k2 == P.first_of_app[a]) ? t : __fadd_rn(ls, t);
+            }
+            bool k = ls <= P.qos[a];
+            // quota: N p + sum of the other stages' minimal N p  <=  C R
+            long long U = (long long)N * P.Q[th];
+            for (int k2 = 0; k2 < n; ++k2)
+                if (k2 != i) U += (P.app[k2] == a) ? (long long)minNP[k2] : (long long)P.Q[0];
+            if (U > (long long)P.C * P.R) k = false;
+            if (F.policy == 1 && has_inc) {
+                const long long ulb = (U + P.R - 1) / P.R;
+                if (ulb > uinc || (ulb >= uinc && U > Uinc)) k = false;
+            }
+            if (!k) keep[i][o] = 0;
+        }
+        __syncthreads();
+    }
+    // compaction in ascending option code (warp w: stage w) + records
+    for (int i = wid; i < n; i += FILTER_THREADS / 32) {
+        int cnt = 0;
+        float maxNT = 0.0f;
+        OptRec *dst = F.rec + ((size_t)i * P.nS + b) * O;
+        const uint32_t As = P.Am[i] * (uint32_t)P.S[b];
+        for (int o0 = 0; o0 < O; o0 += 32) {
+            const int o = o0 + lane;
+            const bool k = o < O && keep[i][o];
+            const unsigned m = __ballot_sync(0xffffffffu, k);
+            if (k) {
+                const int th = o % nQ, N = o / nQ + 1;
+                const float4 e = P.tab[((size_t)i * P.nS + b) * nQ + th];
+                OptRec r;
+                r.code = (uint32_t)o;
+                r.p = (uint32_t)P.Q[th];
+                r.N = (uint32_t)N;
+                r.NP = (uint32_t)(N * P.Q[th]);
+                r.W = P.W[i];
+                r.As = As;
+                r.MEM = P.W[i] + (uint32_t)N * As;
+                r.NB = __fmul_rn((float)N, e.z);
+                r.NT = __fmul_rn((float)N, e.y);
+                r.bw = e.z;
+                r.dur = e.x;
+                r.pmul = (65536u + r.p - 1u) / r.p;
+                dst[cnt + __popc(m & ((1u << lane) - 1u))] = r;
+                maxNT = fmaxf(maxNT, r.NT);
+            }
+            cnt += __popc(m);
+        }
+        for (int off = 16; off; off >>= 1) maxNT = fmaxf(maxNT, __shfl_xor_sync(0xffffffffu, maxNT, off));
+        if (lane == 0) {
+            StageBound s;
+            s.cnt = (uint32_t)cnt;
+            s.maxNT = maxNT;
+            s.mindur = mindur[i];
+            s.minNP = (uint32_t)(cnt ? minNP[i] : 0);
+            F.sb[(size_t)i * P.nS + b] = s;
+        }
+    }
+}
+
+__global__ void init_slots_kernel(Slot *s, int n) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        s[k].key = 0xFFFFFFFFull;
+        s[k].x = ~0ull;
+    }
+}
+
+// item space: for batch combo bc, items = prod_{i<d0} cnt_i(b_app(i)), 0 if any stage is empty
+__global__ void offsets_kernel(const DevProb P, const StageBound *sb, int d0, unsigned long long *item_off,
+                               DevHeader *hdr) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    unsigned long long acc = 0;
+    for (int bc = 0; bc < P.nbc; ++bc) {
+        item_off[bc] = acc;
+        int bb[AMAX];
+        int t = bc;
+        for (int a = P.A - 1; a >= 0; --a) {
+            bb[a] = t % P.nS;
+            t /= P.nS;
+        }
+        unsigned long long it = 1;
+        bool empty = false;
+        for (int i = 0; i < P.n; ++i) {
+            const unsigned c = sb[(size_t)i * P.nS + bb[P.app[i]]].cnt;
+            if (c == 0) empty = true;
+            if (i < d0) it *= c;
+        }
+        acc += empty ? 0ull : it;
+    }
+    item_off[P.nbc] = acc;
+    hdr->items_total = acc;
+}
+
+// the same item offsets, but an "empty" batch combo still has a well-defined
+// (zero) item range; used by chunk_of()
+__device__ inline long long find_code(const OptRec *list, int cnt, uint32_t code) {
+    int lo = 0, hi = cnt;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (list[mid].code < code) lo = mid + 1;
+        else hi = mid;
+    }
+    return (lo < cnt && list[lo].code == code) ? lo : -1;
+}
+
+__device__ inline unsigned long long item_of(const DevProb &P, const StageBound *sb, const OptRec *rec,
+                                             const unsigned long long *item_off, int d0, unsigned long long x) {
+    int beta[AMAX], rho[NMAX], theta[NMAX];
+    decode_index(P, x, beta, rho, theta);
+    int bc = 0;
+    for (int a = 0; a < P.A; ++a) bc = bc * P.nS + beta[a];
+    unsigned long long it = 0;
+    for (int i = 0; i < d0; ++i) {
+        const int b = beta[P.app[i]];
+        const unsigned c = sb[(size_t)i * P.nS + b].cnt;
+        const long long k = find_code(rec + ((size_t)i * P.nS + b) * P.O, (int)c, (uint32_t)(rho[i] * P.nQ + theta[i]));
+        it = it * c + (unsigned long long)(k < 0 ? 0 : k);
+    }
+    return item_off[bc] + it;
+}
+
+__global__ void eq2_kernel(const DevProb P, const float *lam, int nlev, int *y) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= P.nbc * nlev) return;
+    const int bc = idx / nlev, k = idx % nlev;
+    int beta[AMAX];
+    int t = bc;
+    for (int a = P.A - 1; a >= 0; --a) {
+        beta[a] = t % P.nS;
+        t /= P.nS;
+    }
+    y[idx] = eq2_gpus(P, beta, lam + k * P.A);
+}
+
+// slots -> result[k] (exact local best) and packed keys
+__global__ void reduce_kernel(const DevProb P, const Slot *slots, int nslots, int nlev, Slot *result,
+                              long long *keys, const StageBound *sb, const OptRec *rec,
+                              const unsigned long long *item_off, int d0, int chunk_items, int flat_shift) {
+    __shared__ unsigned long long sk[256], sx[256];
+    for (int k = 0; k < nlev; ++k) {
+        unsigned long long bk = ~0ull, bx = ~0ull;
+        for (int s = threadIdx.x; s < nslots; s += blockDim.x) {
+            const Slot v = slots[(size_t)s * nlev + k];
+            if (slot_less(v.key, v.x, bk, bx)) {
+                bk = v.key;
+                bx = v.x;
+            }
+        }
+        sk[threadIdx.x] = bk;
+        sx[threadIdx.x] = bx;
+        __syncthreads();
+        for (int st = blockDim.x / 2; st; st >>= 1) {
+            if (threadIdx.x < st && slot_less(sk[threadIdx.x + st], sx[threadIdx.x + st], sk[threadIdx.x], sx[threadIdx.x])) {
+                sk[threadIdx.x] = sk[threadIdx.x + st];
+                sx[threadIdx.x] = sx[threadIdx.x + st];
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            bk = sk[0];
+            bx = sx[0];
+            if (bk >= 0xFFFFFFFFull) {
+                bk = 0xFFFFFFFFull;
+                bx = ~0ull;
+            }
+            result[k].key = bk;
+            result[k].x = bx;
+            unsigned long long packed;
+            if (bk == 0xFFFFFFFFull) packed = ~0ull;
+            else {
+                unsigned long long low = (P.ntot <= (1ull << 32)) ? bx
+                                         : flat_shift >= 0 ? (bx >> flat_shift)
+                                         : item_of(P, sb, rec, item_off, d0, bx) / (unsigned long long)chunk_items;
+                packed = (bk << 32) | (low & 0xFFFFFFFFull);
+            }
+            keys[k] = (long long)(packed ^ 0x8000000000000000ull);
+        }
+        __syncthreads();
+    }
+}
+
+// keys (after the cross-rank MIN) -> which chunk must be re-scanned / exact index
+struct FinalArgs {
+    int policy, nlev, world;
+    const long long *keys;     // [nlev] reduced, sign-mapped
+    const Slot *local;         // [nlev] this rank's exact best
+    Slot *winner;              // [nlev] out: (objective key, x) ; x = ~0 if unresolved
+    unsigned long long *rescan;// [nlev] out: chunk to re-scan or ~0
+};
+
+__global__ void resolve_kernel(const DevProb P, const FinalArgs F) {
+    const int k = threadIdx.x;
+    if (k >= F.nlev) return;
+    const unsigned long long packed = (unsigned long long)F.keys[k] ^ 0x8000000000000000ull;
+    Slot w;
+    unsigned long long rs = ~0ull;
+    if (packed == ~0ull) {
+        w.key = 0xFFFFFFFFull;
+        w.x = ~0ull;
+    } else {
+        w.key = packed >> 32;
+        const unsigned long long low = packed & 0xFFFFFFFFull;
+        if (F.world == 1) w.x = F.local[k].x;
+        else if (P.ntot <= (1ull << 32)) w.x = low;
+        else {
+            w.x = ~0ull;
+            rs = low;
+        }
+    }
+    F.winner[k] = w;
+    F.rescan[k] = rs;
+}
+
+// winner index -> full plan (device), with the search counters
+__global__ void plan_kernel(const DevProb P, int policy, int nlev, const Slot *winner, const float *lam,
+                            const DevHeader *hdr, camelot_plan *out) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= nlev) return;
+    camelot_plan pl;
+    memset(&pl, 0, sizeof(pl));
+    for (int i = 0; i < CAMELOT_MAX_STAGES * CAMELOT_MAX_REPLICAS; ++i) pl.gpu_of_instance[i] = -1;
+    pl.n_scored = hdr->n_scored;
+    pl.n_feasible = hdr->n_feasible;
+    pl.n_covered = 0;
+    const Slot w = winner[k];
+    if (w.x == ~0ull) {
+        pl.index = ~0ull;
+        pl.status = CAMELOT_INFEASIBLE;
+        pl.violations = hdr->viol_or;
+        out[k] = pl;
+        return;
+    }
+    int beta[AMAX], rho[NMAX], theta[NMAX];
+    decode_index(P, w.x, beta, rho, theta);
+    FullScore s;
+    score_digits(P, beta, rho, theta, s);
+    pl.index = w.x;
+    pl.status = CAMELOT_OK;
+    for (int a = 0; a < P.A; ++a) {
+        pl.batch[a] = P.S[beta[a]];
+        pl.e2e_latency_ms[a] = s.Lsum[a];
+        pl.throughput_qps[a] = s.Tmin[a];
+    }
+    for (int i = 0; i < P.n; ++i) {
+        pl.replicas[i] = rho[i] + 1;
+        pl.quota_pct[i] = P.Q[theta[i]];
+        pl.stage_latency_ms[i] = s.L[i];
+        pl.stage_throughput_qps[i] = s.Ti[i];
+        pl.kappa[i] = s.kappa[i];
+        for (int r = 0; r < CAMELOT_MAX_REPLICAS && r < SCORE_RMAX; ++r)
+            pl.gpu_of_instance[i * CAMELOT_MAX_REPLICAS + r] = s.goi[i * SCORE_RMAX + r];
+    }
+    pl.quota_used = s.U;
+    pl.gpus_used = s.u;
+    if (policy == 1) {
+        pl.eq2_gpus = eq2_gpus(P, beta, lam + k * P.A);
+        pl.violations = level_verdict(P, s, lam + k * P.A, pl.eq2_gpus);
+        pl.objective = (float)s.U;
+    } else {
+        pl.violations = s.verdict;
+        pl.objective = s.T;
+    }
+    out[k] = pl;
+}
+
+// Naive exhaustive search (kernel N5 as a search): one thread scores one
+// candidate from scratch.  Used for PAPER_GLOBAL problems, single-stage
+// problems and as the un-hoisted baseline (CAMELOT_EXEC_NAIVE).  Chunks of
+// 2^FLAT_SHIFT consecutive indices are dealt to ranks round-robin.
+constexpr int FLAT_SHIFT = 15;
+constexpr int FLAT_THREADS = 256;
+
+struct FlatArgs {
+    int policy, nlev, rank, world;
+    unsigned long long lo, hi;
+    const float *lam;
+    const int *y;
+    int ystride, yoff;
+    const Slot *inc;
+    Slot *slots;
+    DevHeader *hdr;
+};
+
+__global__ void __launch_bounds__(FLAT_THREADS) flat_search_kernel(const DevProb P, const FlatArgs F) {
+    __shared__ unsigned long long bk_s[FLAT_THREADS / 32][LMAX], bx_s[FLAT_THREADS / 32][LMAX];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int k = lane; k < F.nlev; k += 32) {
+        bk_s[wid][k] = F.inc[k].key;
+        bx_s[wid][k] = F.inc[k].x;
+    }
+    __syncwarp();
+    unsigned long long scored = 0, feasible = 0;
+    unsigned viol = 0;
+    const unsigned long long CH = 1ull << FLAT_SHIFT;
+    const unsigned long long c0 = F.lo >> FLAT_SHIFT, c1 = (F.hi + CH - 1) >> FLAT_SHIFT;
+    // chunk c belongs to rank (c mod world); threads of the grid stride over its indices
+    const unsigned long long nthreads = (unsigned long long)gridDim.x * blockDim.x;
+    const unsigned long long tid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long cfirst = c0 + (unsigned long long)((F.rank - (long long)(c0 % F.world) + F.world) % F.world);
+    for (unsigned long long c = cfirst; c < c1; c += F.world) {
+        const unsigned long long a = max(c * CH, F.lo), b = min((c + 1) * CH, F.hi);
+        for (unsigned long long base = a; base < b; base += nthreads) {
+            const unsigned long long x = base + tid;
+            const bool v = x < b;
+            int beta[AMAX], rho[NMAX], theta[NMAX];
+            FullScore s;
+            s.verdict = 0xFFu;
+            if (v) {
+                decode_index(P, x, beta, rho, theta);
+                score_digits(P, beta, rho, theta, s);
+                ++scored;
+                viol |= s.verdict;
+                feasible += s.verdict == 0;
+            }
+            if (F.policy == 0) {
+                const bool ok = v && s.verdict == 0;
+                const unsigned long long key = ok ? (unsigned long long)objkey_maxload(s.T) : 0xFFFFFFFFull;
+                const bool imp = ok && slot_less(key, x, bk_s[wid][0], bx_s[wid][0]);
+                unsigned im = __ballot_sync(0xffffffffu, imp);
+                if (im) {
+                    unsigned long long k2 = imp ? key : ~0ull, x2 = imp ? x : ~0ull;
+                    for (int off = 16; off; off >>= 1) {
+                        unsigned long long ok2 = __shfl_xor_sync(0xffffffffu, k2, off);
+                        unsigned long long ox = __shfl_xor_sync(0xffffffffu, x2, off);
+                        if (slot_less(ok2, ox, k2, x2)) { k2 = ok2; x2 = ox; }
+                    }
+                    if (lane == 0 && slot_less(k2, x2, bk_s[wid][0], bx_s[wid][0])) {
+                        bk_s[wid][0] = k2;
+                        bx_s[wid][0] = x2;
+                    }
+                    __syncwarp();
+                }
+            } else {
+                const unsigned long long key = v ? (unsigned long long)objkey_minres(s.u, s.U) : 0xFFFFFFFFull;
+                int bc = 0;
+                if (v)
+                    for (int q = 0; q < P.A; ++q) bc = bc * P.nS + beta[q];
+                for (int k = 0; k < F.nlev; ++k) {
+                    bool ok = v && s.verdict == 0;
+                    if (ok) ok = level_verdict(P, s, F.lam + k * P.A, F.y[bc * F.ystride + F.yoff + k]) == 0;
+                    const bool imp = ok && slot_less(key, x, bk_s[wid][k], bx_s[wid][k]);
+                    unsigned im = __ballot_sync(0xffffffffu, imp);
+                    if (im) {
+                        unsigned long long k2 = imp ? key : ~0ull, x2 = imp ? x : ~0ull;
+                        for (int off = 16; off; off >>= 1) {
+                            unsigned long long ok2 = __shfl_xor_sync(0xffffffffu, k2, off);
+                            unsigned long long ox = __shfl_xor_sync(0xffffffffu, x2, off);
+                            if (slot_less(ok2, ox, k2, x2)) { k2 = ok2; x2 = ox; }
+                        }
+                        if (lane == 0 && slot_less(k2, x2, bk_s[wid][k], bx_s[wid][k])) {
+                            bk_s[wid][k] = k2;
+                            bx_s[wid][k] = x2;
+                        }
+                        __syncwarp();
+                    }
+                }
+            }
+        }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < F.nlev; k += blockDim.x) {
+        unsigned long long bk = bk_s[0][k], bx = bx_s[0][k];
+        for (int w = 1; w < FLAT_THREADS / 32; ++w)
+            if (slot_less(bk_s[w][k], bx_s[w][k], bk, bx)) {
+                bk = bk_s[w][k];
+                bx = bx_s[w][k];
+            }
+        F.slots[(size_t)blockIdx.x * F.nlev + k].key = bk;
+        F.slots[(size_t)blockIdx.x * F.nlev + k].x = bx;
+    }
+    for (int off = 16; off; off >>= 1) {
+        scored += __shfl_xor_sync(0xffffffffu, scored, off);
+        feasible += __shfl_xor_sync(0xffffffffu, feasible, off);
+        viol |= __shfl_xor_sync(0xffffffffu, viol, off);
+    }
+    if (lane == 0) {
+        atomicAdd(&F.hdr->n_scored, scored);
+        atomicAdd(&F.hdr->n_feasible, feasible);
+        atomicOr(&F.hdr->viol_or, viol & 0x7Fu);
+    }
+}
+
+// explicit plan (predict) -> plan
+__global__ void predict_kernel(const DevProb P, unsigned long long x, const float *lam, int nlev, camelot_plan *out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    camelot_plan pl;
+    memset(&pl, 0, sizeof(pl));
+    for (int i = 0; i < CAMELOT_MAX_STAGES * CAMELOT_MAX_REPLICAS; ++i) pl.gpu_of_instance[i] = -1;
+    int beta[AMAX], rho[NMAX], theta[NMAX];
+    decode_index(P, x, beta, rho, theta);
+    FullScore s;
+    score_digits(P, beta, rho, theta, s);
+    pl.index = x;
+    for (int a = 0; a < P.A; ++a) {
+        pl.batch[a] = P.S[beta[a]];
+        pl.e2e_latency_ms[a] = s.Lsum[a];
+        pl.throughput_qps[a] = s.Tmin[a];
+    }
+    for (int i = 0; i < P.n; ++i) {
+        pl.replicas[i] = rho[i] + 1;
+        pl.quota_pct[i] = P.Q[theta[i]];
+        pl.stage_latency_ms[i] = s.L[i];
+        pl.stage_throughput_qps[i] = s.Ti[i];
+        pl.kappa[i] = s.kappa[i];
+        for (int r = 0; r < CAMELOT_MAX_REPLICAS && r < SCORE_RMAX; ++r)
+            pl.gpu_of_instance[i * CAMELOT_MAX_REPLICAS + r] = s.goi[i * SCORE_RMAX + r];
+    }
+    pl.quota_used = s.U;
+    pl.gpus_used = s.u;
+    pl.objective = s.T;
+    pl.violations = s.verdict;
+    if (nlev > 0 && lam) {
+        pl.eq2_gpus = eq2_gpus(P, beta, lam);
+        pl.violations = level_verdict(P, s, lam, pl.eq2_gpus);
+    }
+    pl.status = pl.violations ? CAMELOT_INFEASIBLE : CAMELOT_OK;
+    out[0] = pl;
+}
+
+__global__ void score_range_kernel(const DevProb P, unsigned long long lo, unsigned long long cnt, uint8_t *verdict,
+                                   float *T, int *u, int *U) {
+    const unsigned long long t = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+    if (t >= cnt) return;
+    int beta[AMAX], rho[NMAX], theta[NMAX];
+    decode_index(P, lo + t, beta, rho, theta);
+    FullScore s;
+    score_digits(P, beta, rho, theta, s);
+    if (verdict) verdict[t] = (uint8_t)s.verdict;
+    if (T) T[t] = s.T;
+    if (u) u[t] = s.u;
+    if (U) U[t] = s.U;
+}
+
+}  // namespace cam
