@@ -176,7 +176,7 @@ Layout make_layout(const Dims &d, int nlev) {
     L.slots = put((size_t)MAXSLOTS * L.nlev * sizeof(Slot));
     // frontier of placement-state nodes: as many as there are leaf parents in the
     // whole space, clamped to [256, 2^20] (overflow falls back to inline DFS)
-    const size_t nb = d.C > 8 ? sizeof(Node<16>) : sizeof(Node<8>);
+    const size_t nb = d.C > 8 ? sizeof(Node<16>) : d.C > 4 ? sizeof(Node<8>) : sizeof(Node<4>);
     long double parents = (long double)d.ntot / (long double)d.O;
     L.fcap = (unsigned long long)std::max(256.0L, std::min((long double)(1u << 20), parents));
     // testing knob: force a small frontier to exercise the inline-descent fallback
@@ -260,34 +260,37 @@ struct Ctx {
     bool naive;
 };
 
-template <int CM, int POL>
+template <int CM>
 size_t search_smem() {
     return (size_t)SEARCH_WARPS * NMAX * sizeof(Node<CM>) + SEARCH_WARPS * sizeof(WarpCtl) +
            SEARCH_WARPS * sizeof(WarpBest);
 }
 
-std::mutex g_attr_mu;
-int g_slots_cache[64][2][2];
-bool g_slots_ready[64][2][2];
+// compile-time widths: positions CM in {4, 8, 16} >= C, stages NS in {4, 6, 8} >= n
+int cm_bucket(int C) { return C <= 4 ? 4 : C <= 8 ? 8 : 16; }
+int ns_bucket(int n) { return n <= 4 ? 4 : n <= 6 ? 6 : 8; }
 
-template <int CM, int POL>
+std::mutex g_attr_mu;
+struct GridKey {
+    int dev, cm, ns, pol;
+};
+std::vector<std::pair<GridKey, int>> g_grid_cache;
+
+template <int CM, int NS, int POL>
 int grid_for(int dev, int &grid) {
     std::lock_guard<std::mutex> lk(g_attr_mu);
-    const int ci = CM == 16 ? 1 : 0;
-    if (dev < 64 && g_slots_ready[dev][ci][POL]) {
-        grid = g_slots_cache[dev][ci][POL];
-        return CAMELOT_OK;
-    }
-    const size_t sm = search_smem<CM, POL>();
-    CU(cudaFuncSetAttribute(search_kernel<CM, POL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    for (auto &e : g_grid_cache)
+        if (e.first.dev == dev && e.first.cm == CM && e.first.ns == NS && e.first.pol == POL) {
+            grid = e.second;
+            return CAMELOT_OK;
+        }
+    const size_t sm = search_smem<CM>();
+    CU(cudaFuncSetAttribute(search_kernel<CM, NS, POL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     int per = 0, nsm = 0;
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, search_kernel<CM, POL>, SEARCH_THREADS, sm));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, search_kernel<CM, NS, POL>, SEARCH_THREADS, sm));
     CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     grid = std::max(1, std::min(MAXSLOTS, per * nsm));
-    if (dev < 64) {
-        g_slots_cache[dev][ci][POL] = grid;
-        g_slots_ready[dev][ci][POL] = true;
-    }
+    g_grid_cache.push_back({GridKey{dev, CM, NS, POL}, grid});
     return CAMELOT_OK;
 }
 
@@ -324,27 +327,35 @@ int setup(const camelot_problem *p, const camelot_cluster *c, const camelot_exec
     return CAMELOT_OK;
 }
 
-template <int CM, int POL>
+template <int CM, int NS, int POL>
 int launch_search(const Ctx &X, const SearchArgs &S, int grid) {
-    const size_t sm = search_smem<CM, POL>();
-    search_kernel<CM, POL><<<grid, SEARCH_THREADS, sm, X.st>>>(X.P, S);
+    const size_t sm = search_smem<CM>();
+    search_kernel<CM, NS, POL><<<grid, SEARCH_THREADS, sm, X.st>>>(X.P, S);
     COUNT_LAUNCH();
     CU(cudaGetLastError());
     return CAMELOT_OK;
 }
 
+#define CAM_DISPATCH(FN, ...)                                                                          \
+    do {                                                                                               \
+        const int cm_ = cm_bucket(X.d.C), ns_ = ns_bucket(X.d.n);                                      \
+        if (cm_ == 4 && ns_ == 4) return policy ? FN<4, 4, 1>(__VA_ARGS__) : FN<4, 4, 0>(__VA_ARGS__); \
+        if (cm_ == 4 && ns_ == 6) return policy ? FN<4, 6, 1>(__VA_ARGS__) : FN<4, 6, 0>(__VA_ARGS__); \
+        if (cm_ == 4) return policy ? FN<4, 8, 1>(__VA_ARGS__) : FN<4, 8, 0>(__VA_ARGS__);             \
+        if (cm_ == 8 && ns_ == 4) return policy ? FN<8, 4, 1>(__VA_ARGS__) : FN<8, 4, 0>(__VA_ARGS__); \
+        if (cm_ == 8 && ns_ == 6) return policy ? FN<8, 6, 1>(__VA_ARGS__) : FN<8, 6, 0>(__VA_ARGS__); \
+        if (cm_ == 8) return policy ? FN<8, 8, 1>(__VA_ARGS__) : FN<8, 8, 0>(__VA_ARGS__);             \
+        return policy ? FN<16, 8, 1>(__VA_ARGS__) : FN<16, 8, 0>(__VA_ARGS__);                         \
+    } while (0)
+
 int launch_search_any(const Ctx &X, int policy, const SearchArgs &S, int grid) {
-    if (X.cm16) return policy ? launch_search<16, 1>(X, S, grid) : launch_search<16, 0>(X, S, grid);
-    return policy ? launch_search<8, 1>(X, S, grid) : launch_search<8, 0>(X, S, grid);
+    CAM_DISPATCH(launch_search, X, S, grid);
 }
 
 int grid_any(const Ctx &X, int policy, int dev, int &grid) {
-    if (X.cm16) return policy ? grid_for<16, 1>(dev, grid) : grid_for<16, 0>(dev, grid);
-    return policy ? grid_for<8, 1>(dev, grid) : grid_for<8, 0>(dev, grid);
+    CAM_DISPATCH(grid_for, dev, grid);
 }
 
-// One search pass: filter -> offsets -> search -> reduce.
-//   inc: device incumbents [nlev]; result: device [nlev]; keys: device [nlev]
 int flat_grid(int dev, int &grid) {
     static int cache[64] = {0};
     if (dev < 64 && cache[dev]) {

@@ -36,18 +36,20 @@ struct DevProb {
 
 // One option (N, theta) of stage i at batch index b, precomputed by the filter kernel.
 struct __align__(16) OptRec {
+    // hot 32 bytes (two 16-byte loads in the search)
     uint32_t code;     // option code o = rho*nQ + theta
     uint32_t NP;       // N * p
     uint32_t N;        // replicas
-    uint32_t MEM;      // W_i + N*A_i*s  (MiB)
+    uint32_t pmul;     // ceil(2^16 / p): floor(a/p) = (a*pmul)>>16 for a <= 127
     float NB;          // fl(N * bw)
     float NT;          // fl(N * thr)
     float bw;          // bw of one replica
     float dur;         // duration (ms)
+    // cold
     uint32_t p;        // quota (%)
-    uint32_t pmul;     // ceil(2^16 / p): floor(a/p) = (a*pmul)>>16 for a <= 127
-    uint32_t As;       // A_i * s
     uint32_t W;        // W_i
+    uint32_t As;       // A_i * s
+    uint32_t MEM;      // W_i + N*A_i*s  (MiB)
 };
 
 // Per (stage, batch) bounds over the surviving options.

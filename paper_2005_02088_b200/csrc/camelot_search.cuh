@@ -418,6 +418,241 @@ __device__ __forceinline__ void warp_improve(WarpBest *wb, int k, bool imp, unsi
     __syncwarp();
 }
 
+// ---------------------------------------------------------------- register context (fast path)
+// The parent's placement state hoisted into registers once per parent.
+// Positions are padded to the compile-time width CM (padding: no quota, no
+// capacity => never used); stages to NS >= n.
+template <int CM, int NS>
+struct PCtx {
+    int prq[CM], pkim[CM];
+    float pdem[CM];
+    unsigned empty;                 // bit q: position q hosts no instance yet
+    unsigned hp[NS];                // bit q: placed stage i has a replica at position q
+    float dmax[NS], dur[NS], bw[NS], nt[NS];   // i < j: placed stage; i > j: dur = min duration
+    float tub, restT;
+    int u, U, rqsum, restU, bc;
+    unsigned long long x;
+};
+
+template <int CM, int NS>
+__device__ __forceinline__ void load_ctx(const DevProb &P, const SearchArgs &S, const Node<CM> &nd, int j,
+                                         PCtx<CM, NS> &c) {
+    c.empty = 0;
+#pragma unroll
+    for (int q = 0; q < CM; ++q) {
+        const bool in = q < P.C;
+        c.prq[q] = in ? nd.prq[q] : 0;
+        c.pkim[q] = in ? nd.pkim[q] : 0;
+        c.pdem[q] = in ? nd.pdem[q] : 0.0f;
+        if (in && nd.gcnt[nd.pgid[q]] == 0) c.empty |= 1u << q;
+    }
+#pragma unroll
+    for (int i = 0; i < NS; ++i) {
+        c.hp[i] = 0;
+        c.dmax[i] = 0.0f;
+        c.bw[i] = 0.0f;
+        c.nt[i] = 0.0f;
+        c.dur[i] = 0.0f;
+        if (i < j) {
+            const unsigned hm = nd.hmask[i];
+            unsigned m = 0;
+#pragma unroll
+            for (int q = 0; q < CM; ++q)
+                if (q < P.C && ((hm >> nd.pgid[q]) & 1u)) m |= 1u << q;
+            c.hp[i] = m;
+            c.dmax[i] = nd.dmax[i];
+            c.dur[i] = nd.dur[i];
+            c.bw[i] = nd.bw[i];
+            c.nt[i] = nd.nt[i];
+        } else if (i > j && i < P.n) {
+            c.dur[i] = sb_at(P, S, i, nd.b[P.app[i]]).mindur;
+        }
+    }
+    float restT = __int_as_float(0x7f800000);
+    int restU = 0;
+    for (int i2 = j + 1; i2 < P.n; ++i2) {
+        const StageBound &bb = sb_at(P, S, i2, nd.b[P.app[i2]]);
+        restT = fminf(restT, bb.maxNT);
+        restU += (int)bb.minNP;
+    }
+    c.restT = restT;
+    c.restU = restU;
+    c.tub = nd.tub;
+    c.u = nd.u;
+    c.U = nd.U;
+    c.rqsum = nd.rqsum;
+    c.bc = nd.bc;
+    c.x = nd.x;
+}
+
+struct FastEval {
+    bool placed;
+    int u, U;
+    float lsum[AMAX];
+    float kap[NMAX];
+    unsigned long long x;
+};
+
+// Place stage j with option r on the context and score it (branch-free
+// placement: per-position capacities K_q = canHold(q, N); pass 1 = first q with
+// K_q == N; pass 2 = greedy min(K_q, remaining) -- DESIGN.md 3.2, R14).
+template <int CM, int NS>
+__device__ __forceinline__ void fast_eval(const DevProb &P, const PCtx<CM, NS> &c, int j, const OptRec &r,
+                                          FastEval &fe) {
+    const int N = (int)r.N;
+    const bool cap = !(P.flags & F_NO_BW_CAP);
+    int K[CM];
+#pragma unroll
+    for (int q = 0; q < CM; ++q) {
+        int k = min(min(N, (int)(((uint32_t)c.prq[q] * r.pmul) >> 16)), c.pkim[q]);
+        if (cap && k > 0 && __fadd_rn(c.pdem[q], __fmul_rn((float)k, r.bw)) > P.BW) {
+            do {
+                --k;
+            } while (k > 0 && __fadd_rn(c.pdem[q], __fmul_rn((float)k, r.bw)) > P.BW);
+        }
+        K[q] = k;
+    }
+    int jstar = CM;
+#pragma unroll
+    for (int q = CM - 1; q >= 0; --q)
+        if (K[q] == N) jstar = q;
+    int kk[CM];
+    int rem = N;
+#pragma unroll
+    for (int q = 0; q < CM; ++q) {
+        const int g = min(K[q], rem);
+        rem -= g;
+        kk[q] = (jstar < CM) ? (q == jstar ? N : 0) : g;
+    }
+    fe.placed = (jstar < CM) || rem == 0;
+    fe.x = c.x * (unsigned long long)P.O + r.code;
+    fe.U = c.U + (int)r.NP;
+    float dm[NS];
+#pragma unroll
+    for (int i = 0; i < NS; ++i) dm[i] = c.dmax[i];
+    float dself = 0.0f;
+    int unew = 0;
+#pragma unroll
+    for (int q = 0; q < CM; ++q) {
+        // demand after the stage (== pdem when no replica lands on q)
+        const float d = __fadd_rn(c.pdem[q], __fmul_rn((float)kk[q], r.bw));
+        if (kk[q] > 0) {
+            dself = fmaxf(dself, d);
+            unew += (c.empty >> q) & 1u;
+        }
+#pragma unroll
+        for (int i = 0; i < NS; ++i)
+            if ((c.hp[i] >> q) & 1u) dm[i] = fmaxf(dm[i], d);
+    }
+    fe.u = c.u + unew;
+    float l0 = 0.0f, l1 = 0.0f;
+#pragma unroll
+    for (int i = 0; i < NS; ++i) {
+        if (i < P.n) {
+            float L;
+            if (i < j) {
+                const float k = kappa_of(dm[i], c.bw[i], P.gamma[i], P.invBW, P.flags);
+                fe.kap[i] = k;
+                L = __fmul_rn(c.dur[i], k);
+            } else if (i == j) {
+                const float k = kappa_of(dself, r.bw, P.gamma[i], P.invBW, P.flags);
+                fe.kap[i] = k;
+                L = __fmul_rn(r.dur, k);
+            } else {
+                fe.kap[i] = 1.0f;
+                L = c.dur[i];
+            }
+            // ordered per-application sums (stages are app-major)
+            if (P.app[i] == 0) l0 = (i == 0) ? L : __fadd_rn(l0, L);
+            else l1 = (i == P.first_of_app[1]) ? L : __fadd_rn(l1, L);
+        }
+    }
+    fe.lsum[0] = l0;
+    fe.lsum[1] = l1;
+}
+
+struct Counters {
+    unsigned long long scored, feasible, nodes;
+    unsigned viol;
+};
+
+// Exact leaf scoring + warp-level best update (shared by both paths).
+// nt(i) = fl(N_i thr_i) of stage i, kap(i) = contention factor.
+template <int POLICY, int NS, typename NtF>
+__device__ __forceinline__ void score_leaf(const DevProb &P, const SearchArgs &S, WarpBest *wb, int lane, bool inr,
+                                           bool placed, const float *lsum, const float *kap, NtF nt, float tub,
+                                           int u, int U, int bc, unsigned long long x, Counters &cn) {
+    cn.scored += inr;
+    bool feas = inr && placed;
+    if (feas) {
+        bool q = lsum[0] <= P.qos[0];
+        if (P.A > 1) q &= lsum[1] <= P.qos[1];
+        if (!q) cn.viol |= V_QOS;
+        feas = q;
+    }
+    cn.feasible += feas;
+    const int n = P.n;
+    if (POLICY == 0) {
+        unsigned long long key = 0xFFFFFFFFull;
+        if (feas) {
+            // T <= min_i fl(N_i thr_i): the divisions only when it can win
+            const unsigned long long kl = objkey_maxload(tub);
+            if (slot_less(kl, x, wb->key[0], wb->x[0])) {
+                float T = __int_as_float(0x7f800000);
+#pragma unroll
+                for (int i = 0; i < NS; ++i)
+                    if (i < n) {
+                        const float ti = kap[i] == 1.0f ? nt(i) : __fdiv_rn(nt(i), kap[i]);
+                        T = fminf(T, ti);
+                    }
+                key = objkey_maxload(T);
+            }
+        }
+        const bool imp = key != 0xFFFFFFFFull && slot_less(key, x, wb->key[0], wb->x[0]);
+        warp_improve(wb, 0, imp, key, x, lane);
+        if (lane == 0 && wb->key[0] < wb->bound) {
+            wb->bound = wb->key[0];
+            atomicMin(&S.hdr->best_obj, (unsigned int)wb->key[0]);
+        }
+        __syncwarp();
+    } else {
+        const unsigned long long key = objkey_minres(u, U);
+        const bool cand = feas && key <= wb->bound;
+        float tm0 = __int_as_float(0x7f800000), tm1 = __int_as_float(0x7f800000);
+        if (cand) {
+#pragma unroll
+            for (int i = 0; i < NS; ++i)
+                if (i < n) {
+                    const float ti = kap[i] == 1.0f ? nt(i) : __fdiv_rn(nt(i), kap[i]);
+                    if (P.app[i] == 0) tm0 = fminf(tm0, ti);
+                    else tm1 = fminf(tm1, ti);
+                }
+        }
+        if (__any_sync(0xffffffffu, cand)) {
+            const int nlev = S.nlev;
+            for (int k = 0; k < nlev; ++k) {
+                bool fk = cand;
+                if (fk) {
+                    fk &= tm0 >= S.lam[k * P.A];
+                    if (P.A > 1) fk &= tm1 >= S.lam[k * P.A + 1];
+                    if ((P.flags & F_EQ2_BUDGET) && u > S.y[bc * S.ystride + S.yoff + k]) fk = false;
+                }
+                const bool imp = fk && slot_less(key, x, wb->key[k], wb->x[k]);
+                warp_improve(wb, k, imp, key, x, lane);
+            }
+            if (lane == 0) {
+                unsigned long long m = 0;
+                for (int k = 0; k < nlev; ++k) m = max(m, wb->key[k]);
+                if (m < wb->bound) {
+                    wb->bound = m;
+                    atomicMin(&S.hdr->best_obj, (unsigned int)min(m, 0xFFFFFFFFull));
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
 // does this rank own the node at depth S.d0 (chunk = item / chunk_items,
 // item = canonical position of (beta combo, option indices of stages < d0))?
 template <int CM>
@@ -439,12 +674,80 @@ __device__ __forceinline__ void copy_node(Node<CM> &dst, const Node<CM> &src, in
     __syncwarp();
 }
 
+// Generic depth-first walk below stack[jtop] (no frontier): the fallback when
+// the frontier is full.  Same arithmetic as the fast path (eval_child).
+template <int CM, int POLICY>
+__device__ void dfs_generic(const DevProb &P, const SearchArgs &S, Node<CM> *stack, WarpCtl *ctl, WarpBest *wb,
+                            int jtop, int lane, Counters &cn) {
+    const int n = P.n;
+    int j = jtop;
+    if (lane == 0) {
+        ctl->cur[j] = 0;
+        ctl->msk[j] = 0;
+    }
+    __syncwarp();
+    while (true) {
+        const Node<CM> &nd = stack[j];
+        const int bj = nd.b[P.app[j]];
+        const int cntj = (int)sb_at(P, S, j, bj).cnt;
+        const unsigned msk = ctl->msk[j];
+        if (msk) {
+            const int kk = __ffs(msk) - 1;
+            const int opt = ctl->base[j] + kk;
+            __syncwarp();
+            if (lane == 0) ctl->msk[j] = msk & (msk - 1);
+            build_child<CM>(P, S, nd, j, opt_at(P, S, j, bj, opt), opt, stack[j + 1], lane);
+            if (j + 1 == S.d0 && !owns<CM>(P, S, stack[j + 1])) continue;
+            ++j;
+            if (lane == 0) {
+                ctl->cur[j] = 0;
+                ctl->msk[j] = 0;
+            }
+            __syncwarp();
+            continue;
+        }
+        const int cur = ctl->cur[j];
+        if (cur >= cntj) {
+            if (j == jtop) break;
+            --j;
+            continue;
+        }
+        __syncwarp();
+        if (lane == 0) {
+            ctl->base[j] = cur;
+            ctl->cur[j] = cur + 32;
+        }
+        __syncwarp();
+        const int opt = cur + lane;
+        const bool valid = opt < cntj;
+        const OptRec &r = opt_at(P, S, j, bj, valid ? opt : cur);
+        ChildEval ce;
+        if (valid) eval_child<CM>(P, S, nd, j, r, ce);
+        else ce.placed = false;
+        if (j < n - 1) {
+            cn.nodes += valid;
+            const bool sv = valid && inner_survives<CM>(P, S, nd, j, r, ce, wb->bound);
+            const unsigned m = __ballot_sync(0xffffffffu, sv);
+            if (lane == 0) ctl->msk[j] = m;
+            __syncwarp();
+            continue;
+        }
+        const bool inr = valid && ce.x >= S.lo && ce.x < S.hi;
+        if (inr && !ce.placed) cn.viol |= place_fail_bits<CM>(P, nd, r);
+        const int jj = j;
+        auto nt = [&](int i) { return i < jj ? nd.nt[i] : r.NT; };
+        score_leaf<POLICY, NMAX>(P, S, wb, lane, inr, ce.placed, ce.lsum, ce.kap, nt, fminf(nd.tub, r.NT), ce.u,
+                                 ce.U, nd.bc, ce.x, cn);
+    }
+}
+
 // ---------------------------------------------------------------- the search kernel
 // One level-synchronous pass: warps pop parents (dynamic, `grab` at a time),
-// lanes expand the parent's children 32 at a time, surviving children at depth
-// `flevel` are appended to the output frontier (inline depth-first descent when
-// the frontier is full), leaves are scored exactly.
-template <int CM, int POLICY>
+// hoist the parent into registers, lanes evaluate its children 32 at a time;
+// surviving children at depth `flevel` are appended to the output frontier
+// (generic inline depth-first descent when the frontier is full); leaves are
+// scored exactly.
+template <int CM, int NS, int POLICY>
 __global__ void __launch_bounds__(SEARCH_THREADS)
 search_kernel(const DevProb P, const SearchArgs S) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -468,14 +771,15 @@ search_kernel(const DevProb P, const SearchArgs S) {
         wb->bound = min(m, g);
     }
     __syncwarp();
-    unsigned long long scored = 0, feasible = 0, nodes = 0;
-    unsigned viol_or = 0;
+    Counters cn = {0, 0, 0, 0};
     const int n = P.n;
     const int jtop = S.level;
+    const bool leaf = jtop == n - 1;
     const Node<CM> *in = reinterpret_cast<const Node<CM> *>(S.in_nodes);
     Node<CM> *outf = reinterpret_cast<Node<CM> *>(S.out_nodes);
     const unsigned long long count = in ? min(*(volatile const unsigned long long *)S.in_count, S.in_cap)
                                         : (unsigned long long)P.nbc;
+    const unsigned long long span = P.opow[n - 1 - jtop];
 
     while (true) {
         unsigned long long e0 = 0;
@@ -491,146 +795,101 @@ search_kernel(const DevProb P, const SearchArgs S) {
         for (unsigned long long e = e0; e < e1; ++e) {
             if (!in) {
                 build_root<CM>(P, (int)e, stack[0], lane);
-                if (lane == 0) {
-                    for (int i = 0; i < NMAX; ++i) stack[0].kidx[i] = 0;
-                }
+                if (lane < NMAX) stack[0].kidx[lane] = 0;
                 __syncwarp();
             } else {
                 copy_node<CM>(stack[jtop], in[e], lane);
             }
-            // ---- depth-first walk below the parent (normally one level: the
-            // surviving children go to the next frontier)
-            int j = jtop;
-            if (lane == 0) {
-                ctl->cur[j] = 0;
-                ctl->msk[j] = 0;
+            const Node<CM> &nd = stack[jtop];
+            PCtx<CM, NS> c;
+            load_ctx<CM, NS>(P, S, nd, jtop, c);
+            // parent re-check against the current bound (it may have tightened)
+            if (S.prune) {
+                unsigned long long kl;
+                if (POLICY == 0) kl = objkey_maxload(fminf(c.tub, fminf(sb_at(P, S, jtop, nd.b[P.app[jtop]]).maxNT, c.restT)));
+                else {
+                    const int Ulb = c.U + (int)sb_at(P, S, jtop, nd.b[P.app[jtop]]).minNP + c.restU;
+                    kl = objkey_minres(max(c.u, (Ulb + P.R - 1) / P.R), Ulb);
+                }
+                if (kl > wb->bound) continue;
             }
-            __syncwarp();
-            while (true) {
-                const Node<CM> &nd = stack[j];
-                const int bj = nd.b[P.app[j]];
-                const int cntj = (int)sb_at(P, S, j, bj).cnt;
-                const unsigned msk = ctl->msk[j];
-                if (msk) {
-                    const int kk = __ffs(msk) - 1;
-                    const int opt = ctl->base[j] + kk;
-                    __syncwarp();
-                    if (lane == 0) ctl->msk[j] = msk & (msk - 1);
-                    build_child<CM>(P, S, nd, j, opt_at(P, S, j, bj, opt), opt, stack[j + 1], lane);
-                    if (j + 1 == S.d0 && !owns<CM>(P, S, stack[j + 1])) continue;
-                    if (j + 1 == S.flevel) {
+            const int bj = nd.b[P.app[jtop]];
+            const int cnt = (int)sb_at(P, S, jtop, bj).cnt;
+            const OptRec *list = S.rec + ((size_t)jtop * P.nS + bj) * P.O;
+            for (int base = 0; base < cnt; base += 32) {
+                const int opt = base + lane;
+                const bool valid = opt < cnt;
+                OptRec r;
+                {
+                    const uint4 *src = reinterpret_cast<const uint4 *>(list + (valid ? opt : base));
+                    const uint4 a = __ldg(src), b = __ldg(src + 1);
+                    r.code = a.x;
+                    r.NP = a.y;
+                    r.N = a.z;
+                    r.pmul = a.w;
+                    r.NB = __uint_as_float(b.x);
+                    r.NT = __uint_as_float(b.y);
+                    r.bw = __uint_as_float(b.z);
+                    r.dur = __uint_as_float(b.w);
+                }
+                const unsigned long long x = c.x * (unsigned long long)P.O + r.code;
+                bool go = valid;
+                // cheap exact bounds before the placement
+                if (S.prune && go) {
+                    // prune only when strictly worse than a known feasible key (ties survive)
+                    if (POLICY == 0) {
+                        const float t = leaf ? fminf(c.tub, r.NT) : fminf(fminf(c.tub, r.NT), c.restT);
+                        go = (unsigned long long)objkey_maxload(t) <= wb->bound;
+                    } else {
+                        const int Ulb = c.U + (int)r.NP + c.restU;
+                        go = (unsigned long long)objkey_minres(c.u, Ulb) <= wb->bound;
+                    }
+                    if (go && !leaf && c.rqsum - (int)r.NP < c.restU) go = false;
+                }
+                // canonical index range of the child's subtree
+                if (go) {
+                    const unsigned long long xs = x * span;
+                    if (xs >= S.hi || xs + span <= S.lo) go = false;
+                }
+                FastEval fe;
+                fe.placed = false;
+                if (go) fast_eval<CM, NS>(P, c, jtop, r, fe);
+                if (leaf) {
+                    if (go && !fe.placed) cn.viol |= place_fail_bits<CM>(P, nd, list[opt]);
+                    auto ntf = [&](int i) { return i < jtop ? c.nt[i] : r.NT; };
+                    score_leaf<POLICY, NS>(P, S, wb, lane, go, fe.placed, fe.lsum, fe.kap, ntf, fminf(c.tub, r.NT),
+                                           fe.u, fe.U, c.bc, x, cn);
+                    continue;
+                }
+                // ---- inner: bounds with the current contention
+                cn.nodes += go;
+                bool sv = go && fe.placed;
+                if (sv && S.prune) {
+                    sv &= fe.lsum[0] <= P.qos[0];
+                    if (P.A > 1) sv &= fe.lsum[1] <= P.qos[1];
+                    if (sv && POLICY == 1) {
+                        const int Ulb = fe.U + c.restU;
+                        sv = (unsigned long long)objkey_minres(max(fe.u, (Ulb + P.R - 1) / P.R), Ulb) <= wb->bound;
+                    }
+                }
+                unsigned m = __ballot_sync(0xffffffffu, sv);
+                while (m) {
+                    const int src = __ffs(m) - 1;
+                    m &= m - 1;
+                    const int o2 = base + src;
+                    build_child<CM>(P, S, stack[jtop], jtop, list[o2], o2, stack[jtop + 1], lane);
+                    if (jtop + 1 == S.d0 && !owns<CM>(P, S, stack[jtop + 1])) continue;
+                    if (jtop + 1 == S.flevel) {
                         unsigned long long slot = 0;
                         if (lane == 0) slot = atomicAdd(S.out_tail, 1ull);
                         slot = __shfl_sync(0xffffffffu, slot, 0);
                         if (slot < S.out_cap) {
-                            copy_node<CM>(outf[slot], stack[j + 1], lane);
+                            copy_node<CM>(outf[slot], stack[jtop + 1], lane);
                             continue;
                         }
                     }
-                    ++j;   // descend inline (frontier full, or below the frontier level)
-                    if (lane == 0) {
-                        ctl->cur[j] = 0;
-                        ctl->msk[j] = 0;
-                    }
-                    __syncwarp();
-                    continue;
-                }
-                const int cur = ctl->cur[j];
-                if (cur >= cntj) {
-                    if (j == jtop) break;
-                    --j;
-                    continue;
-                }
-                __syncwarp();
-                if (lane == 0) {
-                    ctl->base[j] = cur;
-                    ctl->cur[j] = cur + 32;
-                }
-                __syncwarp();
-                const int opt = cur + lane;
-                const bool valid = opt < cntj;
-                const OptRec &r = opt_at(P, S, j, bj, valid ? opt : cur);
-                ChildEval ce;
-                if (valid) eval_child<CM>(P, S, nd, j, r, ce);
-                else ce.placed = false;
-                if (j < n - 1) {
-                    // ---- inner node
-                    nodes += valid;
-                    const bool sv = valid && inner_survives<CM>(P, S, nd, j, r, ce, wb->bound);
-                    const unsigned m = __ballot_sync(0xffffffffu, sv);
-                    if (lane == 0) ctl->msk[j] = m;
-                    __syncwarp();
-                    continue;
-                }
-                // ---- leaf: exact score of candidate ce.x
-                const bool inr = valid && ce.x >= S.lo && ce.x < S.hi;
-                scored += inr;
-                if (inr && !ce.placed) viol_or |= place_fail_bits<CM>(P, nd, r);
-                bool feas = inr && ce.placed;
-                if (feas) {
-                    bool q = true;
-                    for (int a = 0; a < P.A; ++a) q &= ce.lsum[a] <= P.qos[a];
-                    if (!q) viol_or |= V_QOS;
-                    feas = q;
-                }
-                feasible += feas;
-                if (POLICY == 0) {
-                    unsigned long long key = 0xFFFFFFFFull;
-                    if (feas) {
-                        // T <= min_i fl(N_i thr_i): skip the divisions when it cannot win
-                        const unsigned long long kl = objkey_maxload(fminf(nd.tub, r.NT));
-                        if (slot_less(kl, ce.x, wb->key[0], wb->x[0])) {
-                            float T = __int_as_float(0x7f800000);
-                            for (int i = 0; i < n; ++i) {
-                                const float nti = (i < j) ? nd.nt[i] : r.NT;
-                                const float ti = ce.kap[i] == 1.0f ? nti : __fdiv_rn(nti, ce.kap[i]);
-                                T = fminf(T, ti);
-                            }
-                            key = objkey_maxload(T);
-                        }
-                    }
-                    const bool imp = key != 0xFFFFFFFFull && slot_less(key, ce.x, wb->key[0], wb->x[0]);
-                    warp_improve(wb, 0, imp, key, ce.x, lane);
-                    if (lane == 0 && wb->key[0] < wb->bound) {
-                        wb->bound = wb->key[0];
-                        atomicMin(&S.hdr->best_obj, (unsigned int)wb->key[0]);
-                    }
-                    __syncwarp();
-                } else {
-                    const unsigned long long key = objkey_minres(ce.u, ce.U);
-                    const bool cand = feas && key <= wb->bound;
-                    float tmin[AMAX] = {0.0f, 0.0f};
-                    if (cand) {
-                        for (int a = 0; a < P.A; ++a) {
-                            float tm = __int_as_float(0x7f800000);
-                            for (int i = P.first_of_app[a]; i <= P.last_of_app[a]; ++i) {
-                                const float nti = (i < j) ? nd.nt[i] : r.NT;
-                                const float ti = ce.kap[i] == 1.0f ? nti : __fdiv_rn(nti, ce.kap[i]);
-                                tm = fminf(tm, ti);
-                            }
-                            tmin[a] = tm;
-                        }
-                    }
-                    if (__any_sync(0xffffffffu, cand)) {
-                        for (int k = 0; k < nlev; ++k) {
-                            bool fk = cand;
-                            if (fk) {
-                                for (int a = 0; a < P.A; ++a) fk &= tmin[a] >= S.lam[k * P.A + a];
-                                if ((P.flags & F_EQ2_BUDGET) && ce.u > S.y[nd.bc * S.ystride + S.yoff + k]) fk = false;
-                            }
-                            const bool imp = fk && slot_less(key, ce.x, wb->key[k], wb->x[k]);
-                            warp_improve(wb, k, imp, key, ce.x, lane);
-                        }
-                        if (lane == 0) {
-                            unsigned long long m = 0;
-                            for (int k = 0; k < nlev; ++k) m = max(m, wb->key[k]);
-                            if (m < wb->bound) {
-                                wb->bound = m;
-                                atomicMin(&S.hdr->best_obj, (unsigned int)min(m, 0xFFFFFFFFull));
-                            }
-                        }
-                        __syncwarp();
-                    }
+                    // frontier full: walk the child's subtree here
+                    dfs_generic<CM, POLICY>(P, S, stack, ctl, wb, jtop + 1, lane, cn);
                 }
             }
         }
@@ -650,16 +909,16 @@ search_kernel(const DevProb P, const SearchArgs S) {
         sl.x = bx;
     }
     for (int off = 16; off; off >>= 1) {
-        scored += __shfl_xor_sync(0xffffffffu, scored, off);
-        feasible += __shfl_xor_sync(0xffffffffu, feasible, off);
-        nodes += __shfl_xor_sync(0xffffffffu, nodes, off);
-        viol_or |= __shfl_xor_sync(0xffffffffu, viol_or, off);
+        cn.scored += __shfl_xor_sync(0xffffffffu, cn.scored, off);
+        cn.feasible += __shfl_xor_sync(0xffffffffu, cn.feasible, off);
+        cn.nodes += __shfl_xor_sync(0xffffffffu, cn.nodes, off);
+        cn.viol |= __shfl_xor_sync(0xffffffffu, cn.viol, off);
     }
     if (lane == 0) {
-        atomicAdd(&S.hdr->n_scored, scored);
-        atomicAdd(&S.hdr->n_feasible, feasible);
-        atomicAdd(&S.hdr->n_nodes, nodes);
-        atomicOr(&S.hdr->viol_or, viol_or);
+        atomicAdd(&S.hdr->n_scored, cn.scored);
+        atomicAdd(&S.hdr->n_feasible, cn.feasible);
+        atomicAdd(&S.hdr->n_nodes, cn.nodes);
+        atomicOr(&S.hdr->viol_or, cn.viol);
     }
 }
 
