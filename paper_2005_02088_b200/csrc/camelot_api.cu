@@ -403,6 +403,12 @@ int flat_pass(const Ctx &X, int dev, int policy, int nlev, int ystride, int yoff
     return CAMELOT_OK;
 }
 
+int xshift_of(unsigned long long ntot) {
+    int s = 0;
+    while (s < 63 && ((ntot - 1) >> s) >= (1ull << 32)) ++s;
+    return s;
+}
+
 // the level-synchronous passes of one search (parents at depth 0..n-1)
 int run_passes(const Ctx &X, int dev, int policy, SearchArgs S, bool timed) {
     char *ws = X.ws;
@@ -459,6 +465,7 @@ int search_pass(const Ctx &X, int dev, int policy, int nlev, bool prune, int str
     DevHeader *hdr = reinterpret_cast<DevHeader *>(ws + X.L.hdr);
     CU(cudaMemsetAsync(hdr, 0, sizeof(DevHeader), X.st));
     CU(cudaMemsetAsync(&hdr->best_obj, 0xFF, sizeof(unsigned int), X.st));
+    CU(cudaMemsetAsync(&hdr->best_packed, 0xFF, sizeof(unsigned long long), X.st));
     FilterArgs F;
     F.policy = policy;
     F.prune = prune;
@@ -495,6 +502,7 @@ int search_pass(const Ctx &X, int dev, int policy, int nlev, bool prune, int str
     S.inc = inc;
     S.hdr = hdr;
     S.slots = reinterpret_cast<Slot *>(ws + slots_off(X.L));
+    S.xshift = xshift_of(X.d.ntot);
     int rc = run_passes(X, dev, policy, S, timed);
     if (rc) return rc;
     int grid = 0;
@@ -542,7 +550,9 @@ int rescan_pass(const Ctx &X, int dev, int policy, int nlev, bool prune, int k, 
     S.slots = reinterpret_cast<Slot *>(ws + slots_off(X.L));
     S.chunk_lo = chunk;
     S.chunk_hi = chunk + 1;
+    S.xshift = xshift_of(X.d.ntot);
     CU(cudaMemsetAsync(&hdr->best_obj, 0xFF, sizeof(unsigned int), X.st));
+    CU(cudaMemsetAsync(&hdr->best_packed, 0xFF, sizeof(unsigned long long), X.st));
     int rc = run_passes(X, dev, policy, S, false);
     if (rc) return rc;
     int grid = 0;
@@ -564,8 +574,28 @@ void range_of(const Ctx &X, const camelot_exec *ex, unsigned long long &lo, unsi
     if (lo > hi) lo = hi;
 }
 
-bool use_coarse(const Ctx &X, bool prune) { return prune && !X.naive && X.d.nQ >= 20 && X.d.ntot > 4000000ull; }
-int coarse_stride(const Ctx &X) { return std::max(2, X.d.nQ / 10); }
+bool use_coarse(const Ctx &X, bool prune) { return prune && !X.naive && X.d.nQ >= 8 && X.d.ntot > 4000000ull; }
+// quota sub-grid strides of the incumbent cascade (every stride-th quota counted
+// from the top, so 100% is always included).  CAMELOT_COARSE="25,10" overrides.
+std::vector<int> coarse_strides(const Ctx &X) {
+    std::vector<int> v;
+    if (const char *e = getenv("CAMELOT_COARSE")) {
+        const char *p = e;
+        while (*p) {
+            char *q = nullptr;
+            const long s = strtol(p, &q, 10);
+            if (q == p) break;
+            if (s >= 2 && s < X.d.nQ) v.push_back((int)s);
+            p = (*q == ',') ? q + 1 : q;
+        }
+        return v;
+    }
+    // measured on C4: (nQ/4, nQ/20) = (25, 5) beats (10) and (25, 10)
+    const int s1 = X.d.nQ / 4, s2 = X.d.nQ / 20;
+    if (s1 >= 2) v.push_back(s1);
+    if (s2 >= 2 && s2 < s1) v.push_back(s2);
+    return v;
+}
 
 // local search (incumbent pass + main pass); leaves keys in X.L.keys (or d_keys) and the
 // exact local best in X.L.result
@@ -591,11 +621,14 @@ int local_search(const Ctx &X, const camelot_exec *ex, int policy, int nlev, lon
     int dev = ex->device;
     int rc;
     if (use_coarse(X, prune)) {
-        // incumbent: exact optimum of the coarse quota sub-grid (replicated on every rank)
-        rc = search_pass(X, dev, policy, nlev, true, coarse_stride(X), inc, result,
-                         reinterpret_cast<long long *>(ws + X.L.keys), 0, 1, lo, hi, false);
-        if (rc) return rc;
-        CU(cudaMemcpyAsync(inc, result, nlev * sizeof(Slot), cudaMemcpyDeviceToDevice, X.st));
+        // incumbent: exact optimum of coarse quota sub-grids, coarsest first (each
+        // pass seeds the next); replicated on every rank
+        for (int stride : coarse_strides(X)) {
+            rc = search_pass(X, dev, policy, nlev, true, stride, inc, result,
+                             reinterpret_cast<long long *>(ws + X.L.keys), 0, 1, lo, hi, false);
+            if (rc) return rc;
+            CU(cudaMemcpyAsync(inc, result, nlev * sizeof(Slot), cudaMemcpyDeviceToDevice, X.st));
+        }
     }
     rc = search_pass(X, dev, policy, nlev, prune, 1, inc, result, keys, ex->rank, ex->world, lo, hi, true);
     if (rc) return rc;

@@ -73,6 +73,7 @@ struct DevHeader {
     unsigned long long t_search_ns;
     unsigned int inc_passes;
     unsigned int pad[7];
+    unsigned long long best_packed;      // (objective key << 32) | (index >> xshift), atomicMin (1 level)
     unsigned long long head[NMAX + 1];   // pop counter of pass j
     unsigned long long tail[NMAX + 1];   // size of the frontier at depth j (may exceed capacity)
 };

@@ -55,6 +55,7 @@ struct SearchArgs {
     unsigned long long *out_tail;
     unsigned long long out_cap;
     unsigned long long *head;   // pop counter of this pass
+    int xshift;                 // index >> xshift fits 32 bits (tie pruning key)
 };
 
 // Placement state after the first j stages, in shared memory (one per DFS
@@ -354,7 +355,32 @@ struct WarpBest {
     unsigned long long key[LMAX];   // objective key (32 bits used), smaller is better
     unsigned long long x[LMAX];
     unsigned long long bound;       // pruning bound: max over levels of key (conservative)
+    unsigned long long gpack;       // device-wide (key << 32 | x >> xshift) best (1 level)
 };
+
+// Can a subtree whose keys are >= kl and whose indices are >= xs still hold
+// the answer?  Strictly worse keys cannot; with ONE level, a key equal to the
+// best can only tie and ties go to the smallest index, so a subtree entirely
+// above the best's index cannot either (exact).
+__device__ __forceinline__ bool can_win(unsigned long long kl, unsigned long long xs, const WarpBest *wb, int nlev,
+                                        int xshift) {
+    if (kl > wb->bound) return false;
+    if (nlev == 1) {
+        if (kl == wb->key[0] && xs > wb->x[0]) return false;
+        if (kl == (wb->gpack >> 32) && (xs >> xshift) > (wb->gpack & 0xFFFFFFFFull)) return false;
+    }
+    return true;
+}
+
+__device__ __forceinline__ void publish_best(const SearchArgs &S, WarpBest *wb) {
+    // lane 0 only: the warp's level-0 best to the device-wide packed best
+    if (wb->key[0] >= 0xFFFFFFFFull) return;
+    const unsigned long long pk = (wb->key[0] << 32) | min(wb->x[0] >> S.xshift, 0xFFFFFFFFull);
+    if (pk < wb->gpack) {
+        wb->gpack = pk;
+        atomicMin(&S.hdr->best_packed, pk);
+    }
+}
 
 // key lower bound of any completion of a child at stage j (inner node)
 template <int CM>
@@ -430,6 +456,8 @@ struct PCtx {
     unsigned hp[NS];                // bit q: placed stage i has a replica at position q
     float dmax[NS], dur[NS], bw[NS], nt[NS];   // i < j: placed stage; i > j: dur = min duration
     float tub, restT;
+    float lpre;                     // ordered fp32 sum of current L of placed stages of app(j) (-1: none)
+    float lother;                   // lower bound of the other application's latency sum (A = 2)
     int u, U, rqsum, restU, bc;
     unsigned long long x;
 };
@@ -477,7 +505,38 @@ __device__ __forceinline__ void load_ctx(const DevProb &P, const SearchArgs &S, 
     }
     c.restT = restT;
     c.restU = restU;
-    c.tub = nd.tub;
+    // throughput upper bound of every completion: contention only grows, so
+    // T_i <= fl(fl(N_i thr_i) / kappa_i(current)) for the placed stages
+    float tub = nd.tub;
+#pragma unroll
+    for (int i = 0; i < NS; ++i)
+        if (i < j) {
+            const float k = kappa_of(c.dmax[i], c.bw[i], P.gamma[i], P.invBW, P.flags);
+            if (k != 1.0f) tub = fminf(tub, __fdiv_rn(c.nt[i], k));
+        }
+    c.tub = tub;
+    // QoS prefix of the child's application (current contention; it only grows)
+    {
+        const int aj = P.app[j];
+        float lp = -1.0f, lo = 0.0f;
+        bool lo_started = false;
+#pragma unroll
+        for (int i = 0; i < NS; ++i)
+            if (i < P.n) {
+                float L;
+                if (i < j) L = __fmul_rn(c.dur[i], kappa_of(c.dmax[i], c.bw[i], P.gamma[i], P.invBW, P.flags));
+                else if (i > j) L = c.dur[i];
+                else continue;
+                if (P.app[i] == aj) {
+                    if (i < j) lp = (lp < 0.0f) ? L : __fadd_rn(lp, L);
+                } else {
+                    lo = lo_started ? __fadd_rn(lo, L) : L;
+                    lo_started = true;
+                }
+            }
+        c.lpre = lp;
+        c.lother = lo_started ? lo : 0.0f;
+    }
     c.u = nd.u;
     c.U = nd.U;
     c.rqsum = nd.rqsum;
@@ -571,6 +630,18 @@ __device__ __forceinline__ void fast_eval(const DevProb &P, const PCtx<CM, NS> &
     fe.lsum[1] = l1;
 }
 
+// Is min_i fl(nt_i / kap_i) over stages i <= j certainly below the threshold
+// T_thr?  __fdividef is within 2 ulp; with the 2^-19 margin the answer "yes" is
+// exact-safe (used only to prune; exact values are computed with __fdiv_rn).
+template <int NS, typename NtF>
+__device__ __forceinline__ bool t_certainly_below(const DevProb &P, int j, const float *kap, NtF nt, float T_thr) {
+    float t = __int_as_float(0x7f800000);
+#pragma unroll
+    for (int i = 0; i < NS; ++i)
+        if (i <= j && i < P.n) t = fminf(t, kap[i] == 1.0f ? nt(i) : __fdividef(nt(i), kap[i]));
+    return __fmul_rn(t, 1.0f + 1.0f / 524288.0f) < T_thr;
+}
+
 struct Counters {
     unsigned long long scored, feasible, nodes;
     unsigned viol;
@@ -597,7 +668,12 @@ __device__ __forceinline__ void score_leaf(const DevProb &P, const SearchArgs &S
         if (feas) {
             // T <= min_i fl(N_i thr_i): the divisions only when it can win
             const unsigned long long kl = objkey_maxload(tub);
-            if (slot_less(kl, x, wb->key[0], wb->x[0])) {
+            bool maybe = slot_less(kl, x, wb->key[0], wb->x[0]);
+            if (maybe && wb->key[0] < 0xFFFFFFFFull) {
+                const float Tb = __uint_as_float(0xFFFFFFFFu - (unsigned)wb->key[0]);
+                if (t_certainly_below<NS>(P, n - 1, kap, nt, Tb)) maybe = false;
+            }
+            if (maybe) {
                 float T = __int_as_float(0x7f800000);
 #pragma unroll
                 for (int i = 0; i < NS; ++i)
@@ -610,9 +686,12 @@ __device__ __forceinline__ void score_leaf(const DevProb &P, const SearchArgs &S
         }
         const bool imp = key != 0xFFFFFFFFull && slot_less(key, x, wb->key[0], wb->x[0]);
         warp_improve(wb, 0, imp, key, x, lane);
-        if (lane == 0 && wb->key[0] < wb->bound) {
-            wb->bound = wb->key[0];
-            atomicMin(&S.hdr->best_obj, (unsigned int)wb->key[0]);
+        if (lane == 0) {
+            if (wb->key[0] < wb->bound) {
+                wb->bound = wb->key[0];
+                atomicMin(&S.hdr->best_obj, (unsigned int)wb->key[0]);
+            }
+            publish_best(S, wb);
         }
         __syncwarp();
     } else {
@@ -647,6 +726,7 @@ __device__ __forceinline__ void score_leaf(const DevProb &P, const SearchArgs &S
                     wb->bound = m;
                     atomicMin(&S.hdr->best_obj, (unsigned int)min(m, 0xFFFFFFFFull));
                 }
+                if (nlev == 1) publish_best(S, wb);
             }
             __syncwarp();
         }
@@ -733,7 +813,7 @@ __device__ void dfs_generic(const DevProb &P, const SearchArgs &S, Node<CM> *sta
             continue;
         }
         const bool inr = valid && ce.x >= S.lo && ce.x < S.hi;
-        if (inr && !ce.placed) cn.viol |= place_fail_bits<CM>(P, nd, r);
+        if (!S.prune && inr && !ce.placed) cn.viol |= place_fail_bits<CM>(P, nd, r);
         const int jj = j;
         auto nt = [&](int i) { return i < jj ? nd.nt[i] : r.NT; };
         score_leaf<POLICY, NMAX>(P, S, wb, lane, inr, ce.placed, ce.lsum, ce.kap, nt, fminf(nd.tub, r.NT), ce.u,
@@ -769,6 +849,9 @@ search_kernel(const DevProb P, const SearchArgs S) {
         for (int k = 0; k < nlev; ++k) m = max(m, wb->key[k]);
         const unsigned long long g = (unsigned long long)(*(volatile unsigned int *)&S.hdr->best_obj);
         wb->bound = min(m, g);
+        wb->gpack = *(volatile unsigned long long *)&S.hdr->best_packed;
+        if (nlev == 1 && wb->key[0] < 0xFFFFFFFFull)
+            wb->gpack = min(wb->gpack, (wb->key[0] << 32) | min(wb->x[0] >> S.xshift, 0xFFFFFFFFull));
     }
     __syncwarp();
     Counters cn = {0, 0, 0, 0};
@@ -780,19 +863,27 @@ search_kernel(const DevProb P, const SearchArgs S) {
     const unsigned long long count = in ? min(*(volatile const unsigned long long *)S.in_count, S.in_cap)
                                         : (unsigned long long)P.nbc;
     const unsigned long long span = P.opow[n - 1 - jtop];
+    // few parents (shallow passes): each block of 32 children is its own work item
+    const int nblk = (P.O + 31) / 32;
+    const int split = (count < 4ull * gridDim.x * SEARCH_WARPS) ? nblk : 1;
+    const unsigned long long items = count * (unsigned long long)split;
 
     while (true) {
         unsigned long long e0 = 0;
         if (lane == 0) e0 = atomicAdd(S.head, (unsigned long long)S.grab);
         e0 = __shfl_sync(0xffffffffu, e0, 0);
-        if (e0 >= count) break;
-        if (lane == 0) {   // refresh the pruning bound from the device-wide best
+        if (e0 >= items) break;
+        if (lane == 0) {   // refresh the pruning bounds from the device-wide best
             const unsigned long long g = (unsigned long long)(*(volatile unsigned int *)&S.hdr->best_obj);
             if (g < wb->bound) wb->bound = g;
+            const unsigned long long gp = *(volatile unsigned long long *)&S.hdr->best_packed;
+            if (gp < wb->gpack) wb->gpack = gp;
         }
         __syncwarp();
-        const unsigned long long e1 = min(e0 + (unsigned long long)S.grab, count);
-        for (unsigned long long e = e0; e < e1; ++e) {
+        const unsigned long long e1 = min(e0 + (unsigned long long)S.grab, items);
+        for (unsigned long long it = e0; it < e1; ++it) {
+            const unsigned long long e = it / (unsigned)split;
+            const int blk = (int)(it % (unsigned)split);
             if (!in) {
                 build_root<CM>(P, (int)e, stack[0], lane);
                 if (lane < NMAX) stack[0].kidx[lane] = 0;
@@ -811,12 +902,14 @@ search_kernel(const DevProb P, const SearchArgs S) {
                     const int Ulb = c.U + (int)sb_at(P, S, jtop, nd.b[P.app[jtop]]).minNP + c.restU;
                     kl = objkey_minres(max(c.u, (Ulb + P.R - 1) / P.R), Ulb);
                 }
-                if (kl > wb->bound) continue;
+                if (!can_win(kl, c.x * P.opow[n - jtop], wb, nlev, S.xshift)) continue;
             }
             const int bj = nd.b[P.app[jtop]];
             const int cnt = (int)sb_at(P, S, jtop, bj).cnt;
             const OptRec *list = S.rec + ((size_t)jtop * P.nS + bj) * P.O;
-            for (int base = 0; base < cnt; base += 32) {
+            const int b_lo = split > 1 ? blk * 32 : 0;
+            const int b_hi = split > 1 ? min(cnt, b_lo + 32) : cnt;
+            for (int base = b_lo; base < b_hi; base += 32) {
                 const int opt = base + lane;
                 const bool valid = opt < cnt;
                 OptRec r;
@@ -836,15 +929,27 @@ search_kernel(const DevProb P, const SearchArgs S) {
                 bool go = valid;
                 // cheap exact bounds before the placement
                 if (S.prune && go) {
-                    // prune only when strictly worse than a known feasible key (ties survive)
+                    // prune only when the subtree cannot hold the answer (ties by index)
+                    unsigned long long kl;
                     if (POLICY == 0) {
                         const float t = leaf ? fminf(c.tub, r.NT) : fminf(fminf(c.tub, r.NT), c.restT);
-                        go = (unsigned long long)objkey_maxload(t) <= wb->bound;
+                        kl = objkey_maxload(t);
                     } else {
                         const int Ulb = c.U + (int)r.NP + c.restU;
-                        go = (unsigned long long)objkey_minres(c.u, Ulb) <= wb->bound;
+                        kl = objkey_minres(max(c.u, (Ulb + P.R - 1) / P.R), Ulb);
                     }
+                    go = can_win(kl, x * span, wb, nlev, S.xshift);
                     if (go && !leaf && c.rqsum - (int)r.NP < c.restU) go = false;
+                }
+                // QoS lower bound before placement: L_j >= dur, placed stages' L
+                // only grow, unplaced stages >= their minimum duration (ordered sum)
+                if (S.prune && go) {
+                    const int aj = P.app[jtop];
+                    float lb = c.lpre < 0.0f ? r.dur : __fadd_rn(c.lpre, r.dur);
+#pragma unroll
+                    for (int i = 0; i < NS; ++i)
+                        if (i > jtop && i < n && P.app[i] == aj) lb = __fadd_rn(lb, c.dur[i]);
+                    go = lb <= P.qos[aj];
                 }
                 // canonical index range of the child's subtree
                 if (go) {
@@ -855,7 +960,8 @@ search_kernel(const DevProb P, const SearchArgs S) {
                 fe.placed = false;
                 if (go) fast_eval<CM, NS>(P, c, jtop, r, fe);
                 if (leaf) {
-                    if (go && !fe.placed) cn.viol |= place_fail_bits<CM>(P, nd, list[opt]);
+                    // violation diagnostics are exact (and computed) only in flat mode
+                    if (!S.prune && go && !fe.placed) cn.viol |= place_fail_bits<CM>(P, nd, list[opt]);
                     auto ntf = [&](int i) { return i < jtop ? c.nt[i] : r.NT; };
                     score_leaf<POLICY, NS>(P, S, wb, lane, go, fe.placed, fe.lsum, fe.kap, ntf, fminf(c.tub, r.NT),
                                            fe.u, fe.U, c.bc, x, cn);
@@ -867,6 +973,11 @@ search_kernel(const DevProb P, const SearchArgs S) {
                 if (sv && S.prune) {
                     sv &= fe.lsum[0] <= P.qos[0];
                     if (P.A > 1) sv &= fe.lsum[1] <= P.qos[1];
+                    if (sv && POLICY == 0 && wb->bound < 0xFFFFFFFFull) {
+                        const float Tbest = __uint_as_float(0xFFFFFFFFu - (unsigned)wb->bound);
+                        auto ntf2 = [&](int i) { return i < jtop ? c.nt[i] : r.NT; };
+                        if (t_certainly_below<NS>(P, jtop, fe.kap, ntf2, Tbest)) sv = false;
+                    }
                     if (sv && POLICY == 1) {
                         const int Ulb = fe.U + c.restU;
                         sv = (unsigned long long)objkey_minres(max(fe.u, (Ulb + P.R - 1) / P.R), Ulb) <= wb->bound;
