@@ -258,13 +258,13 @@ def main():
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
     clocks = clk.summary()
     ops_per_eval = algorithmic_ops_per_eval(prob)
-    evals = sum(s1["n_scored"] + s1["n_nodes"] + s2["n_scored"] + s2["n_nodes"] for s1, s2 in kt) / args.steps
+    evals = sum(s1["cum_scored"] + s1["cum_nodes"] + s2["cum_scored"] + s2["cum_nodes"] for s1, s2 in kt) / args.steps
     k_ns = sum(s1["t_ns"] + s2["t_ns"] for s1, s2 in kt) / args.steps
     achieved = ops_per_eval * evals / (k_ns * 1e-9) / 1e12 if k_ns else None
     peak = n_sm * 4 * 32 * sm_max * 1e6 / 1e12          # lane-instructions/s (issue bound)
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s",
             "frac": (achieved / peak) if achieved else None, "traffic": None,
-            "kernel": "search_kernel (main pass, both policies)",
+            "kernel": "search_kernel + filter (incumbent cascade and main pass, both policies)",
             "ops_per_eval": ops_per_eval, "evals_per_step": evals,
             "kernel_ms_per_step": k_ns / 1e6,
             "kernel_share_of_step": (k_ns / 1e6) / ms_step if ms_step else None,

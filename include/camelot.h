@@ -240,12 +240,14 @@ int camelot_finalize(const camelot_problem *p, const camelot_cluster *c, int pol
                      const float *load_qps, int n_loads, const int64_t *d_keys,
                      const camelot_exec *exec, camelot_plan *out);
 
-/* Statistics of the last search on this workspace (host out, synchronises the
- * stream): [0] leaf candidates scored, [1] inner tree nodes evaluated,
- * [2] feasible candidates seen, [3] duration of the main search kernel in ns
- * (CUDA events on exec->stream), [4] work items of the main pass,
- * [5] kernels launched by the last plan/search call. */
-int camelot_last_stats(const camelot_exec *exec, uint64_t *out6);
+/* Statistics of the last search on this workspace (host out[8], synchronises
+ * the stream): [0] leaf candidates scored by the main pass, [1] inner tree
+ * nodes evaluated by the main pass, [2] feasible candidates seen, [3] device
+ * time of the whole search (incumbent cascade + main pass, CUDA events on
+ * exec->stream, ns), [4] depth-d0 work items of the main pass, [5] kernels
+ * launched by the last plan/search call, [6] leaves and [7] inner nodes
+ * evaluated over the cascade and the main pass. */
+int camelot_last_stats(const camelot_exec *exec, uint64_t *out8);
 
 /* Process-wide number of kernels launched by this library so far. */
 uint64_t camelot_kernel_launches(void);

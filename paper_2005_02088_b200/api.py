@@ -221,11 +221,11 @@ class Session:
         return [_plan(o, self.n, self.A) for o in out]
 
     def last_stats(self):
-        out = (C.c_uint64 * 6)()
+        out = (C.c_uint64 * 8)()
         ex = self.exec()
         L.check(L.lib().camelot_last_stats(C.byref(ex), out), False)
         return dict(n_scored=out[0], n_nodes=out[1], n_feasible=out[2], t_ns=out[3], items=out[4],
-                    inc_passes=out[5])
+                    launches=out[5], cum_scored=out[6], cum_nodes=out[7])
 
 
 # ---------------------------------------------------------------------- functional API

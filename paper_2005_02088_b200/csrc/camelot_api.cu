@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstddef>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -463,7 +464,7 @@ int search_pass(const Ctx &X, int dev, int policy, int nlev, bool prune, int str
         return flat_pass(X, dev, policy, nlev, nlev, 0, reinterpret_cast<const float *>(ws + X.L.lam), inc, result,
                          keys, rank, world, lo, hi);
     DevHeader *hdr = reinterpret_cast<DevHeader *>(ws + X.L.hdr);
-    CU(cudaMemsetAsync(hdr, 0, sizeof(DevHeader), X.st));
+    CU(cudaMemsetAsync(hdr, 0, offsetof(DevHeader, cum_scored), X.st));
     CU(cudaMemsetAsync(&hdr->best_obj, 0xFF, sizeof(unsigned int), X.st));
     CU(cudaMemsetAsync(&hdr->best_packed, 0xFF, sizeof(unsigned long long), X.st));
     FilterArgs F;
@@ -590,10 +591,10 @@ std::vector<int> coarse_strides(const Ctx &X) {
         }
         return v;
     }
-    // measured on C4: (nQ/4, nQ/20) = (25, 5) beats (10) and (25, 10)
-    const int s1 = X.d.nQ / 4, s2 = X.d.nQ / 20;
-    if (s1 >= 2) v.push_back(s1);
-    if (s2 >= 2 && s2 < s1) v.push_back(s2);
+    // measured on C4 / C5: (nQ/2, nQ/4, nQ/20) = C4 (50, 25, 5),
+    // C5 (5, 2) beat single levels (10) / (2) and (25, 10)
+    for (int s : {X.d.nQ / 2, X.d.nQ / 4, X.d.nQ / 20})
+        if (s >= 2 && (v.empty() || s < v.back())) v.push_back(s);
     return v;
 }
 
@@ -620,6 +621,20 @@ int local_search(const Ctx &X, const camelot_exec *ex, int policy, int nlev, lon
     range_of(X, ex, lo, hi);
     int dev = ex->device;
     int rc;
+    {
+        DevHeader *hdr = reinterpret_cast<DevHeader *>(ws + X.L.hdr);
+        CU(cudaMemsetAsync(&hdr->cum_scored, 0, 2 * sizeof(unsigned long long), X.st));
+    }
+    if (t_ev.dev != dev) {
+        if (t_ev.a) {
+            cudaEventDestroy(t_ev.a);
+            cudaEventDestroy(t_ev.b);
+        }
+        CU(cudaEventCreate(&t_ev.a));
+        CU(cudaEventCreate(&t_ev.b));
+        t_ev.dev = dev;
+    }
+    CU(cudaEventRecord(t_ev.a, X.st));
     if (use_coarse(X, prune)) {
         // incumbent: exact optimum of coarse quota sub-grids, coarsest first (each
         // pass seeds the next); replicated on every rank
@@ -630,8 +645,10 @@ int local_search(const Ctx &X, const camelot_exec *ex, int policy, int nlev, lon
             CU(cudaMemcpyAsync(inc, result, nlev * sizeof(Slot), cudaMemcpyDeviceToDevice, X.st));
         }
     }
-    rc = search_pass(X, dev, policy, nlev, prune, 1, inc, result, keys, ex->rank, ex->world, lo, hi, true);
+    rc = search_pass(X, dev, policy, nlev, prune, 1, inc, result, keys, ex->rank, ex->world, lo, hi, false);
     if (rc) return rc;
+    CU(cudaEventRecord(t_ev.b, X.st));
+    t_ev.armed = true;
     CU(cudaMemcpyAsync(ws + X.L.hdr2, ws + X.L.hdr, sizeof(DevHeader), cudaMemcpyDeviceToDevice, X.st));
     return CAMELOT_OK;
 }
@@ -834,8 +851,9 @@ int camelot_score_range(const camelot_problem *p, const camelot_cluster *c, uint
 
 uint64_t camelot_kernel_launches(void) { return g_launches.load(); }
 
-int camelot_last_stats(const camelot_exec *ex, uint64_t *out6) {
-    if (!ex || !out6 || !ex->workspace) return fail(CAMELOT_EINVAL, "null argument");
+int camelot_last_stats(const camelot_exec *ex, uint64_t *out8) {
+    if (!ex || !out8 || !ex->workspace) return fail(CAMELOT_EINVAL, "null argument");
+    uint64_t *out6 = out8;
     float ms = 0.0f;
     if (t_ev.armed) {
         CU(cudaEventSynchronize(t_ev.b));
@@ -852,6 +870,8 @@ int camelot_last_stats(const camelot_exec *ex, uint64_t *out6) {
     out6[3] = (uint64_t)((double)ms * 1e6);
     out6[4] = h.items_total;
     out6[5] = t_call_launches;
+    out8[6] = h.cum_scored;
+    out8[7] = h.cum_nodes;
     return CAMELOT_OK;
 }
 

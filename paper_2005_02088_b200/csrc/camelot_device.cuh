@@ -76,6 +76,8 @@ struct DevHeader {
     unsigned long long best_packed;      // (objective key << 32) | (index >> xshift), atomicMin (1 level)
     unsigned long long head[NMAX + 1];   // pop counter of pass j
     unsigned long long tail[NMAX + 1];   // size of the frontier at depth j (may exceed capacity)
+    // cumulative over the incumbent cascade + main search of one call (not reset per pass)
+    unsigned long long cum_scored, cum_nodes;
 };
 
 struct Slot {                      // (objective key, canonical index), smaller is better

@@ -1029,6 +1029,8 @@ search_kernel(const DevProb P, const SearchArgs S) {
         atomicAdd(&S.hdr->n_scored, cn.scored);
         atomicAdd(&S.hdr->n_feasible, cn.feasible);
         atomicAdd(&S.hdr->n_nodes, cn.nodes);
+        atomicAdd(&S.hdr->cum_scored, cn.scored);
+        atomicAdd(&S.hdr->cum_nodes, cn.nodes);
         atomicOr(&S.hdr->viol_or, cn.viol);
     }
 }
