@@ -133,6 +133,8 @@ def main():
     ap.add_argument("--ref-seconds", type=float, default=8.0, help="--impl reference seconds per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-flat", action="store_true", help="skip the flat-scan roofline leg")
+    ap.add_argument("--flat-config", type=int, default=6, help="config of the flat scan (6 = C4r)")
     args = ap.parse_args()
     assert args.warmup >= 3 or args.impl == "reference", "timing rules: >= 3 warm-up steps"
 
@@ -270,6 +272,34 @@ def main():
             "kernel_share_of_step": (k_ns / 1e6) / ms_step if ms_step else None,
             "peak_note": f"{n_sm} SMs x 4 SMSP x 32 lanes x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)"}
 
+    # flat exhaustive scan (NO_FILTER: every candidate placed and scored, no
+    # pruning) of C4r: the sustained hot loop, for the issue-roofline view
+    flat = None
+    if not args.no_flat and rank == 0:
+        fp = G.config_problems(args.flat_config)[0]
+        fs = api.Session(fp, device=local, flags=fp.flags | L.F_NO_FILTER)
+        fs.plan_max_load()
+        fts, fev, fsc = [], [], []
+        for _ in range(3):
+            fr = fs.plan_max_load()
+            st = fs.last_stats()
+            fts.append(st["t_ns"])
+            fev.append(st["cum_scored"] + st["cum_nodes"])
+            fsc.append(st["cum_scored"])
+        ft = statistics.median(fts) * 1e-9
+        fnt = 1
+        for _ in range(fp.n_apps):
+            fnt *= len(fp.batch)
+        for _ in range(fp.n_stages):
+            fnt *= fp.max_replicas * len(fp.quota_pct)
+        fops = algorithmic_ops_per_eval(fp)
+        fach = fops * statistics.median(fev) / ft / 1e12
+        flat = {"workload": f"{fp.name} max-load, NO_FILTER exhaustive scan ({fnt:.4g} candidates)",
+                "index": fr.index, "ms": ft * 1e3, "candidates_per_s": fnt / ft,
+                "leaves_scored_per_s": statistics.median(fsc) / ft,
+                "roofline": {"bound": "alu", "achieved": fach, "peak": peak, "unit": "Tops/s",
+                             "frac": fach / peak, "ops_per_eval": fops}}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         r = cpu_reference_leg(prob, args, rank, world, as_main=False)
@@ -288,7 +318,8 @@ def main():
                                        "quota_pct": pm.quota_pct, "batch": pm.batch},
                           "min_resource": {"index": pr.index, "gpus_used": pr.gpus_used,
                                            "quota_used": pr.quota_used, "load": LOW_LOAD * pm.objective}},
-                "scored_per_step": evals, "gpu_launches": launches, "roofline": roof, "clocks": clocks,
+                "scored_per_step": evals, "gpu_launches": launches, "roofline": roof, "flat_scan": flat,
+                "clocks": clocks,
                 "e2e": e2e, "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -13,7 +13,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "libcamelot.so")
+LIB = os.environ.get("CAMELOT_LIB") or os.path.join(HERE, "libcamelot.so")   # override: experiments only
 HEADER = os.path.join(ROOT, "include", "camelot.h")
 
 MAX_STAGES, MAX_APPS, MAX_GPUS, MAX_REPLICAS, MAX_LOADS = 8, 2, 16, 16, 64

@@ -26,6 +26,9 @@ namespace cam {
 
 constexpr int SEARCH_THREADS = 256;
 constexpr int SEARCH_WARPS = SEARCH_THREADS / 32;
+#ifndef SEARCH_MINB
+#define SEARCH_MINB 2   // measured: 128 regs x 2 CTAs beats 200 regs x 1 CTA (C4 2.8 vs 3.3 ms)
+#endif
 
 struct SearchArgs {
     int policy;                 // 0 max-load, 1 min-resource
@@ -58,16 +61,14 @@ struct SearchArgs {
     int xshift;                 // index >> xshift fits 32 bits (tie pruning key)
 };
 
-// Placement state after the first j stages, in shared memory (one per DFS
-// level per warp).  GPU arrays are indexed by GPU id (g*) and by position in
-// the deployment order for the NEXT stage (p*: sorted by remaining memory,
-// remaining quota, index -- PAPER.md L929-942).
+// Placement state after the first j stages (shared-memory DFS stack and the
+// global frontier).  Per-GPU arrays are stored in POSITION order of the
+// deployment order for the NEXT stage (sorted by remaining memory, remaining
+// quota, index -- PAPER.md L929-942); pgid maps a position to its GPU id.
 template <int CM>
 struct Node {
-    int grq[CM], gcnt[CM];
-    uint32_t grm[CM];
-    float gdem[CM];
-    int prq[CM], pkim[CM], pgid[CM];
+    int prq[CM], pcnt[CM], pkim[CM], pgid[CM];
+    uint32_t prm[CM];
     float pdem[CM];
     float dur[NMAX], bw[NMAX], nt[NMAX], dmax[NMAX];
     uint32_t hmask[NMAX];
@@ -132,8 +133,9 @@ __device__ __forceinline__ uint32_t place_fail_bits(const DevProb &P, const Node
     for (int q = 0; q < P.C; ++q) {
         if ((int)r.p > nd.prq[q]) v |= V_QUOTA;
         int g = nd.pgid[q];
-        if (nd.gcnt[g] + 1 > P.I) v |= V_INST;
-        if (r.W + r.As > nd.grm[g]) v |= V_MEM;
+        (void)g;
+        if (nd.pcnt[q] + 1 > P.I) v |= V_INST;
+        if (r.W + r.As > nd.prm[q]) v |= V_MEM;
         if (!(P.flags & F_NO_BW_CAP) && __fadd_rn(nd.pdem[q], r.bw) > P.BW) v |= V_BW;
     }
     return v ? v : V_QUOTA;
@@ -177,7 +179,7 @@ __device__ __forceinline__ void eval_child(const DevProb &P, const SearchArgs &S
             float d = __fadd_rn(nd.pdem[q], __fmul_rn((float)kpos[q], r.bw));
             dself = fmaxf(dself, d);
             int g = nd.pgid[q];
-            unew += nd.gcnt[g] == 0;
+            unew += nd.pcnt[q] == 0;
 #pragma unroll
             for (int i = 0; i < NMAX; ++i)
                 if (i < j && ((nd.hmask[i] >> g) & 1u)) dm[i] = fmaxf(dm[i], d);
@@ -227,10 +229,10 @@ __device__ void build_child(const DevProb &P, const SearchArgs &S, const Node<CM
     uint32_t rm = 0;
     float dem = 0.0f;
     if (lane < P.C) {
-        rq = nd.grq[g] - k * (int)r.p;
-        cnt = nd.gcnt[g] + k;
-        rm = nd.grm[g] - (k > 0 ? r.W + (uint32_t)k * r.As : 0u);
-        dem = k > 0 ? __fadd_rn(nd.gdem[g], __fmul_rn((float)k, r.bw)) : nd.gdem[g];
+        rq = nd.prq[lane] - k * (int)r.p;
+        cnt = nd.pcnt[lane] + k;
+        rm = nd.prm[lane] - (k > 0 ? r.W + (uint32_t)k * r.As : 0u);
+        dem = k > 0 ? __fadd_rn(nd.pdem[lane], __fmul_rn((float)k, r.bw)) : nd.pdem[lane];
     }
     unsigned used = __ballot_sync(0xffffffffu, lane < P.C && k > 0);
     // host mask of the new stage (GPU ids)
@@ -272,11 +274,9 @@ __device__ void build_child(const DevProb &P, const SearchArgs &S, const Node<CM
     }
     __syncwarp();
     if (lane < P.C) {
-        out.grq[g] = rq;
-        out.gcnt[g] = cnt;
-        out.grm[g] = rm;
-        out.gdem[g] = dem;
         out.prq[rank] = rq;
+        out.pcnt[rank] = cnt;
+        out.prm[rank] = rm;
         out.pkim[rank] = kim;
         out.pgid[rank] = g;
         out.pdem[rank] = dem;
@@ -289,7 +289,7 @@ __device__ void build_child(const DevProb &P, const SearchArgs &S, const Node<CM
         out.kidx[lane] = nd.kidx[lane];
     }
     if (lane <= j) out.dmax[lane] = dmi;
-    unsigned unew = __popc(__ballot_sync(0xffffffffu, lane < P.C && k > 0 && nd.gcnt[g] == 0));
+    unsigned unew = __popc(__ballot_sync(0xffffffffu, lane < P.C && k > 0 && nd.pcnt[lane] == 0));
     if (lane == 0) {
         out.dur[j] = r.dur;
         out.bw[j] = r.bw;
@@ -323,10 +323,8 @@ __device__ void build_root(const DevProb &P, int bc, Node<CM> &out, int lane) {
     __syncwarp();
     if (lane < P.C) {
         const int g = lane;
-        out.grq[g] = P.R;
-        out.gcnt[g] = 0;
-        out.grm[g] = P.FM;
-        out.gdem[g] = 0.0f;
+        out.pcnt[g] = 0;
+        out.prm[g] = P.FM;
         // all GPUs equal: order = index
         const uint32_t W0 = P.W[0], As0 = P.Am[0] * (uint32_t)P.S[b[P.app[0]]];
         int km = P.Rmax;
@@ -472,7 +470,7 @@ __device__ __forceinline__ void load_ctx(const DevProb &P, const SearchArgs &S, 
         c.prq[q] = in ? nd.prq[q] : 0;
         c.pkim[q] = in ? nd.pkim[q] : 0;
         c.pdem[q] = in ? nd.pdem[q] : 0.0f;
-        if (in && nd.gcnt[nd.pgid[q]] == 0) c.empty |= 1u << q;
+        if (in && nd.pcnt[q] == 0) c.empty |= 1u << q;
     }
 #pragma unroll
     for (int i = 0; i < NS; ++i) {
@@ -555,6 +553,35 @@ struct FastEval {
 // Place stage j with option r on the context and score it (branch-free
 // placement: per-position capacities K_q = canHold(q, N); pass 1 = first q with
 // K_q == N; pass 2 = greedy min(K_q, remaining) -- DESIGN.md 3.2, R14).
+template <int CM, int NS>
+__device__ __forceinline__ bool fast_place(const DevProb &P, const PCtx<CM, NS> &c, const OptRec &r, int (&kk)[CM]) {
+    const int N = (int)r.N;
+    const bool cap = !(P.flags & F_NO_BW_CAP);
+    int K[CM];
+#pragma unroll
+    for (int q = 0; q < CM; ++q) {
+        int k = min(min(N, (int)(((uint32_t)c.prq[q] * r.pmul) >> 16)), c.pkim[q]);
+        if (cap && k > 0 && __fadd_rn(c.pdem[q], __fmul_rn((float)k, r.bw)) > P.BW) {
+            do {
+                --k;
+            } while (k > 0 && __fadd_rn(c.pdem[q], __fmul_rn((float)k, r.bw)) > P.BW);
+        }
+        K[q] = k;
+    }
+    int jstar = CM;
+#pragma unroll
+    for (int q = CM - 1; q >= 0; --q)
+        if (K[q] == N) jstar = q;
+    int rem = N;
+#pragma unroll
+    for (int q = 0; q < CM; ++q) {
+        const int g = min(K[q], rem);
+        rem -= g;
+        kk[q] = (jstar < CM) ? (q == jstar ? N : 0) : g;
+    }
+    return (jstar < CM) || rem == 0;
+}
+
 template <int CM, int NS>
 __device__ __forceinline__ void fast_eval(const DevProb &P, const PCtx<CM, NS> &c, int j, const OptRec &r,
                                           FastEval &fe) {
@@ -754,6 +781,121 @@ __device__ __forceinline__ void copy_node(Node<CM> &dst, const Node<CM> &src, in
     __syncwarp();
 }
 
+// Ownership of the child (stage j, option index kopt) of nd at depth S.d0 = j+1.
+template <int CM>
+__device__ __forceinline__ bool owns_child(const DevProb &P, const SearchArgs &S, const Node<CM> &nd, int j,
+                                           int kopt) {
+    unsigned long long it = 0;
+    for (int i = 0; i <= j; ++i)
+        it = it * sb_at(P, S, i, nd.b[P.app[i]]).cnt + (unsigned long long)(i < j ? nd.kidx[i] : kopt);
+    const unsigned long long chunk = (S.item_off[nd.bc] + it) / (unsigned long long)S.chunk_items;
+    if (chunk < S.chunk_lo) return false;
+    if (S.chunk_hi && chunk >= S.chunk_hi) return false;
+    return (chunk % (unsigned long long)S.world) == (unsigned long long)S.rank;
+}
+
+// One lane builds its own surviving child (stage j placed with option r) and
+// writes it to the global frontier: the same state as build_child (warp
+// version), computed independently per lane so that all survivors of a batch
+// are emitted in parallel.
+template <int CM, int NS>
+__device__ __forceinline__ void emit_child(const DevProb &P, const Node<CM> &nd, const PCtx<CM, NS> &c, int j,
+                                           const OptRec &r, uint32_t p, uint32_t W, uint32_t As, int kopt,
+                                           Node<CM> *out) {
+    int kk[CM];
+    fast_place<CM, NS>(P, c, r, kk);
+    int rq[CM], cnt[CM], g[CM];
+    uint32_t rm[CM];
+    float dem[CM];
+    unsigned hm = 0;
+    int unew = 0;
+    float dself = 0.0f;
+#pragma unroll
+    for (int q = 0; q < CM; ++q) {
+        rq[q] = 0;
+        cnt[q] = 0;
+        g[q] = 0;
+        rm[q] = 0;
+        dem[q] = 0.0f;
+        if (q < P.C) {
+            const int k = kk[q];
+            g[q] = nd.pgid[q];
+            rq[q] = c.prq[q] - k * (int)p;
+            cnt[q] = nd.pcnt[q] + k;
+            rm[q] = nd.prm[q] - (k > 0 ? W + (uint32_t)k * As : 0u);
+            dem[q] = k > 0 ? __fadd_rn(c.pdem[q], __fmul_rn((float)k, r.bw)) : c.pdem[q];
+            if (k > 0) {
+                hm |= 1u << g[q];
+                unew += nd.pcnt[q] == 0;
+                dself = fmaxf(dself, dem[q]);
+            }
+        }
+    }
+    const bool more = j + 1 < P.n;
+    uint32_t W2 = 0, As2 = 0;
+    if (more) {
+        const int i2 = j + 1;
+        W2 = P.W[i2];
+        As2 = P.Am[i2] * (uint32_t)P.S[nd.b[P.app[i2]]];
+    }
+#pragma unroll
+    for (int q = 0; q < CM; ++q) {
+        if (q < P.C) {
+            int rank = 0;
+#pragma unroll
+            for (int h = 0; h < CM; ++h)
+                if (h < P.C && h != q) {
+                    const bool lt = rm[h] < rm[q] || (rm[h] == rm[q] && (rq[h] < rq[q] || (rq[h] == rq[q] && g[h] < g[q])));
+                    rank += lt ? 1 : 0;
+                }
+            int kim = 0;
+            if (more) {
+                int km = P.Rmax;
+                if (rm[q] < W2) km = 0;
+                else if (As2 > 0) km = (int)min((uint32_t)P.Rmax, (rm[q] - W2) / As2);
+                kim = max(0, min(km, min(P.Rmax, P.I - cnt[q])));
+            }
+            out->prq[rank] = rq[q];
+            out->pcnt[rank] = cnt[q];
+            out->prm[rank] = rm[q];
+            out->pkim[rank] = kim;
+            out->pgid[rank] = g[q];
+            out->pdem[rank] = dem[q];
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < NS; ++i) {
+        if (i < j) {
+            float dm = nd.dmax[i];
+            const unsigned hmi = nd.hmask[i];
+#pragma unroll
+            for (int q = 0; q < CM; ++q)
+                if (q < P.C && kk[q] > 0 && ((hmi >> g[q]) & 1u)) dm = fmaxf(dm, dem[q]);
+            out->dur[i] = nd.dur[i];
+            out->bw[i] = nd.bw[i];
+            out->nt[i] = nd.nt[i];
+            out->dmax[i] = dm;
+            out->hmask[i] = hmi;
+            out->kidx[i] = nd.kidx[i];
+        } else if (i == j) {
+            out->dur[i] = r.dur;
+            out->bw[i] = r.bw;
+            out->nt[i] = r.NT;
+            out->dmax[i] = dself;
+            out->hmask[i] = hm;
+            out->kidx[i] = kopt;
+        }
+    }
+    out->x = nd.x * (unsigned long long)P.O + r.code;
+    out->U = nd.U + (int)r.NP;
+    out->u = nd.u + unew;
+    out->rqsum = nd.rqsum - (int)r.NP;
+    out->bc = nd.bc;
+    out->b[0] = nd.b[0];
+    out->b[AMAX - 1] = nd.b[AMAX - 1];
+    out->tub = fminf(nd.tub, r.NT);
+}
+
 // Generic depth-first walk below stack[jtop] (no frontier): the fallback when
 // the frontier is full.  Same arithmetic as the fast path (eval_child).
 template <int CM, int POLICY>
@@ -828,7 +970,7 @@ __device__ void dfs_generic(const DevProb &P, const SearchArgs &S, Node<CM> *sta
 // (generic inline depth-first descent when the frontier is full); leaves are
 // scored exactly.
 template <int CM, int NS, int POLICY>
-__global__ void __launch_bounds__(SEARCH_THREADS)
+__global__ void __launch_bounds__(SEARCH_THREADS, SEARCH_MINB)
 search_kernel(const DevProb P, const SearchArgs S) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -983,23 +1125,27 @@ search_kernel(const DevProb P, const SearchArgs S) {
                         sv = (unsigned long long)objkey_minres(max(fe.u, (Ulb + P.R - 1) / P.R), Ulb) <= wb->bound;
                     }
                 }
+                if (sv && jtop + 1 == S.d0) sv = owns_child<CM>(P, S, nd, jtop, opt);
                 unsigned m = __ballot_sync(0xffffffffu, sv);
+                if (m && jtop + 1 == S.flevel) {
+                    // every surviving lane emits its own child into the frontier
+                    unsigned long long fbase = 0;
+                    if (lane == 0) fbase = atomicAdd(S.out_tail, (unsigned long long)__popc(m));
+                    fbase = __shfl_sync(0xffffffffu, fbase, 0);
+                    const unsigned long long slot = fbase + __popc(m & ((1u << lane) - 1u));
+                    const bool fits = sv && slot < S.out_cap;
+                    if (fits) {
+                        const OptRec &full = list[opt];
+                        emit_child<CM, NS>(P, nd, c, jtop, r, full.p, full.W, full.As, opt, outf + slot);
+                    }
+                    m = __ballot_sync(0xffffffffu, sv && !fits);   // frontier full: serial fallback
+                }
                 while (m) {
                     const int src = __ffs(m) - 1;
                     m &= m - 1;
                     const int o2 = base + src;
                     build_child<CM>(P, S, stack[jtop], jtop, list[o2], o2, stack[jtop + 1], lane);
-                    if (jtop + 1 == S.d0 && !owns<CM>(P, S, stack[jtop + 1])) continue;
-                    if (jtop + 1 == S.flevel) {
-                        unsigned long long slot = 0;
-                        if (lane == 0) slot = atomicAdd(S.out_tail, 1ull);
-                        slot = __shfl_sync(0xffffffffu, slot, 0);
-                        if (slot < S.out_cap) {
-                            copy_node<CM>(outf[slot], stack[jtop + 1], lane);
-                            continue;
-                        }
-                    }
-                    // frontier full: walk the child's subtree here
+                    // walk the child's subtree here
                     dfs_generic<CM, POLICY>(P, S, stack, ctl, wb, jtop + 1, lane, cn);
                 }
             }
