@@ -1,24 +1,24 @@
-// camelot_search.cuh -- the exact, pruned, warp-cooperative allocation search
-// (kernels N1 search, N3 option filter) for sm_100a.
+// camelot_search.cuh -- the exact, pruned allocation search (kernel N1) for
+// sm_100a.
 //
-// Search order.  The candidate space is the tree  beta-combo -> stage 1 option
-// -> ... -> stage n option  (option = (N_i, p_i); batch
-// L858).  The top d0 stage levels are flattened into "items" that lanes
-// evaluate independently; below, a warp walks the tree depth-first: at each
-// node all 32 lanes evaluate 32 children (the next stage's options) in
-// parallel against the node's placement state (held once in shared memory),
-// ballot the survivors and descend into them in order.  Leaves (the last
-// stage) are scored exactly and reduced into the warp's best (objective key,
-// canonical index).
+// Search order.  The candidate space is the tree  batch combo -> stage-1 option
+// -> ... -> stage-n option  (option = (N_i, p_i); batch
+// L858).  It is expanded LEVEL-SYNCHRONOUSLY: pass j pops parents (placement
+// state after stages 0..j-1) from a global frontier with one atomic per parent,
+// hoists the parent into registers, and the 32 lanes of a warp evaluate 32
+// children (stage-j options) at a time: placement, contention, latency sums,
+// bounds.  Every surviving child is written by its own lane to the next
+// frontier; when the frontier is full the warp descends inline (explicit
+// per-warp stack, same evaluator).  Leaves (last stage) are scored exactly and
+// reduced into the warp's best (objective key, canonical index).
 //
-// Pruning.  A child is dropped only if every
-// candidate below it is infeasible or strictly worse than a candidate already
-// known to be feasible (the incumbent / best so far): placement failure of the
-// placed prefix; QoS lower bound (contention only grows as stages are added,
-// so the ordered fp32 latency sum of the current latencies plus the minimum
-// durations of the unplaced stages is a lower bound); throughput upper bound
-// (T_i <= fl(N_i thr_i)); quota left; min-resource key lower bound.  Ties are
-// never pruned, so the smallest index among optimal candidates survives.
+// Pruning.  A child is dropped only if no candidate below it
+// can be feasible and at least as good as a feasible candidate already known
+// (incumbent / best so far): failed placement of the prefix; QoS lower bound
+// (contention only grows, ordered fp32 sums are monotone); throughput upper
+// bound (T_i <= fl(N_i thr_i) / kappa_i(current)); quota left; min-resource key
+// lower bound; ties by index (a subtree that can at best tie and lies entirely
+// above the best's index).  Strictly better keys are never pruned.
 #pragma once
 #include "camelot_device.cuh"
 
@@ -81,9 +81,10 @@ struct Node {
 
 // per-warp DFS bookkeeping (shared memory)
 struct WarpCtl {
-    int cur[NMAX];
-    int base[NMAX];
-    unsigned msk[NMAX];
+    int cur[NMAX];     // next child batch of the node at each depth
+    int end[NMAX];     // end of that node's child range
+    int base[NMAX];    // first child of the batch whose survivors are pending
+    unsigned msk[NMAX];   // pending (inline-descent) survivors of that batch
 };
 
 // ---------------------------------------------------------------- placement of one stage
@@ -146,69 +147,6 @@ __device__ __forceinline__ const OptRec &opt_at(const DevProb &P, const SearchAr
 }
 __device__ __forceinline__ const StageBound &sb_at(const DevProb &P, const SearchArgs &S, int i, int b) {
     return S.sb[(size_t)i * P.nS + b];
-}
-
-// Child evaluation of stage j (option r) on node nd, by one lane.
-// Computes everything needed for (a) the bound test of an inner node, or (b)
-// the exact leaf score.  Returns false if the placement fails.
-struct ChildEval {
-    bool placed;
-    float lsum[AMAX];     // exact (leaf) or lower bound (inner)
-    float kap[NMAX];      // contention factors of placed stages 0..j
-    int u, U;
-    unsigned long long x;
-};
-
-template <int CM>
-__device__ __forceinline__ void eval_child(const DevProb &P, const SearchArgs &S, const Node<CM> &nd, int j,
-                                           const OptRec &r, ChildEval &ce) {
-    int kpos[CM];
-    ce.placed = place_stage<CM>(P, nd, r, kpos);
-    ce.x = nd.x * (unsigned long long)P.O + r.code;
-    ce.U = nd.U + (int)r.NP;
-    if (!ce.placed) return;
-    // demand after this stage on the GPUs it uses; update max demand of hosts
-    float dm[NMAX];
-#pragma unroll
-    for (int i = 0; i < NMAX; ++i) dm[i] = (i < j) ? nd.dmax[i] : 0.0f;
-    float dself = 0.0f;
-    int unew = 0;
-#pragma unroll
-    for (int q = 0; q < CM; ++q) {
-        if (kpos[q] > 0) {
-            float d = __fadd_rn(nd.pdem[q], __fmul_rn((float)kpos[q], r.bw));
-            dself = fmaxf(dself, d);
-            int g = nd.pgid[q];
-            unew += nd.pcnt[q] == 0;
-#pragma unroll
-            for (int i = 0; i < NMAX; ++i)
-                if (i < j && ((nd.hmask[i] >> g) & 1u)) dm[i] = fmaxf(dm[i], d);
-        }
-    }
-    ce.u = nd.u + unew;
-    // contention factors and ordered latency sums (lower bound for unplaced stages)
-#pragma unroll
-    for (int a = 0; a < AMAX; ++a) ce.lsum[a] = 0.0f;
-    const int b0 = nd.b[0], b1 = nd.b[AMAX - 1];
-#pragma unroll
-    for (int i = 0; i < NMAX; ++i) {
-        if (i >= P.n) break;
-        float L;
-        if (i < j) {
-            float k = kappa_of(dm[i], nd.bw[i], P.gamma[i], P.invBW, P.flags);
-            ce.kap[i] = k;
-            L = __fmul_rn(nd.dur[i], k);
-        } else if (i == j) {
-            float k = kappa_of(dself, r.bw, P.gamma[i], P.invBW, P.flags);
-            ce.kap[i] = k;
-            L = __fmul_rn(r.dur, k);
-        } else {
-            L = sb_at(P, S, i, P.app[i] == 0 ? b0 : b1).mindur;
-        }
-        int a = P.app[i];
-        if (i == P.first_of_app[a]) ce.lsum[a] = L;
-        else ce.lsum[a] = __fadd_rn(ce.lsum[a], L);
-    }
 }
 
 // ---------------------------------------------------------------- node construction
@@ -378,46 +316,6 @@ __device__ __forceinline__ void publish_best(const SearchArgs &S, WarpBest *wb) 
         wb->gpack = pk;
         atomicMin(&S.hdr->best_packed, pk);
     }
-}
-
-// key lower bound of any completion of a child at stage j (inner node)
-template <int CM>
-__device__ __forceinline__ unsigned int child_keylb(const DevProb &P, const SearchArgs &S, const Node<CM> &nd, int j,
-                                                    const OptRec &r, const ChildEval &ce, float restT, int restU) {
-    if (S.policy == 0) {
-        float tub = fminf(fminf(nd.tub, r.NT), restT);
-        return objkey_maxload(tub);
-    }
-    int Ulb = ce.U + restU;
-    int ulb = max(ce.u, (Ulb + P.R - 1) / P.R);
-    return objkey_minres(ulb, Ulb);
-}
-
-// inner-node survival test for child (stage j, option r) of nd; exact bounds only
-template <int CM>
-__device__ __forceinline__ bool inner_survives(const DevProb &P, const SearchArgs &S, const Node<CM> &nd, int j,
-                                               const OptRec &r, const ChildEval &ce, unsigned long long bound) {
-    if (!ce.placed) return false;
-    const int n = P.n;
-    const unsigned long long span = P.opow[n - 1 - j];
-    const unsigned long long xs = ce.x * span;
-    if (xs >= S.hi || xs + span <= S.lo) return false;
-    if (!S.prune) return true;
-    bool ok = true;
-    for (int a = 0; a < P.A; ++a) ok &= ce.lsum[a] <= P.qos[a];
-    float restT = __int_as_float(0x7f800000);
-    int restU = 0;
-    for (int i2 = j + 1; i2 < n; ++i2) {
-        const StageBound &bb = sb_at(P, S, i2, nd.b[P.app[i2]]);
-        restT = fminf(restT, bb.maxNT);
-        restU += (int)bb.minNP;
-    }
-    if (nd.rqsum - (int)r.NP < restU) ok = false;
-    if (ok) {
-        unsigned kl = child_keylb<CM>(P, S, nd, j, r, ce, restT, restU);
-        if ((unsigned long long)kl > bound) ok = false;
-    }
-    return ok;
 }
 
 // warp-wide min of (key, x) over lanes with imp set; updates slot k of wb
@@ -896,73 +794,6 @@ __device__ __forceinline__ void emit_child(const DevProb &P, const Node<CM> &nd,
     out->tub = fminf(nd.tub, r.NT);
 }
 
-// Generic depth-first walk below stack[jtop] (no frontier): the fallback when
-// the frontier is full.  Same arithmetic as the fast path (eval_child).
-template <int CM, int POLICY>
-__device__ void dfs_generic(const DevProb &P, const SearchArgs &S, Node<CM> *stack, WarpCtl *ctl, WarpBest *wb,
-                            int jtop, int lane, Counters &cn) {
-    const int n = P.n;
-    int j = jtop;
-    if (lane == 0) {
-        ctl->cur[j] = 0;
-        ctl->msk[j] = 0;
-    }
-    __syncwarp();
-    while (true) {
-        const Node<CM> &nd = stack[j];
-        const int bj = nd.b[P.app[j]];
-        const int cntj = (int)sb_at(P, S, j, bj).cnt;
-        const unsigned msk = ctl->msk[j];
-        if (msk) {
-            const int kk = __ffs(msk) - 1;
-            const int opt = ctl->base[j] + kk;
-            __syncwarp();
-            if (lane == 0) ctl->msk[j] = msk & (msk - 1);
-            build_child<CM>(P, S, nd, j, opt_at(P, S, j, bj, opt), opt, stack[j + 1], lane);
-            if (j + 1 == S.d0 && !owns<CM>(P, S, stack[j + 1])) continue;
-            ++j;
-            if (lane == 0) {
-                ctl->cur[j] = 0;
-                ctl->msk[j] = 0;
-            }
-            __syncwarp();
-            continue;
-        }
-        const int cur = ctl->cur[j];
-        if (cur >= cntj) {
-            if (j == jtop) break;
-            --j;
-            continue;
-        }
-        __syncwarp();
-        if (lane == 0) {
-            ctl->base[j] = cur;
-            ctl->cur[j] = cur + 32;
-        }
-        __syncwarp();
-        const int opt = cur + lane;
-        const bool valid = opt < cntj;
-        const OptRec &r = opt_at(P, S, j, bj, valid ? opt : cur);
-        ChildEval ce;
-        if (valid) eval_child<CM>(P, S, nd, j, r, ce);
-        else ce.placed = false;
-        if (j < n - 1) {
-            cn.nodes += valid;
-            const bool sv = valid && inner_survives<CM>(P, S, nd, j, r, ce, wb->bound);
-            const unsigned m = __ballot_sync(0xffffffffu, sv);
-            if (lane == 0) ctl->msk[j] = m;
-            __syncwarp();
-            continue;
-        }
-        const bool inr = valid && ce.x >= S.lo && ce.x < S.hi;
-        if (!S.prune && inr && !ce.placed) cn.viol |= place_fail_bits<CM>(P, nd, r);
-        const int jj = j;
-        auto nt = [&](int i) { return i < jj ? nd.nt[i] : r.NT; };
-        score_leaf<POLICY, NMAX>(P, S, wb, lane, inr, ce.placed, ce.lsum, ce.kap, nt, fminf(nd.tub, r.NT), ce.u,
-                                 ce.U, nd.bc, ce.x, cn);
-    }
-}
-
 // ---------------------------------------------------------------- the search kernel
 // One level-synchronous pass: warps pop parents (dynamic, `grab` at a time),
 // hoist the parent into registers, lanes evaluate its children 32 at a time;
@@ -999,12 +830,10 @@ search_kernel(const DevProb P, const SearchArgs S) {
     Counters cn = {0, 0, 0, 0};
     const int n = P.n;
     const int jtop = S.level;
-    const bool leaf = jtop == n - 1;
     const Node<CM> *in = reinterpret_cast<const Node<CM> *>(S.in_nodes);
     Node<CM> *outf = reinterpret_cast<Node<CM> *>(S.out_nodes);
     const unsigned long long count = in ? min(*(volatile const unsigned long long *)S.in_count, S.in_cap)
                                         : (unsigned long long)P.nbc;
-    const unsigned long long span = P.opow[n - 1 - jtop];
     // few parents (shallow passes): each block of 32 children is its own work item
     const int nblk = (P.O + 31) / 32;
     const int split = (count < 4ull * gridDim.x * SEARCH_WARPS) ? nblk : 1;
@@ -1033,27 +862,83 @@ search_kernel(const DevProb P, const SearchArgs S) {
             } else {
                 copy_node<CM>(stack[jtop], in[e], lane);
             }
-            const Node<CM> &nd = stack[jtop];
-            PCtx<CM, NS> c;
-            load_ctx<CM, NS>(P, S, nd, jtop, c);
-            // parent re-check against the current bound (it may have tightened)
-            if (S.prune) {
-                unsigned long long kl;
-                if (POLICY == 0) kl = objkey_maxload(fminf(c.tub, fminf(sb_at(P, S, jtop, nd.b[P.app[jtop]]).maxNT, c.restT)));
-                else {
-                    const int Ulb = c.U + (int)sb_at(P, S, jtop, nd.b[P.app[jtop]]).minNP + c.restU;
-                    kl = objkey_minres(max(c.u, (Ulb + P.R - 1) / P.R), Ulb);
+            {
+                const int cnt0 = (int)sb_at(P, S, jtop, stack[jtop].b[P.app[jtop]]).cnt;
+                __syncwarp();
+                if (lane == 0) {
+                    ctl->cur[jtop] = split > 1 ? blk * 32 : 0;
+                    ctl->end[jtop] = split > 1 ? min(cnt0, blk * 32 + 32) : cnt0;
+                    ctl->msk[jtop] = 0;
                 }
-                if (!can_win(kl, c.x * P.opow[n - jtop], wb, nlev, S.xshift)) continue;
+                __syncwarp();
             }
-            const int bj = nd.b[P.app[jtop]];
-            const int cnt = (int)sb_at(P, S, jtop, bj).cnt;
-            const OptRec *list = S.rec + ((size_t)jtop * P.nS + bj) * P.O;
-            const int b_lo = split > 1 ? blk * 32 : 0;
-            const int b_hi = split > 1 ? min(cnt, b_lo + 32) : cnt;
-            for (int base = b_lo; base < b_hi; base += 32) {
+            // ---- explicit-stack walk: normally one level (survivors go to the
+            // frontier); inline descents (frontier full) use the same fast path
+            int j = jtop;
+            bool reload = true;
+            PCtx<CM, NS> c;
+            while (true) {
+                const Node<CM> &nd = stack[j];
+                const int bj = nd.b[P.app[j]];
+                const OptRec *list = S.rec + ((size_t)j * P.nS + bj) * P.O;
+                if (reload) {
+                    reload = false;
+                    load_ctx<CM, NS>(P, S, nd, j, c);
+                    // re-check the node against the current bound (it may have tightened)
+                    if (S.prune) {
+                        unsigned long long kl;
+                        if (POLICY == 0) kl = objkey_maxload(fminf(c.tub, fminf(sb_at(P, S, j, bj).maxNT, c.restT)));
+                        else {
+                            const int Ulb = c.U + (int)sb_at(P, S, j, bj).minNP + c.restU;
+                            kl = objkey_minres(max(c.u, (Ulb + P.R - 1) / P.R), Ulb);
+                        }
+                        if (!can_win(kl, c.x * P.opow[n - j], wb, nlev, S.xshift)) {
+                            __syncwarp();
+                            if (lane == 0) {
+                                ctl->cur[j] = ctl->end[j];
+                                ctl->msk[j] = 0;
+                            }
+                            __syncwarp();
+                        }
+                    }
+                }
+                const unsigned pend = ctl->msk[j];
+                if (pend) {
+                    // inline descent into the next pending survivor
+                    const int kk = __ffs(pend) - 1;
+                    const int o2 = ctl->base[j] + kk;
+                    __syncwarp();
+                    if (lane == 0) ctl->msk[j] = pend & (pend - 1);
+                    build_child<CM>(P, S, nd, j, list[o2], o2, stack[j + 1], lane);
+                    ++j;
+                    const int cntc = (int)sb_at(P, S, j, stack[j].b[P.app[j]]).cnt;
+                    if (lane == 0) {
+                        ctl->cur[j] = 0;
+                        ctl->end[j] = cntc;
+                        ctl->msk[j] = 0;
+                    }
+                    __syncwarp();
+                    reload = true;
+                    continue;
+                }
+                const int base = ctl->cur[j];
+                if (base >= ctl->end[j]) {
+                    if (j == jtop) break;
+                    --j;
+                    reload = true;
+                    continue;
+                }
+                const int endj = ctl->end[j];
+                __syncwarp();
+                if (lane == 0) {
+                    ctl->base[j] = base;
+                    ctl->cur[j] = base + 32;
+                }
+                __syncwarp();
+                const bool leaf = j == n - 1;
+                const unsigned long long span = P.opow[n - 1 - j];
                 const int opt = base + lane;
-                const bool valid = opt < cnt;
+                const bool valid = opt < endj;
                 OptRec r;
                 {
                     const uint4 *src = reinterpret_cast<const uint4 *>(list + (valid ? opt : base));
@@ -1086,11 +971,11 @@ search_kernel(const DevProb P, const SearchArgs S) {
                 // QoS lower bound before placement: L_j >= dur, placed stages' L
                 // only grow, unplaced stages >= their minimum duration (ordered sum)
                 if (S.prune && go) {
-                    const int aj = P.app[jtop];
+                    const int aj = P.app[j];
                     float lb = c.lpre < 0.0f ? r.dur : __fadd_rn(c.lpre, r.dur);
 #pragma unroll
                     for (int i = 0; i < NS; ++i)
-                        if (i > jtop && i < n && P.app[i] == aj) lb = __fadd_rn(lb, c.dur[i]);
+                        if (i > j && i < n && P.app[i] == aj) lb = __fadd_rn(lb, c.dur[i]);
                     go = lb <= P.qos[aj];
                 }
                 // canonical index range of the child's subtree
@@ -1100,11 +985,12 @@ search_kernel(const DevProb P, const SearchArgs S) {
                 }
                 FastEval fe;
                 fe.placed = false;
-                if (go) fast_eval<CM, NS>(P, c, jtop, r, fe);
+                if (go) fast_eval<CM, NS>(P, c, j, r, fe);
                 if (leaf) {
                     // violation diagnostics are exact (and computed) only in flat mode
                     if (!S.prune && go && !fe.placed) cn.viol |= place_fail_bits<CM>(P, nd, list[opt]);
-                    auto ntf = [&](int i) { return i < jtop ? c.nt[i] : r.NT; };
+                    const int jj = j;
+                    auto ntf = [&](int i) { return i < jj ? c.nt[i] : r.NT; };
                     score_leaf<POLICY, NS>(P, S, wb, lane, go, fe.placed, fe.lsum, fe.kap, ntf, fminf(c.tub, r.NT),
                                            fe.u, fe.U, c.bc, x, cn);
                     continue;
@@ -1117,17 +1003,18 @@ search_kernel(const DevProb P, const SearchArgs S) {
                     if (P.A > 1) sv &= fe.lsum[1] <= P.qos[1];
                     if (sv && POLICY == 0 && wb->bound < 0xFFFFFFFFull) {
                         const float Tbest = __uint_as_float(0xFFFFFFFFu - (unsigned)wb->bound);
-                        auto ntf2 = [&](int i) { return i < jtop ? c.nt[i] : r.NT; };
-                        if (t_certainly_below<NS>(P, jtop, fe.kap, ntf2, Tbest)) sv = false;
+                        const int jj = j;
+                        auto ntf2 = [&](int i) { return i < jj ? c.nt[i] : r.NT; };
+                        if (t_certainly_below<NS>(P, j, fe.kap, ntf2, Tbest)) sv = false;
                     }
                     if (sv && POLICY == 1) {
                         const int Ulb = fe.U + c.restU;
                         sv = (unsigned long long)objkey_minres(max(fe.u, (Ulb + P.R - 1) / P.R), Ulb) <= wb->bound;
                     }
                 }
-                if (sv && jtop + 1 == S.d0) sv = owns_child<CM>(P, S, nd, jtop, opt);
+                if (sv && j + 1 == S.d0) sv = owns_child<CM>(P, S, nd, j, opt);
                 unsigned m = __ballot_sync(0xffffffffu, sv);
-                if (m && jtop + 1 == S.flevel) {
+                if (m && j + 1 == S.flevel) {
                     // every surviving lane emits its own child into the frontier
                     unsigned long long fbase = 0;
                     if (lane == 0) fbase = atomicAdd(S.out_tail, (unsigned long long)__popc(m));
@@ -1136,18 +1023,13 @@ search_kernel(const DevProb P, const SearchArgs S) {
                     const bool fits = sv && slot < S.out_cap;
                     if (fits) {
                         const OptRec &full = list[opt];
-                        emit_child<CM, NS>(P, nd, c, jtop, r, full.p, full.W, full.As, opt, outf + slot);
+                        emit_child<CM, NS>(P, nd, c, j, r, full.p, full.W, full.As, opt, outf + slot);
                     }
-                    m = __ballot_sync(0xffffffffu, sv && !fits);   // frontier full: serial fallback
+                    m = __ballot_sync(0xffffffffu, sv && !fits);   // frontier full: descend inline
                 }
-                while (m) {
-                    const int src = __ffs(m) - 1;
-                    m &= m - 1;
-                    const int o2 = base + src;
-                    build_child<CM>(P, S, stack[jtop], jtop, list[o2], o2, stack[jtop + 1], lane);
-                    // walk the child's subtree here
-                    dfs_generic<CM, POLICY>(P, S, stack, ctl, wb, jtop + 1, lane, cn);
-                }
+                __syncwarp();
+                if (lane == 0) ctl->msk[j] = m;
+                __syncwarp();
             }
         }
     }

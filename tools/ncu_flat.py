@@ -1,0 +1,12 @@
+"""One flat (NO_FILTER) max-load plan of a config (ncu capture target)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from gen import problems as G  # noqa: E402
+from paper_2005_02088_b200 import _lib as L, api  # noqa: E402
+
+p = G.config_problems(int(sys.argv[1]) if len(sys.argv) > 1 else 6)[0]
+s = api.Session(p, flags=p.flags | L.F_NO_FILTER)
+r = s.plan_max_load()
+print(p.name, r.index, s.last_stats())
