@@ -411,13 +411,15 @@ int xshift_of(unsigned long long ntot) {
 }
 
 // the level-synchronous passes of one search (parents at depth 0..n-1)
-int run_passes(const Ctx &X, int dev, int policy, SearchArgs S, bool timed) {
+// `fresh`: the frontier counters and slots still have to be reset (re-scan);
+// otherwise search_pass's header reset and the fused filter already did it.
+int run_passes(const Ctx &X, int dev, int policy, SearchArgs S, bool timed, bool fresh) {
     char *ws = X.ws;
     DevHeader *hdr = S.hdr;
     int grid = 0;
     int rc = grid_any(X, policy, dev, grid);
     if (rc) return rc;
-    CU(cudaMemsetAsync(hdr->head, 0, sizeof(hdr->head) + sizeof(hdr->tail), X.st));
+    if (fresh) CU(cudaMemsetAsync(hdr->head, 0, sizeof(hdr->head) + sizeof(hdr->tail), X.st));
     if (timed) {
         if (t_ev.dev != dev) {
             if (t_ev.a) {
@@ -430,9 +432,11 @@ int run_passes(const Ctx &X, int dev, int policy, SearchArgs S, bool timed) {
         }
         CU(cudaEventRecord(t_ev.a, X.st));
     }
-    init_slots_kernel<<<(grid * S.nlev + 255) / 256, 256, 0, X.st>>>(S.slots, grid * S.nlev);
-    COUNT_LAUNCH();
-    CU(cudaGetLastError());
+    if (fresh) {
+        init_slots_kernel<<<(grid * S.nlev + 255) / 256, 256, 0, X.st>>>(S.slots, grid * S.nlev);
+        COUNT_LAUNCH();
+        CU(cudaGetLastError());
+    }
     void *buf[2] = {ws + X.L.front0, ws + X.L.front1};
     const int n = X.d.n;
     for (int j = 0; j < n; ++j) {
@@ -446,6 +450,7 @@ int run_passes(const Ctx &X, int dev, int policy, SearchArgs S, bool timed) {
         S.out_cap = X.L.fcap;
         S.head = &hdr->head[j];
         S.grab = 1;
+        S.reduce_last = j == n - 1;   // the last pass reduces the slots (fused)
         rc = launch_search_any(X, policy, S, grid);
         if (rc) return rc;
     }
@@ -458,7 +463,7 @@ int run_passes(const Ctx &X, int dev, int policy, SearchArgs S, bool timed) {
 
 int search_pass(const Ctx &X, int dev, int policy, int nlev, bool prune, int stride, const Slot *inc,
                 Slot *result, long long *keys, int rank, int world, unsigned long long lo, unsigned long long hi,
-                bool timed) {
+                bool timed, Slot *inc_out = nullptr) {
     char *ws = X.ws;
     if (X.naive)
         return flat_pass(X, dev, policy, nlev, nlev, 0, reinterpret_cast<const float *>(ws + X.L.lam), inc, result,
@@ -476,10 +481,15 @@ int search_pass(const Ctx &X, int dev, int policy, int nlev, bool prune, int str
     F.lam = reinterpret_cast<const float *>(ws + X.L.lam);
     F.rec = reinterpret_cast<OptRec *>(ws + X.L.rec);
     F.sb = reinterpret_cast<StageBound *>(ws + X.L.sb);
-    filter_kernel<<<X.d.nS, FILTER_THREADS, 0, X.st>>>(X.P, F);
-    COUNT_LAUNCH();
-    CU(cudaGetLastError());
-    offsets_kernel<<<1, 32, 0, X.st>>>(X.P, F.sb, X.d0, reinterpret_cast<unsigned long long *>(ws + X.L.item_off), hdr);
+    int grid = 0;
+    int rc = grid_any(X, policy, dev, grid);
+    if (rc) return rc;
+    F.slots = reinterpret_cast<Slot *>(ws + slots_off(X.L));
+    F.nslots = grid * nlev;
+    F.item_off = reinterpret_cast<unsigned long long *>(ws + X.L.item_off);
+    F.hdr = hdr;
+    F.d0 = X.d0;
+    filter_kernel<<<X.d.nS, FILTER_THREADS, 0, X.st>>>(X.P, F);   // + slot reset + item offsets
     COUNT_LAUNCH();
     CU(cudaGetLastError());
     SearchArgs S;
@@ -504,16 +514,10 @@ int search_pass(const Ctx &X, int dev, int policy, int nlev, bool prune, int str
     S.hdr = hdr;
     S.slots = reinterpret_cast<Slot *>(ws + slots_off(X.L));
     S.xshift = xshift_of(X.d.ntot);
-    int rc = run_passes(X, dev, policy, S, timed);
-    if (rc) return rc;
-    int grid = 0;
-    rc = grid_any(X, policy, dev, grid);
-    if (rc) return rc;
-    reduce_kernel<<<1, 256, 0, X.st>>>(X.P, S.slots, grid, nlev, result, keys, S.sb, S.rec, S.item_off, X.d0,
-                                       CHUNK_ITEMS, -1);
-    COUNT_LAUNCH();
-    CU(cudaGetLastError());
-    return CAMELOT_OK;
+    S.result = result;
+    S.keys = keys;
+    S.inc_out = inc_out;
+    return run_passes(X, dev, policy, S, timed, false);
 }
 
 // re-scan chunk `chunk` for level k after the cross-rank reduction (same filter state)
@@ -554,17 +558,11 @@ int rescan_pass(const Ctx &X, int dev, int policy, int nlev, bool prune, int k, 
     S.xshift = xshift_of(X.d.ntot);
     CU(cudaMemsetAsync(&hdr->best_obj, 0xFF, sizeof(unsigned int), X.st));
     CU(cudaMemsetAsync(&hdr->best_packed, 0xFF, sizeof(unsigned long long), X.st));
-    int rc = run_passes(X, dev, policy, S, false);
-    if (rc) return rc;
-    int grid = 0;
-    rc = grid_any(X, policy, dev, grid);
-    if (rc) return rc;
-    long long *dummy = reinterpret_cast<long long *>(ws + X.L.keys) + k;
-    reduce_kernel<<<1, 256, 0, X.st>>>(X.P, S.slots, grid, 1, winner_k, dummy, S.sb, S.rec, S.item_off, X.d0,
-                                       CHUNK_ITEMS, -1);
-    COUNT_LAUNCH();
-    CU(cudaGetLastError());
-    return CAMELOT_OK;
+    CU(cudaMemsetAsync(&hdr->done_ctas, 0, sizeof(unsigned int), X.st));
+    S.result = winner_k;
+    S.keys = reinterpret_cast<long long *>(ws + X.L.keys) + k;
+    S.inc_out = nullptr;
+    return run_passes(X, dev, policy, S, false, true);
 }
 
 void range_of(const Ctx &X, const camelot_exec *ex, unsigned long long &lo, unsigned long long &hi) {
@@ -640,9 +638,8 @@ int local_search(const Ctx &X, const camelot_exec *ex, int policy, int nlev, lon
         // pass seeds the next); replicated on every rank
         for (int stride : coarse_strides(X)) {
             rc = search_pass(X, dev, policy, nlev, true, stride, inc, result,
-                             reinterpret_cast<long long *>(ws + X.L.keys), 0, 1, lo, hi, false);
+                             reinterpret_cast<long long *>(ws + X.L.keys), 0, 1, lo, hi, false, inc);
             if (rc) return rc;
-            CU(cudaMemcpyAsync(inc, result, nlev * sizeof(Slot), cudaMemcpyDeviceToDevice, X.st));
         }
     }
     rc = search_pass(X, dev, policy, nlev, prune, 1, inc, result, keys, ex->rank, ex->world, lo, hi, false);

@@ -66,8 +66,8 @@ struct DevHeader {
     unsigned long long n_scored, n_feasible, n_nodes;
     unsigned int best_obj;          // dynamic incumbent objective key (32-bit, smaller better)
     unsigned int viol_or;
-    unsigned int done_ctas;
-    unsigned int overflow;
+    unsigned int done_ctas;         // last-CTA detection of the leaf pass (fused reduction)
+    unsigned int filt_done;         // last-CTA detection of the filter (fused item offsets)
     unsigned long long items_total; // number of depth-d0 items of the (filtered) space
     unsigned long long nchunks;
     unsigned long long t_search_ns;

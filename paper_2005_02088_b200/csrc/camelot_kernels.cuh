@@ -22,7 +22,16 @@ struct FilterArgs {
     const float *lam;      // [nlev][A]
     OptRec *rec;           // [n][nS][O]
     StageBound *sb;        // [n][nS]
+    // fused: search-slot reset and item offsets (last block)
+    Slot *slots;
+    int nslots;            // grid * nlev slots to reset
+    unsigned long long *item_off;
+    DevHeader *hdr;
+    int d0;
 };
+
+__device__ void item_offsets(const DevProb &P, const StageBound *sb, int d0, unsigned long long *item_off,
+                             DevHeader *hdr);
 
 // One CTA per batch index b: filters the options of every stage at batch b.
 // An option survives unless it provably cannot be part of a feasible
@@ -157,6 +166,24 @@ __global__ void __launch_bounds__(FILTER_THREADS) filter_kernel(const DevProb P,
             F.sb[(size_t)i * P.nS + b] = s;
         }
     }
+    // fused: reset the search slots, then the last block computes the item offsets
+    if (F.slots)
+        for (int q = blockIdx.x * blockDim.x + tid; q < F.nslots; q += gridDim.x * blockDim.x) {
+            F.slots[q].key = 0xFFFFFFFFull;
+            F.slots[q].x = ~0ull;
+        }
+    if (F.item_off) {
+        __shared__ int is_last;
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) is_last = atomicAdd(&F.hdr->filt_done, 1u) == gridDim.x - 1;
+        __syncthreads();
+        if (is_last && tid == 0) {
+            __threadfence();
+            item_offsets(P, F.sb, F.d0, F.item_off, F.hdr);
+            F.hdr->filt_done = 0;
+        }
+    }
 }
 
 __global__ void init_slots_kernel(Slot *s, int n) {
@@ -167,9 +194,8 @@ __global__ void init_slots_kernel(Slot *s, int n) {
 }
 
 // item space: for batch combo bc, items = prod_{i<d0} cnt_i(b_app(i)), 0 if any stage is empty
-__global__ void offsets_kernel(const DevProb P, const StageBound *sb, int d0, unsigned long long *item_off,
-                               DevHeader *hdr) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__device__ void item_offsets(const DevProb &P, const StageBound *sb, int d0, unsigned long long *item_off,
+                             DevHeader *hdr) {
     unsigned long long acc = 0;
     for (int bc = 0; bc < P.nbc; ++bc) {
         item_off[bc] = acc;
@@ -192,34 +218,6 @@ __global__ void offsets_kernel(const DevProb P, const StageBound *sb, int d0, un
     hdr->items_total = acc;
 }
 
-// the same item offsets, but an "empty" batch combo still has a well-defined
-// (zero) item range; used by chunk_of()
-__device__ inline long long find_code(const OptRec *list, int cnt, uint32_t code) {
-    int lo = 0, hi = cnt;
-    while (lo < hi) {
-        int mid = (lo + hi) >> 1;
-        if (list[mid].code < code) lo = mid + 1;
-        else hi = mid;
-    }
-    return (lo < cnt && list[lo].code == code) ? lo : -1;
-}
-
-__device__ inline unsigned long long item_of(const DevProb &P, const StageBound *sb, const OptRec *rec,
-                                             const unsigned long long *item_off, int d0, unsigned long long x) {
-    int beta[AMAX], rho[NMAX], theta[NMAX];
-    decode_index(P, x, beta, rho, theta);
-    int bc = 0;
-    for (int a = 0; a < P.A; ++a) bc = bc * P.nS + beta[a];
-    unsigned long long it = 0;
-    for (int i = 0; i < d0; ++i) {
-        const int b = beta[P.app[i]];
-        const unsigned c = sb[(size_t)i * P.nS + b].cnt;
-        const long long k = find_code(rec + ((size_t)i * P.nS + b) * P.O, (int)c, (uint32_t)(rho[i] * P.nQ + theta[i]));
-        it = it * c + (unsigned long long)(k < 0 ? 0 : k);
-    }
-    return item_off[bc] + it;
-}
-
 __global__ void eq2_kernel(const DevProb P, const float *lam, int nlev, int *y) {
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= P.nbc * nlev) return;
@@ -233,51 +231,13 @@ __global__ void eq2_kernel(const DevProb P, const float *lam, int nlev, int *y) 
     y[idx] = eq2_gpus(P, beta, lam + k * P.A);
 }
 
-// slots -> result[k] (exact local best) and packed keys
+// slots -> result[k] and packed keys (stand-alone kernel: naive path)
 __global__ void reduce_kernel(const DevProb P, const Slot *slots, int nslots, int nlev, Slot *result,
                               long long *keys, const StageBound *sb, const OptRec *rec,
                               const unsigned long long *item_off, int d0, int chunk_items, int flat_shift) {
     __shared__ unsigned long long sk[256], sx[256];
-    for (int k = 0; k < nlev; ++k) {
-        unsigned long long bk = ~0ull, bx = ~0ull;
-        for (int s = threadIdx.x; s < nslots; s += blockDim.x) {
-            const Slot v = slots[(size_t)s * nlev + k];
-            if (slot_less(v.key, v.x, bk, bx)) {
-                bk = v.key;
-                bx = v.x;
-            }
-        }
-        sk[threadIdx.x] = bk;
-        sx[threadIdx.x] = bx;
-        __syncthreads();
-        for (int st = blockDim.x / 2; st; st >>= 1) {
-            if (threadIdx.x < st && slot_less(sk[threadIdx.x + st], sx[threadIdx.x + st], sk[threadIdx.x], sx[threadIdx.x])) {
-                sk[threadIdx.x] = sk[threadIdx.x + st];
-                sx[threadIdx.x] = sx[threadIdx.x + st];
-            }
-            __syncthreads();
-        }
-        if (threadIdx.x == 0) {
-            bk = sk[0];
-            bx = sx[0];
-            if (bk >= 0xFFFFFFFFull) {
-                bk = 0xFFFFFFFFull;
-                bx = ~0ull;
-            }
-            result[k].key = bk;
-            result[k].x = bx;
-            unsigned long long packed;
-            if (bk == 0xFFFFFFFFull) packed = ~0ull;
-            else {
-                unsigned long long low = (P.ntot <= (1ull << 32)) ? bx
-                                         : flat_shift >= 0 ? (bx >> flat_shift)
-                                         : item_of(P, sb, rec, item_off, d0, bx) / (unsigned long long)chunk_items;
-                packed = (bk << 32) | (low & 0xFFFFFFFFull);
-            }
-            keys[k] = (long long)(packed ^ 0x8000000000000000ull);
-        }
-        __syncthreads();
-    }
+    reduce_slots_block(P, slots, nslots, nlev, result, keys, nullptr, sb, rec, item_off, d0, chunk_items,
+                       flat_shift, sk, sx);
 }
 
 // keys (after the cross-rank MIN) -> which chunk must be re-scanned / exact index
@@ -425,6 +385,7 @@ __global__ void __launch_bounds__(FLAT_THREADS) flat_search_kernel(const DevProb
                         unsigned long long ox = __shfl_xor_sync(0xffffffffu, x2, off);
                         if (slot_less(ok2, ox, k2, x2)) { k2 = ok2; x2 = ox; }
                     }
+                    __syncwarp();   // all lanes have read the warp best before lane 0 updates it
                     if (lane == 0 && slot_less(k2, x2, bk_s[wid][0], bx_s[wid][0])) {
                         bk_s[wid][0] = k2;
                         bx_s[wid][0] = x2;
@@ -448,6 +409,7 @@ __global__ void __launch_bounds__(FLAT_THREADS) flat_search_kernel(const DevProb
                             unsigned long long ox = __shfl_xor_sync(0xffffffffu, x2, off);
                             if (slot_less(ok2, ox, k2, x2)) { k2 = ok2; x2 = ox; }
                         }
+                        __syncwarp();
                         if (lane == 0 && slot_less(k2, x2, bk_s[wid][k], bx_s[wid][k])) {
                             bk_s[wid][k] = k2;
                             bx_s[wid][k] = x2;

@@ -21,6 +21,7 @@
 // above the best's index).  Strictly better keys are never pruned.
 #pragma once
 #include "camelot_device.cuh"
+#include "camelot_score.cuh"
 
 namespace cam {
 
@@ -59,6 +60,11 @@ struct SearchArgs {
     unsigned long long out_cap;
     unsigned long long *head;   // pop counter of this pass
     int xshift;                 // index >> xshift fits 32 bits (tie pruning key)
+    // fused reduction (last pass): the last CTA reduces all slots
+    int reduce_last;
+    Slot *result;               // [nlev] exact local best
+    long long *keys;            // [nlev] packed keys
+    Slot *inc_out;              // [nlev] next incumbent (cascade) or nullptr
 };
 
 // Placement state after the first j stages (shared-memory DFS stack and the
@@ -406,13 +412,15 @@ __device__ __forceinline__ void load_ctx(const DevProb &P, const SearchArgs &S, 
     float tub = nd.tub;
 #pragma unroll
     for (int i = 0; i < NS; ++i)
-        if (i < j) {
+        if (S.prune && i < j) {
             const float k = kappa_of(c.dmax[i], c.bw[i], P.gamma[i], P.invBW, P.flags);
             if (k != 1.0f) tub = fminf(tub, __fdiv_rn(c.nt[i], k));
         }
     c.tub = tub;
     // QoS prefix of the child's application (current contention; it only grows)
-    {
+    c.lpre = -1.0f;
+    c.lother = 0.0f;
+    if (S.prune) {
         const int aj = P.app[j];
         float lp = -1.0f, lo = 0.0f;
         bool lo_started = false;
@@ -794,6 +802,86 @@ __device__ __forceinline__ void emit_child(const DevProb &P, const Node<CM> &nd,
     out->tub = fminf(nd.tub, r.NT);
 }
 
+// the same item offsets, but an "empty" batch combo still has a well-defined
+// (zero) item range; used by chunk_of()
+__device__ inline long long find_code(const OptRec *list, int cnt, uint32_t code) {
+    int lo = 0, hi = cnt;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (list[mid].code < code) lo = mid + 1;
+        else hi = mid;
+    }
+    return (lo < cnt && list[lo].code == code) ? lo : -1;
+}
+
+__device__ inline unsigned long long item_of(const DevProb &P, const StageBound *sb, const OptRec *rec,
+                                             const unsigned long long *item_off, int d0, unsigned long long x) {
+    int beta[AMAX], rho[NMAX], theta[NMAX];
+    decode_index(P, x, beta, rho, theta);
+    int bc = 0;
+    for (int a = 0; a < P.A; ++a) bc = bc * P.nS + beta[a];
+    unsigned long long it = 0;
+    for (int i = 0; i < d0; ++i) {
+        const int b = beta[P.app[i]];
+        const unsigned c = sb[(size_t)i * P.nS + b].cnt;
+        const long long k = find_code(rec + ((size_t)i * P.nS + b) * P.O, (int)c, (uint32_t)(rho[i] * P.nQ + theta[i]));
+        it = it * c + (unsigned long long)(k < 0 ? 0 : k);
+    }
+    return item_off[bc] + it;
+}
+
+// slots -> result[k] (exact local best), packed keys and (optionally) the next
+// incumbent; executed by ONE block of 256 threads (sk/sx: 256-entry scratch)
+__device__ void reduce_slots_block(const DevProb &P, const Slot *slots, int nslots, int nlev, Slot *result,
+                                   long long *keys, Slot *inc_out, const StageBound *sb, const OptRec *rec,
+                                   const unsigned long long *item_off, int d0, int chunk_items, int flat_shift,
+                                   unsigned long long *sk, unsigned long long *sx) {
+    for (int k = 0; k < nlev; ++k) {
+        unsigned long long bk = ~0ull, bx = ~0ull;
+        for (int s = threadIdx.x; s < nslots; s += blockDim.x) {
+            const Slot v = slots[(size_t)s * nlev + k];
+            if (slot_less(v.key, v.x, bk, bx)) {
+                bk = v.key;
+                bx = v.x;
+            }
+        }
+        sk[threadIdx.x] = bk;
+        sx[threadIdx.x] = bx;
+        __syncthreads();
+        for (int st = blockDim.x / 2; st; st >>= 1) {
+            if (threadIdx.x < st && slot_less(sk[threadIdx.x + st], sx[threadIdx.x + st], sk[threadIdx.x], sx[threadIdx.x])) {
+                sk[threadIdx.x] = sk[threadIdx.x + st];
+                sx[threadIdx.x] = sx[threadIdx.x + st];
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            bk = sk[0];
+            bx = sx[0];
+            if (bk >= 0xFFFFFFFFull) {
+                bk = 0xFFFFFFFFull;
+                bx = ~0ull;
+            }
+            result[k].key = bk;
+            result[k].x = bx;
+            if (inc_out) {
+                inc_out[k].key = bk;
+                inc_out[k].x = bx;
+            }
+            unsigned long long packed;
+            if (bk == 0xFFFFFFFFull) packed = ~0ull;
+            else {
+                unsigned long long low = (P.ntot <= (1ull << 32)) ? bx
+                                         : flat_shift >= 0 ? (bx >> flat_shift)
+                                         : item_of(P, sb, rec, item_off, d0, bx) / (unsigned long long)chunk_items;
+                packed = (bk << 32) | (low & 0xFFFFFFFFull);
+            }
+            keys[k] = (long long)(packed ^ 0x8000000000000000ull);
+        }
+        __syncthreads();
+    }
+}
+
 // ---------------------------------------------------------------- the search kernel
 // One level-synchronous pass: warps pop parents (dynamic, `grab` at a time),
 // hoist the parent into registers, lanes evaluate its children 32 at a time;
@@ -1060,6 +1148,21 @@ search_kernel(const DevProb P, const SearchArgs S) {
         atomicAdd(&S.hdr->cum_scored, cn.scored);
         atomicAdd(&S.hdr->cum_nodes, cn.nodes);
         atomicOr(&S.hdr->viol_or, cn.viol);
+    }
+    // ---- fused reduction of the search: the last CTA to finish reduces all slots
+    if (S.reduce_last) {
+        __shared__ int is_last;
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) is_last = atomicAdd(&S.hdr->done_ctas, 1u) == gridDim.x - 1;
+        __syncthreads();
+        if (is_last) {
+            __threadfence();
+            unsigned long long *sk = reinterpret_cast<unsigned long long *>(smem_raw);
+            reduce_slots_block(P, S.slots, gridDim.x, nlev, S.result, S.keys, S.inc_out, S.sb, S.rec, S.item_off,
+                               S.d0, S.chunk_items, -1, sk, sk + SEARCH_THREADS);
+            if (threadIdx.x == 0) S.hdr->done_ctas = 0;
+        }
     }
 }
 

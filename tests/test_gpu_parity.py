@@ -295,3 +295,24 @@ def test_frontier_overflow_fallback(api, oracle, cap, monkeypatch):
         gm = api.Session(prob, n_loads=1).plan_min_resource(lam)[0]
         rm = oracle.search(prob, "min_resource", loads=lam, threads=8)[0]
         check_plan(api, prob, gm, rm, oracle, loads=lam)
+
+
+@pytest.mark.parametrize("C,n,A,seed", [(12, 3, 1, 1), (16, 2, 1, 2), (9, 4, 2, 3), (3, 7, 1, 4), (2, 8, 2, 5),
+                                        (10, 5, 1, 6)])
+def test_wide_instantiations(api, oracle, C, n, A, seed):
+    """Exercise the CM=16 (9-16 GPUs) and NS=8 (7-8 stages) kernel widths."""
+    qstep = 34 if n >= 7 else 25
+    prob = G.random_small_problem(100 + seed, n_stages=n, n_gpus=C, n_apps=A, quota_step=qstep,
+                                  batches=(1, 8), max_replicas=2 if n < 7 else 1, qos_rho=1.25)
+    if oracle.ntot(prob) > 4_000_000:
+        pytest.skip("space too large for the in-test oracle")
+    got = api.Session(prob).plan_max_load()
+    ref = oracle.search(prob, threads=8)[0]
+    check_plan(api, prob, got, ref, oracle)
+    if ref.index is not None:
+        lam = [[np.float32(0.3) * np.float32(ref.T)] * A]
+        gm = api.Session(prob, n_loads=1).plan_min_resource(lam)[0]
+        rm = oracle.search(prob, "min_resource", loads=lam, threads=8)[0]
+        check_plan(api, prob, gm, rm, oracle, loads=lam)
+        flat = api.Session(prob, flags=prob.flags | G.F_NO_FILTER).plan_max_load()
+        assert flat.index == ref.index and flat.n_feasible == ref.n_feasible

@@ -1,0 +1,29 @@
+"""compute-sanitizer memcheck / racecheck / synccheck over a small workload
+that runs every kernel (SURVEY.md section 4, T-sanitizer)."""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
+def test_compute_sanitizer(tool):
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    exe = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    if not os.path.exists(exe):
+        pytest.skip("compute-sanitizer not installed")
+    cmd = [exe, "--tool", tool, "--error-exitcode", "17", "--target-processes", "all",
+           sys.executable, os.path.join(ROOT, "tools", "sanitize.py")]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=1500, cwd=ROOT)
+    tail = (p.stdout + p.stderr)[-4000:]
+    assert p.returncode == 0, tail
+    assert "sanitize workload ok" in p.stdout, tail
+    out = p.stdout + p.stderr
+    assert ("ERROR SUMMARY: 0 errors" in out) or ("(0 errors, 0 warnings)" in out), tail

@@ -1,0 +1,27 @@
+"""Small end-to-end workload for compute-sanitizer (memcheck / racecheck /
+synccheck): every kernel of libcamelot.so runs at least once."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from gen import problems as G  # noqa: E402
+from paper_2005_02088_b200 import _lib as L, api  # noqa: E402
+
+probs = [G.config_problems(1)[0], G.config_problems(2)[4],
+         G.random_small_problem(3, n_stages=4, n_gpus=9, n_apps=2, quota_step=25, batches=(1, 8))]
+for p in probs:
+    s = api.Session(p, n_loads=2)
+    r = s.plan_max_load()
+    m = s.plan_min_resource([[0.3 * max(r.objective, 1.0)] * p.n_apps, [0.5 * max(r.objective, 1.0)] * p.n_apps])
+    s.predict_index(0, loads=[[1.0] * p.n_apps])
+    s.score_range(0, min(5000, 1 << 12))
+    keys = [s.search_local(0, rank=k, world=2).clone() for k in range(2)]
+    red = torch.stack(keys).min(dim=0).values
+    s.finalize(0, red, rank=0, world=2)
+    f = api.Session(p, flags=p.flags | L.F_NO_FILTER).plan_max_load()
+    g = api.Session(p, flags=p.flags | L.F_PAPER_GLOBAL).plan_max_load()
+    print(p.name, r.index, m[0].index, f.index, g.index, flush=True)
+torch.cuda.synchronize()
+print("sanitize workload ok")
