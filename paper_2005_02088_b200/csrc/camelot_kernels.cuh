@@ -13,7 +13,7 @@
 
 namespace cam {
 
-constexpr int FILTER_THREADS = 256;
+constexpr int FILTER_THREADS = 512;
 constexpr int OMAX = 16 * 128;   // Rmax * nQ upper bound
 
 struct FilterArgs {
@@ -40,9 +40,14 @@ __global__ void __launch_bounds__(FILTER_THREADS) filter_kernel(const DevProb P,
     __shared__ unsigned char keep[NMAX][OMAX];
     __shared__ float mindur[NMAX];
     __shared__ int minNP[NMAX];
+    __shared__ float4 tabs[NMAX * CAMELOT_MAX_QUOTAS];   // this batch's table slice (staged once)
+    __shared__ int Qs[CAMELOT_MAX_QUOTAS];
     const int b = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int n = P.n, O = P.O, nQ = P.nQ;
+    for (int q = tid; q < n * nQ; q += blockDim.x) tabs[q] = P.tab[((size_t)(q / nQ) * P.nS + b) * nQ + q % nQ];
+    for (int q = tid; q < nQ; q += blockDim.x) Qs[q] = P.Q[q];
+    __syncthreads();
     const bool cap = !(P.flags & F_NO_BW_CAP);
     // incumbent
     unsigned long long ikey = 0xFFFFFFFFull;
@@ -61,7 +66,7 @@ __global__ void __launch_bounds__(FILTER_THREADS) filter_kernel(const DevProb P,
     for (int idx = tid; idx < n * O; idx += blockDim.x) {
         const int i = idx / O, o = idx % O;
         const int th = o % nQ, N = o / nQ + 1;
-        const float4 e = P.tab[((size_t)i * P.nS + b) * nQ + th];
+        const float4 e = tabs[i * nQ + th];
         const uint32_t As = P.Am[i] * (uint32_t)P.S[b];
         bool k = true;
         if (F.stride > 1 && ((nQ - 1 - th) % F.stride) != 0) k = false;
@@ -85,8 +90,8 @@ __global__ void __launch_bounds__(FILTER_THREADS) filter_kernel(const DevProb P,
             for (int o = lane; o < O; o += 32)
                 if (keep[i][o]) {
                     const int th = o % nQ, N = o / nQ + 1;
-                    md = fminf(md, P.tab[((size_t)i * P.nS + b) * nQ + th].x);
-                    mn = min(mn, N * P.Q[th]);
+                    md = fminf(md, tabs[i * nQ + th].x);
+                    mn = min(mn, N * Qs[th]);
                 }
             for (int off = 16; off; off >>= 1) {
                 md = fminf(md, __shfl_xor_sync(0xffffffffu, md, off));
@@ -104,7 +109,7 @@ __global__ void __launch_bounds__(FILTER_THREADS) filter_kernel(const DevProb P,
             if (!keep[i][o]) continue;
             const int th = o % nQ, N = o / nQ + 1;
             const int a = P.app[i];
-            const float dur = P.tab[((size_t)i * P.nS + b) * nQ + th].x;
+            const float dur = tabs[i * nQ + th].x;
             // QoS: ordered fp32 sum with this option's duration and the others' minima
             float ls = 0.0f;
             for (int k2 = P.first_of_app[a]; k2 <= P.last_of_app[a]; ++k2) {
@@ -113,7 +118,7 @@ __global__ void __launch_bounds__(FILTER_THREADS) filter_kernel(const DevProb P,
             }
             bool k = ls <= P.qos[a];
             // quota: N p + sum of the other stages' minimal N p  <=  C R
-            long long U = (long long)N * P.Q[th];
+            long long U = (long long)N * Qs[th];
             for (int k2 = 0; k2 < n; ++k2)
                 if (k2 != i) U += (P.app[k2] == a) ? (long long)minNP[k2] : (long long)P.Q[0];
             if (U > (long long)P.C * P.R) k = false;
@@ -137,12 +142,12 @@ __global__ void __launch_bounds__(FILTER_THREADS) filter_kernel(const DevProb P,
             const unsigned m = __ballot_sync(0xffffffffu, k);
             if (k) {
                 const int th = o % nQ, N = o / nQ + 1;
-                const float4 e = P.tab[((size_t)i * P.nS + b) * nQ + th];
+                const float4 e = tabs[i * nQ + th];
                 OptRec r;
                 r.code = (uint32_t)o;
-                r.p = (uint32_t)P.Q[th];
+                r.p = (uint32_t)Qs[th];
                 r.N = (uint32_t)N;
-                r.NP = (uint32_t)(N * P.Q[th]);
+                r.NP = (uint32_t)(N * Qs[th]);
                 r.W = P.W[i];
                 r.As = As;
                 r.MEM = P.W[i] + (uint32_t)N * As;

@@ -1135,19 +1135,41 @@ search_kernel(const DevProb P, const SearchArgs S) {
         sl.key = bk;
         sl.x = bx;
     }
+    // counters: warp -> CTA (shared) -> one atomic per CTA and non-zero counter
     for (int off = 16; off; off >>= 1) {
         cn.scored += __shfl_xor_sync(0xffffffffu, cn.scored, off);
         cn.feasible += __shfl_xor_sync(0xffffffffu, cn.feasible, off);
         cn.nodes += __shfl_xor_sync(0xffffffffu, cn.nodes, off);
         cn.viol |= __shfl_xor_sync(0xffffffffu, cn.viol, off);
     }
+    __shared__ unsigned long long cta_cnt[SEARCH_WARPS][3];
+    __shared__ unsigned cta_viol[SEARCH_WARPS];
     if (lane == 0) {
-        atomicAdd(&S.hdr->n_scored, cn.scored);
-        atomicAdd(&S.hdr->n_feasible, cn.feasible);
-        atomicAdd(&S.hdr->n_nodes, cn.nodes);
-        atomicAdd(&S.hdr->cum_scored, cn.scored);
-        atomicAdd(&S.hdr->cum_nodes, cn.nodes);
-        atomicOr(&S.hdr->viol_or, cn.viol);
+        cta_cnt[wid][0] = cn.scored;
+        cta_cnt[wid][1] = cn.feasible;
+        cta_cnt[wid][2] = cn.nodes;
+        cta_viol[wid] = cn.viol;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long sc = 0, fe = 0, no = 0;
+        unsigned vi = 0;
+        for (int w = 0; w < SEARCH_WARPS; ++w) {
+            sc += cta_cnt[w][0];
+            fe += cta_cnt[w][1];
+            no += cta_cnt[w][2];
+            vi |= cta_viol[w];
+        }
+        if (sc) {
+            atomicAdd(&S.hdr->n_scored, sc);
+            atomicAdd(&S.hdr->cum_scored, sc);
+        }
+        if (fe) atomicAdd(&S.hdr->n_feasible, fe);
+        if (no) {
+            atomicAdd(&S.hdr->n_nodes, no);
+            atomicAdd(&S.hdr->cum_nodes, no);
+        }
+        if (vi) atomicOr(&S.hdr->viol_or, vi);
     }
     // ---- fused reduction of the search: the last CTA to finish reduces all slots
     if (S.reduce_last) {
