@@ -349,6 +349,49 @@ int launch_search(const Ctx &X, const SearchArgs &S, int grid) {
         return policy ? FN<16, 8, 1>(__VA_ARGS__) : FN<16, 8, 0>(__VA_ARGS__);                         \
     } while (0)
 
+template <int CM>
+size_t level_smem() {
+    return std::max(search_smem<CM>(), sizeof(FilterSmem));
+}
+
+template <int CM, int NS, int POL>
+int coop_grid_for(int dev, int &grid) {
+    static std::mutex mu;
+    static std::vector<std::pair<int, int>> cache;   // (dev, grid)
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto &e : cache)
+        if (e.first == dev) {
+            grid = e.second;
+            return CAMELOT_OK;
+        }
+    const size_t sm = level_smem<CM>();
+    CU(cudaFuncSetAttribute(search_level_kernel<CM, NS, POL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    int per = 0, nsm = 0;
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, search_level_kernel<CM, NS, POL>, SEARCH_THREADS, sm));
+    CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    grid = std::max(1, std::min(MAXSLOTS, per * nsm));
+    cache.push_back({dev, grid});
+    return CAMELOT_OK;
+}
+
+template <int CM, int NS, int POL>
+int launch_level(const Ctx &X, int dev, LevelArgs LA) {
+    int grid = 0;
+    int rc = coop_grid_for<CM, NS, POL>(dev, grid);
+    if (rc) return rc;
+    LA.F.nslots = grid * LA.S.nlev;
+    const size_t sm = level_smem<CM>();
+    void *args[] = {(void *)&X.P, (void *)&LA};
+    CU(cudaLaunchCooperativeKernel((const void *)search_level_kernel<CM, NS, POL>, dim3(grid), dim3(SEARCH_THREADS),
+                                   args, sm, X.st));
+    COUNT_LAUNCH();
+    return CAMELOT_OK;
+}
+
+int launch_level_any(const Ctx &X, int policy, int dev, const LevelArgs &LA) {
+    CAM_DISPATCH(launch_level, X, dev, LA);
+}
+
 int launch_search_any(const Ctx &X, int policy, const SearchArgs &S, int grid) {
     CAM_DISPATCH(launch_search, X, S, grid);
 }
@@ -402,6 +445,13 @@ int flat_pass(const Ctx &X, int dev, int policy, int nlev, int ystride, int yoff
     COUNT_LAUNCH();
     CU(cudaGetLastError());
     return CAMELOT_OK;
+}
+
+// one cooperative launch per search level (default); CAMELOT_COOP=0 selects the
+// multi-launch path (filter kernel + one kernel per pass)
+bool use_coop() {
+    const char *e = getenv("CAMELOT_COOP");
+    return !(e && e[0] == '0');
 }
 
 int xshift_of(unsigned long long ntot) {
@@ -469,9 +519,12 @@ int search_pass(const Ctx &X, int dev, int policy, int nlev, bool prune, int str
         return flat_pass(X, dev, policy, nlev, nlev, 0, reinterpret_cast<const float *>(ws + X.L.lam), inc, result,
                          keys, rank, world, lo, hi);
     DevHeader *hdr = reinterpret_cast<DevHeader *>(ws + X.L.hdr);
-    CU(cudaMemsetAsync(hdr, 0, offsetof(DevHeader, cum_scored), X.st));
-    CU(cudaMemsetAsync(&hdr->best_obj, 0xFF, sizeof(unsigned int), X.st));
-    CU(cudaMemsetAsync(&hdr->best_packed, 0xFF, sizeof(unsigned long long), X.st));
+    const bool coop = use_coop();
+    if (!coop) {
+        CU(cudaMemsetAsync(hdr, 0, offsetof(DevHeader, cum_scored), X.st));
+        CU(cudaMemsetAsync(&hdr->best_obj, 0xFF, sizeof(unsigned int), X.st));
+        CU(cudaMemsetAsync(&hdr->best_packed, 0xFF, sizeof(unsigned long long), X.st));
+    }
     FilterArgs F;
     F.policy = policy;
     F.prune = prune;
@@ -489,9 +542,11 @@ int search_pass(const Ctx &X, int dev, int policy, int nlev, bool prune, int str
     F.item_off = reinterpret_cast<unsigned long long *>(ws + X.L.item_off);
     F.hdr = hdr;
     F.d0 = X.d0;
-    filter_kernel<<<X.d.nS, FILTER_THREADS, 0, X.st>>>(X.P, F);   // + slot reset + item offsets
-    COUNT_LAUNCH();
-    CU(cudaGetLastError());
+    if (!coop) {
+        filter_kernel<<<X.d.nS, FILTER_THREADS, 0, X.st>>>(X.P, F);   // + slot reset + item offsets
+        COUNT_LAUNCH();
+        CU(cudaGetLastError());
+    }
     SearchArgs S;
     memset(&S, 0, sizeof(S));
     S.policy = policy;
@@ -517,6 +572,15 @@ int search_pass(const Ctx &X, int dev, int policy, int nlev, bool prune, int str
     S.result = result;
     S.keys = keys;
     S.inc_out = inc_out;
+    if (coop) {
+        LevelArgs LA;
+        LA.S = S;
+        LA.F = F;
+        LA.buf0 = ws + X.L.front0;
+        LA.buf1 = ws + X.L.front1;
+        LA.fcap = X.L.fcap;
+        return launch_level_any(X, policy, dev, LA);
+    }
     return run_passes(X, dev, policy, S, timed, false);
 }
 

@@ -36,13 +36,21 @@ __device__ void item_offsets(const DevProb &P, const StageBound *sb, int d0, uns
 // One CTA per batch index b: filters the options of every stage at batch b.
 // An option survives unless it provably cannot be part of a feasible
 // candidate at least as good as the incumbent.
-__global__ void __launch_bounds__(FILTER_THREADS) filter_kernel(const DevProb P, const FilterArgs F) {
-    __shared__ unsigned char keep[NMAX][OMAX];
-    __shared__ float mindur[NMAX];
-    __shared__ int minNP[NMAX];
-    __shared__ float4 tabs[NMAX * CAMELOT_MAX_QUOTAS];   // this batch's table slice (staged once)
-    __shared__ int Qs[CAMELOT_MAX_QUOTAS];
-    const int b = blockIdx.x;
+struct FilterSmem {
+    float4 tabs[NMAX * CAMELOT_MAX_QUOTAS];   // this batch's table slice (staged once)
+    unsigned char keep[NMAX][OMAX];
+    float mindur[NMAX];
+    int minNP[NMAX];
+    int Qs[CAMELOT_MAX_QUOTAS];
+};
+
+// Filter body for batch b, executed by one whole CTA (any blockDim multiple of 32).
+__device__ void filter_body(const DevProb &P, const FilterArgs &F, int b, FilterSmem &fsm) {
+    auto &keep = fsm.keep;
+    auto &mindur = fsm.mindur;
+    auto &minNP = fsm.minNP;
+    auto &tabs = fsm.tabs;
+    auto &Qs = fsm.Qs;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int n = P.n, O = P.O, nQ = P.nQ;
     for (int q = tid; q < n * nQ; q += blockDim.x) tabs[q] = P.tab[((size_t)(q / nQ) * P.nS + b) * nQ + q % nQ];
@@ -84,7 +92,7 @@ __global__ void __launch_bounds__(FILTER_THREADS) filter_kernel(const DevProb P,
     const int rounds = F.prune ? 3 : 0;
     for (int it = 0; it <= rounds; ++it) {
         // per-stage minima over surviving options (warp w: stage w)
-        for (int i = wid; i < n; i += FILTER_THREADS / 32) {
+        for (int i = wid; i < n; i += (int)(blockDim.x >> 5)) {
             float md = __int_as_float(0x7f800000);
             int mn = 0x7fffffff;
             for (int o = lane; o < O; o += 32)
@@ -131,7 +139,7 @@ __global__ void __launch_bounds__(FILTER_THREADS) filter_kernel(const DevProb P,
         __syncthreads();
     }
     // compaction in ascending option code (warp w: stage w) + records
-    for (int i = wid; i < n; i += FILTER_THREADS / 32) {
+    for (int i = wid; i < n; i += (int)(blockDim.x >> 5)) {
         int cnt = 0;
         float maxNT = 0.0f;
         OptRec *dst = F.rec + ((size_t)i * P.nS + b) * O;
@@ -171,7 +179,14 @@ __global__ void __launch_bounds__(FILTER_THREADS) filter_kernel(const DevProb P,
             F.sb[(size_t)i * P.nS + b] = s;
         }
     }
-    // fused: reset the search slots, then the last block computes the item offsets
+}
+
+// One CTA per batch index b: filters the options of every stage at batch b
+// (+ fused: search-slot reset and, by the last block, the item offsets).
+__global__ void __launch_bounds__(FILTER_THREADS) filter_kernel(const DevProb P, const FilterArgs F) {
+    __shared__ FilterSmem fsm;
+    const int tid = threadIdx.x;
+    filter_body(P, F, blockIdx.x, fsm);
     if (F.slots)
         for (int q = blockIdx.x * blockDim.x + tid; q < F.nslots; q += gridDim.x * blockDim.x) {
             F.slots[q].key = 0xFFFFFFFFull;
@@ -497,6 +512,92 @@ __global__ void score_range_kernel(const DevProb P, unsigned long long lo, unsig
     if (T) T[t] = s.T;
     if (u) u[t] = s.u;
     if (U) U[t] = s.U;
+}
+
+}  // namespace cam
+
+// ============================================================================
+// Cooperative persistent kernel: ONE launch per search level (incumbent
+// cascade level or main search): header reset -> option filter -> item offsets
+// -> the n level-synchronous passes -> slot reduction, separated by grid-wide
+// barriers instead of kernel boundaries.  Launched with
+// cudaLaunchCooperativeKernel (all CTAs co-resident).
+#include <cooperative_groups.h>
+
+namespace cam {
+
+struct LevelArgs {
+    SearchArgs S;      // shared fields; per-pass fields are set in the kernel
+    FilterArgs F;
+    void *buf0, *buf1; // frontier ping-pong buffers
+    unsigned long long fcap;
+};
+
+template <int CM, int NS, int POLICY>
+__global__ void __launch_bounds__(SEARCH_THREADS, SEARCH_MINB)
+search_level_kernel(const DevProb P, const LevelArgs LA) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SearchArgs S = LA.S;
+    DevHeader *hdr = S.hdr;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    // phase 0: reset this level's header state (the cumulative counters stay)
+    if (blockIdx.x == 0) {
+        unsigned *h = reinterpret_cast<unsigned *>(hdr);
+        for (int w = threadIdx.x; w < (int)(offsetof(DevHeader, cum_scored) / 4); w += blockDim.x) h[w] = 0u;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            hdr->best_obj = 0xFFFFFFFFu;
+            hdr->best_packed = ~0ull;
+        }
+    }
+    grid.sync();
+    // phase 1: option filter (one CTA per batch) and slot reset
+    for (int b = blockIdx.x; b < P.nS; b += gridDim.x) {
+        filter_body(P, LA.F, b, *reinterpret_cast<FilterSmem *>(smem_raw));
+        __syncthreads();
+    }
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < gridDim.x * S.nlev; q += gridDim.x * blockDim.x) {
+        S.slots[q].key = 0xFFFFFFFFull;
+        S.slots[q].x = ~0ull;
+    }
+    grid.sync();
+    // phase 2: item offsets (chunk ownership)
+    if (blockIdx.x == 0 && threadIdx.x == 0) item_offsets(P, S.sb, S.d0, LA.F.item_off, hdr);
+    grid.sync();
+    // phase 3: the passes (shared memory now holds the search state)
+    Node<CM> *stack_all = reinterpret_cast<Node<CM> *>(smem_raw);
+    WarpCtl *ctl_all = reinterpret_cast<WarpCtl *>(stack_all + (size_t)SEARCH_WARPS * NMAX);
+    WarpBest *wb_all = reinterpret_cast<WarpBest *>(ctl_all + SEARCH_WARPS);
+    Node<CM> *stack = stack_all + (size_t)wid * NMAX;
+    WarpCtl *ctl = ctl_all + wid;
+    WarpBest *wb = wb_all + wid;
+    init_warp_best(S, wb, lane);
+    Counters cn = {0, 0, 0, 0};
+    const int n = P.n;
+    for (int j = 0; j < n; ++j) {
+        S.level = j;
+        S.flevel = (j + 1 <= n - 1) ? j + 1 : -1;
+        S.in_nodes = j == 0 ? nullptr : ((j & 1) ? LA.buf1 : LA.buf0);
+        S.in_count = &hdr->tail[j];
+        S.in_cap = LA.fcap;
+        S.out_nodes = ((j + 1) & 1) ? LA.buf1 : LA.buf0;
+        S.out_tail = &hdr->tail[j + 1];
+        S.out_cap = LA.fcap;
+        S.head = &hdr->head[j];
+        S.grab = 1;
+        pass_body<CM, NS, POLICY>(P, S, stack, ctl, wb, lane, cn);
+        grid.sync();
+    }
+    cta_finish<CM>(S, wb_all, lane, wid, cn);
+    grid.sync();
+    // phase 4: reduction of the CTA slots (block 0)
+    if (blockIdx.x == 0) {
+        unsigned long long *sk = reinterpret_cast<unsigned long long *>(smem_raw);
+        reduce_slots_block(P, S.slots, gridDim.x, S.nlev, S.result, S.keys, S.inc_out, S.sb, S.rec, S.item_off, S.d0,
+                           S.chunk_items, -1, sk, sk + SEARCH_THREADS);
+    }
 }
 
 }  // namespace cam

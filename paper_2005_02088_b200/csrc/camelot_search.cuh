@@ -888,17 +888,8 @@ __device__ void reduce_slots_block(const DevProb &P, const Slot *slots, int nslo
 // surviving children at depth `flevel` are appended to the output frontier
 // (generic inline depth-first descent when the frontier is full); leaves are
 // scored exactly.
-template <int CM, int NS, int POLICY>
-__global__ void __launch_bounds__(SEARCH_THREADS, SEARCH_MINB)
-search_kernel(const DevProb P, const SearchArgs S) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    Node<CM> *stack_all = reinterpret_cast<Node<CM> *>(smem_raw);
-    WarpCtl *ctl_all = reinterpret_cast<WarpCtl *>(stack_all + (size_t)SEARCH_WARPS * NMAX);
-    WarpBest *wb_all = reinterpret_cast<WarpBest *>(ctl_all + SEARCH_WARPS);
-    Node<CM> *stack = stack_all + (size_t)wid * NMAX;
-    WarpCtl *ctl = ctl_all + wid;
-    WarpBest *wb = wb_all + wid;
+// warp best + pruning bounds from the incumbent (start of a search level)
+__device__ __forceinline__ void init_warp_best(const SearchArgs &S, WarpBest *wb, int lane) {
     const int nlev = S.nlev;
     for (int k = lane; k < nlev; k += 32) {
         wb->key[k] = S.inc[k].key;
@@ -915,7 +906,14 @@ search_kernel(const DevProb P, const SearchArgs S) {
             wb->gpack = min(wb->gpack, (wb->key[0] << 32) | min(wb->x[0] >> S.xshift, 0xFFFFFFFFull));
     }
     __syncwarp();
-    Counters cn = {0, 0, 0, 0};
+}
+
+// One level-synchronous pass (parents at depth S.level), executed by one warp
+// of a persistent grid until the pass's work is exhausted.
+template <int CM, int NS, int POLICY>
+__device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S, Node<CM> *stack, WarpCtl *ctl,
+                                          WarpBest *wb, int lane, Counters &cn) {
+    const int nlev = S.nlev;
     const int n = P.n;
     const int jtop = S.level;
     const Node<CM> *in = reinterpret_cast<const Node<CM> *>(S.in_nodes);
@@ -1121,6 +1119,13 @@ search_kernel(const DevProb P, const SearchArgs S) {
             }
         }
     }
+}
+
+// End of a search level for one CTA: merge the warps' bests into the CTA's slot
+// and add the counters (one atomic per CTA and non-zero counter).
+template <int CM>
+__device__ __forceinline__ void cta_finish(const SearchArgs &S, WarpBest *wb_all, int lane, int wid, Counters &cn) {
+    const int nlev = S.nlev;
     // ---- CTA reduction of warp bests, MERGED into this CTA's slot (slots are
     // reset once per search; every pass may score leaves via inline descent)
     __syncthreads();
@@ -1171,6 +1176,24 @@ search_kernel(const DevProb P, const SearchArgs S) {
         }
         if (vi) atomicOr(&S.hdr->viol_or, vi);
     }
+}
+
+template <int CM, int NS, int POLICY>
+__global__ void __launch_bounds__(SEARCH_THREADS, SEARCH_MINB)
+search_kernel(const DevProb P, const SearchArgs S) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    Node<CM> *stack_all = reinterpret_cast<Node<CM> *>(smem_raw);
+    WarpCtl *ctl_all = reinterpret_cast<WarpCtl *>(stack_all + (size_t)SEARCH_WARPS * NMAX);
+    WarpBest *wb_all = reinterpret_cast<WarpBest *>(ctl_all + SEARCH_WARPS);
+    Node<CM> *stack = stack_all + (size_t)wid * NMAX;
+    WarpCtl *ctl = ctl_all + wid;
+    WarpBest *wb = wb_all + wid;
+    const int nlev = S.nlev;
+    init_warp_best(S, wb, lane);
+    Counters cn = {0, 0, 0, 0};
+    pass_body<CM, NS, POLICY>(P, S, stack, ctl, wb, lane, cn);
+    cta_finish<CM>(S, wb_all, lane, wid, cn);
     // ---- fused reduction of the search: the last CTA to finish reduces all slots
     if (S.reduce_last) {
         __shared__ int is_last;
