@@ -350,8 +350,9 @@ int launch_search(const Ctx &X, const SearchArgs &S, int grid) {
     } while (0)
 
 template <int CM>
-size_t level_smem() {
-    return std::max(search_smem<CM>(), sizeof(FilterSmem));
+size_t level_smem() {   // filter scratch, then search state + StageBound cache (n x nS <= 8 x 64)
+    return std::max(search_smem_bytes<CM>() + (size_t)NMAX * CAMELOT_MAX_BATCHES * sizeof(StageBound),
+                    sizeof(FilterSmem));
 }
 
 template <int CM, int NS, int POL>

@@ -566,6 +566,13 @@ search_level_kernel(const DevProb P, const LevelArgs LA) {
     // phase 2: item offsets (chunk ownership)
     if (blockIdx.x == 0 && threadIdx.x == 0) item_offsets(P, S.sb, S.d0, LA.F.item_off, hdr);
     grid.sync();
+    // per-CTA copy of the (stage, batch) bounds in shared memory, after the search state
+    {
+        StageBound *sbs = reinterpret_cast<StageBound *>(smem_raw + search_smem_bytes<CM>());
+        for (int q = threadIdx.x; q < P.n * P.nS; q += blockDim.x) sbs[q] = S.sb[q];
+        __syncthreads();
+        S.sb = sbs;
+    }
     // phase 3: the passes (shared memory now holds the search state)
     Node<CM> *stack_all = reinterpret_cast<Node<CM> *>(smem_raw);
     WarpCtl *ctl_all = reinterpret_cast<WarpCtl *>(stack_all + (size_t)SEARCH_WARPS * NMAX);

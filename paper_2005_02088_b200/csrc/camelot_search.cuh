@@ -888,6 +888,13 @@ __device__ void reduce_slots_block(const DevProb &P, const Slot *slots, int nslo
 // surviving children at depth `flevel` are appended to the output frontier
 // (generic inline depth-first descent when the frontier is full); leaves are
 // scored exactly.
+// dynamic shared memory of the search state (DFS stacks, walk control, warp bests)
+template <int CM>
+__host__ __device__ constexpr size_t search_smem_bytes() {
+    return (size_t)SEARCH_WARPS * NMAX * sizeof(Node<CM>) + SEARCH_WARPS * sizeof(WarpCtl) +
+           SEARCH_WARPS * sizeof(WarpBest);
+}
+
 // warp best + pruning bounds from the incumbent (start of a search level)
 __device__ __forceinline__ void init_warp_best(const SearchArgs &S, WarpBest *wb, int lane) {
     const int nlev = S.nlev;
