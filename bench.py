@@ -134,7 +134,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-flat", action="store_true", help="skip the flat-scan roofline leg")
-    ap.add_argument("--flat-config", type=int, default=6, help="config of the flat scan (6 = C4r)")
+    ap.add_argument("--no-sa", action="store_true", help="skip the simulated-annealing baseline")
+    ap.add_argument("--sa-chains", type=int, default=4096)
+    ap.add_argument("--sa-iters", type=int, default=500)
+    ap.add_argument("--flat-config", type=int, default=4, help="config of the flat scan (4 = C4)")
+    ap.add_argument("--flat-slice", type=int, default=1 << 31, help="candidates of the flat-scan slice (0 = all)")
     args = ap.parse_args()
     assert args.warmup >= 3 or args.impl == "reference", "timing rules: >= 3 warm-up steps"
 
@@ -278,27 +282,54 @@ def main():
     if not args.no_flat and rank == 0:
         fp = G.config_problems(args.flat_config)[0]
         fs = api.Session(fp, device=local, flags=fp.flags | L.F_NO_FILTER)
-        fs.plan_max_load()
-        fts, fev, fsc = [], [], []
-        for _ in range(3):
-            fr = fs.plan_max_load()
-            st = fs.last_stats()
-            fts.append(st["t_ns"])
-            fev.append(st["cum_scored"] + st["cum_nodes"])
-            fsc.append(st["cum_scored"])
-        ft = statistics.median(fts) * 1e-9
         fnt = 1
         for _ in range(fp.n_apps):
             fnt *= len(fp.batch)
         for _ in range(fp.n_stages):
             fnt *= fp.max_replicas * len(fp.quota_pct)
+        # a slice of the canonical index space (the full C4 flat scan is 8.2e13)
+        flo = (fnt // 3) - (fnt // 3) % (fp.max_replicas * len(fp.quota_pct))
+        fhi = min(fnt, flo + args.flat_slice) if args.flat_slice else fnt
+        fs.plan_max_load(lo=flo, hi=fhi)
+        fts, fev, fsc = [], [], []
+        for _ in range(3):
+            fr = fs.plan_max_load(lo=flo, hi=fhi)
+            st = fs.last_stats()
+            fts.append(st["t_ns"])
+            fev.append(st["cum_scored"] + st["cum_nodes"])
+            fsc.append(st["cum_scored"])
+        ft = statistics.median(fts) * 1e-9
+        fnt = fhi - flo
         fops = algorithmic_ops_per_eval(fp)
         fach = fops * statistics.median(fev) / ft / 1e12
-        flat = {"workload": f"{fp.name} max-load, NO_FILTER exhaustive scan ({fnt:.4g} candidates)",
+        flat = {"workload": f"{fp.name} max-load, NO_FILTER exhaustive scan of indices [{flo}, {fhi}) "
+                            f"({fnt:.4g} candidates)",
                 "index": fr.index, "ms": ft * 1e3, "candidates_per_s": fnt / ft,
                 "leaves_scored_per_s": statistics.median(fsc) / ft,
                 "roofline": {"bound": "alu", "achieved": fach, "peak": peak, "unit": "Tops/s",
                              "frac": fach / peak, "ops_per_eval": fops}}
+
+    # the paper's own solver (simulated annealing, NEXT-1) on the same device:
+    # time and quality against the exact plans of this step
+    sa = None
+    if not args.no_sa and rank == 0:
+        ss = api.Session(prob, device=local, n_loads=1)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r1 = ss.sa(L.POLICY_MAX_LOAD, seed=1, chains=args.sa_chains, iters=args.sa_iters, p0=0.3, cool=0.995)
+        lam_sa = [[LOW_LOAD * pm.objective] * prob.n_apps]
+        r2 = ss.sa(L.POLICY_MIN_RESOURCE, lam_sa, seed=2, chains=args.sa_chains, iters=args.sa_iters, p0=0.3,
+                   cool=0.995)
+        torch.cuda.synchronize()
+        sa = {"chains": args.sa_chains, "iters": args.sa_iters, "p0": 0.3, "cool": 0.995,
+              "ms_both_policies": (time.perf_counter() - t0) * 1e3,
+              "max_load": {"T_sa": r1.objective, "T_exact": pm.objective,
+                           "gap_pct": 100.0 * (1.0 - r1.objective / pm.objective) if r1.index is not None else None,
+                           "same_plan_as_exact": r1.index == pm.index},
+              "min_resource": {"u_U_sa": [r2.gpus_used, r2.quota_used] if r2.index is not None else None,
+                               "u_U_exact": [pr.gpus_used, pr.quota_used],
+                               "same_plan_as_exact": r2.index == pr.index},
+              "note": "PAPER.md L880-888 solver, reading R13; chains bit-identical to the oracle SA"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -319,6 +350,7 @@ def main():
                           "min_resource": {"index": pr.index, "gpus_used": pr.gpus_used,
                                            "quota_used": pr.quota_used, "load": LOW_LOAD * pm.objective}},
                 "scored_per_step": evals, "gpu_launches": launches, "roofline": roof, "flat_scan": flat,
+                "sa_baseline": sa,
                 "clocks": clocks,
                 "e2e": e2e, "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)

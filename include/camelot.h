@@ -252,6 +252,24 @@ int camelot_last_stats(const camelot_exec *exec, uint64_t *out8);
 /* Process-wide number of kernels launched by this library so far. */
 uint64_t camelot_kernel_launches(void);
 
+/* The paper's own solver (NEXT-1): simulated annealing over V = [n1..nN,
+ * p1..pN] plus the batch digit(s) (reading R13), run as
+ * `chains` independent chains of `iters` moves on the device.  A move changes
+ * one random digit by +-1 (reflected at the grid edge); invalid states are
+ * rejected once the chain is valid; a worse valid state is accepted with
+ * probability p0 * cool^k at iteration k; every valid proposal that improves
+ * the objective updates the best.  Randomness is counter-based:
+ *   h(seed, chain, k, purpose) = sm64(sm64(seed ^ chain*0xD1B54A32D192ED03) + (k<<2 | purpose))
+ * (sm64 = splitmix64; purposes 0 digit, 1 direction, 2 acceptance, 3 initial
+ * digit k), so a chain is reproducible anywhere.  policy: CAMELOT_POLICY_*;
+ * load_qps: host [A] (min-resource) or NULL.  out: best plan over all chains
+ * (INFEASIBLE if no chain reached a valid state).  Optional DEVICE outputs
+ * d_chain_index [chains] (UINT64_MAX = none) and d_chain_key [chains] (the
+ * 32-bit objective key of each chain's best).  chains <= 2^20. */
+int camelot_sa(const camelot_problem *p, const camelot_cluster *c, int policy, const float *load_qps,
+               uint64_t seed, int chains, int iters, float p0, float cool, const camelot_exec *exec,
+               camelot_plan *out, uint64_t *d_chain_index, uint32_t *d_chain_key);
+
 #ifdef __cplusplus
 }
 #endif

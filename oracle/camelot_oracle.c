@@ -591,3 +591,119 @@ int oc_eq2_y(const oc_problem *P, const int32_t *beta, const float *lam) { retur
 
 int oc_sizeof_score(void) { return (int)sizeof(oc_score_t); }
 int oc_sizeof_best(void) { return (int)sizeof(oc_best_t); }
+
+/* ---------------------------------------------------------------- simulated annealing
+ * The paper's solver: a state V = [n1..nN, p1..pN] (plus the
+ * batch digit(s), L858) "randomly moves in one direction"; an invalid new state
+ * is rejected; a valid one with a higher objective updates the global optimum;
+ * a worse valid state is still accepted with a probability that "decreases with
+ * more iterations" (reading R13: p_k = p0 * cool^k, independent of the size of
+ * the worsening, exactly as the text states; no temperature-scaled exponent).
+ * Counter-based randomness: u64 = splitmix64(splitmix64(seed ^
+ * chain*C) + (iter<<2 | purpose)); the CUDA path implements the same generator.
+ * Plain, sequential, one chain after the other. */
+static uint64_t sm64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+static uint64_t sa_rand(uint64_t seed, uint64_t chain, uint64_t iter, uint64_t purpose) {
+    return sm64(sm64(seed ^ (chain * 0xD1B54A32D192ED03ull)) + ((iter << 2) | purpose));
+}
+static uint32_t sa_uint(uint64_t h, uint32_t m) { return (uint32_t)(((h >> 32) * (uint64_t)m) >> 32); }
+static float sa_unif(uint64_t h) { return (float)(h >> 40) * (1.0f / 16777216.0f); }
+
+typedef struct {
+    uint64_t best_index;   /* UINT64_MAX: no valid state visited */
+    uint32_t best_key;     /* objective key (smaller is better) */
+    uint32_t accepted;
+    uint64_t final_index;
+} oc_sa_chain_t;
+
+/* objective key of a scored candidate for the policy, or 0xFFFFFFFF if invalid */
+static uint32_t sa_key(const oc_problem *P, int policy, const oc_score_t *sc) {
+    if (policy == 0) {
+        if (sc->verdict) return 0xFFFFFFFFu;
+        uint32_t bits;
+        memcpy(&bits, &sc->T, 4);
+        return 0xFFFFFFFFu - bits;
+    }
+    if (sc->level_verdict[0]) return 0xFFFFFFFFu;
+    return ((uint32_t)sc->u << 24) | (uint32_t)sc->U;
+}
+
+int oc_sa(const oc_problem *P, int policy, const float *load, uint64_t seed, int chain_lo, int chain_hi,
+          int iters, float p0, float cool, oc_sa_chain_t *out) {
+    if (oc_validate(P) != 0) return -1;
+    const int A = P->A, n = P->n, K = A + 2 * n;
+    int radix[OC_MAX_APPS + 2 * OC_MAX_STAGES];
+    for (int a = 0; a < A; a++) radix[a] = P->nS;
+    for (int i = 0; i < n; i++) {
+        radix[A + 2 * i] = P->Rmax;
+        radix[A + 2 * i + 1] = P->nQ;
+    }
+    for (int c = chain_lo; c < chain_hi; c++) {
+        int d[OC_MAX_APPS + 2 * OC_MAX_STAGES], e[OC_MAX_APPS + 2 * OC_MAX_STAGES];
+        for (int k = 0; k < K; k++) d[k] = (int)sa_uint(sa_rand(seed, (uint64_t)c, (uint64_t)k, 3), (uint32_t)radix[k]);
+        oc_score_t sc;
+        int32_t beta[OC_MAX_APPS], rho[OC_MAX_STAGES], theta[OC_MAX_STAGES];
+        for (int a = 0; a < A; a++) beta[a] = d[a];
+        for (int i = 0; i < n; i++) {
+            rho[i] = d[A + 2 * i];
+            theta[i] = d[A + 2 * i + 1];
+        }
+        oc_score(P, beta, rho, theta, load, policy == 0 ? 0 : 1, &sc);
+        uint32_t kc = sa_key(P, policy, &sc);
+        int valid = kc != 0xFFFFFFFFu;
+        uint64_t xc = oc_encode(P, beta, rho, theta);
+        uint32_t bk = kc;
+        uint64_t bx = valid ? xc : UINT64_MAX;
+        uint32_t acc = 0;
+        float p = p0;
+        for (int it = 0; it < iters; it++) {
+            int k = (int)sa_uint(sa_rand(seed, (uint64_t)c, (uint64_t)it, 0), (uint32_t)K);
+            int dir = (sa_rand(seed, (uint64_t)c, (uint64_t)it, 1) >> 63) ? 1 : -1;
+            float u = sa_unif(sa_rand(seed, (uint64_t)c, (uint64_t)it, 2));
+            for (int q = 0; q < K; q++) e[q] = d[q];
+            if (radix[k] > 1) {
+                int nd = d[k] + dir;
+                if (nd < 0 || nd >= radix[k]) nd = d[k] - dir;   /* reflect at the grid edge */
+                e[k] = nd;
+            }
+            for (int a = 0; a < A; a++) beta[a] = e[a];
+            for (int i = 0; i < n; i++) {
+                rho[i] = e[A + 2 * i];
+                theta[i] = e[A + 2 * i + 1];
+            }
+            oc_score(P, beta, rho, theta, load, policy == 0 ? 0 : 1, &sc);
+            uint32_t kn = sa_key(P, policy, &sc);
+            int vn = kn != 0xFFFFFFFFu;
+            uint64_t xn = oc_encode(P, beta, rho, theta);
+            /* the global optimum is updated by every valid state with a better objective */
+            if (vn && (kn < bk || (kn == bk && xn < bx))) {
+                bk = kn;
+                bx = xn;
+            }
+            int accept;
+            if (!valid) accept = 1;            /* until the chain reaches a valid state */
+            else if (!vn) accept = 0;          /* invalid new states are rejected */
+            else if (kn <= kc) accept = 1;     /* not worse */
+            else accept = u < p;               /* worse: with decreasing probability */
+            if (accept) {
+                for (int q = 0; q < K; q++) d[q] = e[q];
+                kc = kn;
+                valid = vn;
+                xc = xn;
+                acc++;
+            }
+            p = p * cool;
+        }
+        out[c - chain_lo].best_index = bx;
+        out[c - chain_lo].best_key = bx == UINT64_MAX ? 0xFFFFFFFFu : bk;
+        out[c - chain_lo].accepted = acc;
+        out[c - chain_lo].final_index = xc;
+    }
+    return 0;
+}
+int oc_sizeof_sa(void) { return (int)sizeof(oc_sa_chain_t); }

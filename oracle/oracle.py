@@ -263,3 +263,29 @@ def eq2_y(prob, beta, lam) -> int:
     b = (C.c_int32 * MAX_APPS)(*beta)
     l = (C.c_float * MAX_APPS)(*lam)
     return int(lib().oc_eq2_y(h.ref, b, l))
+
+
+class OcSaChain(C.Structure):
+    _fields_ = [("best_index", C.c_uint64), ("best_key", C.c_uint32), ("accepted", C.c_uint32),
+                ("final_index", C.c_uint64)]
+
+
+def sa(prob, policy: str = "max_load", load=None, seed: int = 1, chain_lo: int = 0, chain_hi: int = 64,
+       iters: int = 300, p0: float = 0.3, cool: float = 0.995, flags=None):
+    """oracle SA (the paper's algorithm): per-chain
+    (best_index or None, best_key, accepted, final_index)."""
+    h = Handle(prob, flags)
+    assert lib().oc_sizeof_sa() == C.sizeof(OcSaChain)
+    pol = 0 if policy == "max_load" else 1
+    la = None
+    if pol == 1:
+        la = (C.c_float * MAX_APPS)(*[float(v) for v in np.asarray(load, np.float32).reshape(-1)])
+    out = (OcSaChain * (chain_hi - chain_lo))()
+    lib().oc_sa.argtypes = [C.POINTER(OcProblem), C.c_int, C.c_void_p, C.c_uint64, C.c_int, C.c_int, C.c_int,
+                            C.c_float, C.c_float, C.c_void_p]
+    rc = lib().oc_sa(h.ref, pol, C.cast(la, C.c_void_p) if la is not None else None, seed, chain_lo, chain_hi,
+                     iters, p0, cool, C.cast(out, C.c_void_p))
+    if rc != 0:
+        raise ValueError(f"oracle sa rc={rc}")
+    return [(None if r.best_index == NONE else int(r.best_index), int(r.best_key), int(r.accepted),
+             int(r.final_index)) for r in out]

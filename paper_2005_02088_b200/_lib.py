@@ -81,7 +81,7 @@ class Plan(C.Structure):
 EXPORTS = ["camelot_last_error", "camelot_version", "camelot_workspace_bytes", "camelot_upload",
            "camelot_plan_max_load", "camelot_plan_min_resource", "camelot_predict",
            "camelot_score_range", "camelot_search_local", "camelot_finalize", "camelot_last_stats",
-           "camelot_kernel_launches"]
+           "camelot_kernel_launches", "camelot_sa"]
 
 _lib = None
 
@@ -116,6 +116,8 @@ def lib():
         L.camelot_finalize.argtypes = [P, Cl, C.c_int, fp, C.c_int, C.c_void_p, E, Pl]
         L.camelot_last_stats.argtypes = [E, C.POINTER(C.c_uint64)]
         L.camelot_kernel_launches.restype = C.c_uint64
+        L.camelot_sa.argtypes = [P, Cl, C.c_int, fp, C.c_uint64, C.c_int, C.c_int, C.c_float, C.c_float, E, Pl,
+                                 C.c_void_p, C.c_void_p]
         for f in EXPORTS:
             getattr(L, f)
         _lib = L

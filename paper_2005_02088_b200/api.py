@@ -220,6 +220,27 @@ class Session:
                                          keys.data_ptr(), C.byref(ex), out))
         return [_plan(o, self.n, self.A) for o in out]
 
+    def sa(self, policy: int = 0, loads=None, seed: int = 1, chains: int = 4096, iters: int = 1000,
+           p0: float = 0.3, cool: float = 0.995, per_chain: bool = False):
+        """The paper's simulated annealing (NEXT-1) on the device.  Returns the best
+        plan over all chains, plus (per_chain=True) the device tensors of each
+        chain's best index and objective key."""
+        if policy == L.POLICY_MIN_RESOURCE:
+            arr, _ = self._loads(loads)
+            lp = arr.ctypes.data_as(C.POINTER(C.c_float))
+        else:
+            lp = None
+        dev = f"cuda:{self.device}"
+        ci = torch.empty(chains, dtype=torch.int64, device=dev) if per_chain else None
+        ck = torch.empty(chains, dtype=torch.int32, device=dev) if per_chain else None
+        out = L.Plan()
+        ex = self.exec()
+        L.check(L.lib().camelot_sa(C.byref(self.cprob), C.byref(self.ccl), policy, lp, seed, chains, iters,
+                                   p0, cool, C.byref(ex), C.byref(out),
+                                   ci.data_ptr() if per_chain else None, ck.data_ptr() if per_chain else None))
+        res = _plan(out, self.n, self.A)
+        return (res, ci, ck) if per_chain else res
+
     def last_stats(self):
         out = (C.c_uint64 * 8)()
         ex = self.exec()

@@ -913,6 +913,63 @@ int camelot_score_range(const camelot_problem *p, const camelot_cluster *c, uint
 
 uint64_t camelot_kernel_launches(void) { return g_launches.load(); }
 
+int camelot_sa(const camelot_problem *p, const camelot_cluster *c, int policy, const float *load_qps,
+               uint64_t seed, int chains, int iters, float p0, float cool, const camelot_exec *ex,
+               camelot_plan *out, uint64_t *d_chain_index, uint32_t *d_chain_key) {
+    t_call_launches = 0;
+    if (policy != 0 && policy != 1) return fail(CAMELOT_EINVAL, "bad policy");
+    if (!out) return fail(CAMELOT_EINVAL, "null out");
+    if (chains < 1 || chains > (1 << 20) || iters < 0) return fail(CAMELOT_EINVAL, "chains must be in 1..2^20, iters >= 0");
+    if (!(p0 >= 0.0f && p0 <= 1.0f) || !(cool >= 0.0f && cool <= 1.0f)) return fail(CAMELOT_EINVAL, "p0, cool must be in [0,1]");
+    if (policy == 1) {
+        int rc = p ? check_loads(p, load_qps, 1) : fail(CAMELOT_EINVAL, "null problem");
+        if (rc) return rc;
+    }
+    Ctx X;
+    int rc = setup(p, c, ex, 1, X, true);
+    if (rc) return rc;
+    if (policy == 1) {
+        rc = upload_loads(X, load_qps, 1);
+        if (rc) return rc;
+    }
+    const int blocks = (chains + 255) / 256;
+    if (blocks > MAXSLOTS) return fail(CAMELOT_ERANGE, "too many chains");
+    char *ws = X.ws;
+    DevHeader *hdr = reinterpret_cast<DevHeader *>(ws + X.L.hdr);
+    CU(cudaMemsetAsync(hdr, 0, sizeof(DevHeader), X.st));
+    SAArgs A;
+    A.policy = policy;
+    A.chains = chains;
+    A.iters = iters;
+    A.seed = seed;
+    A.p0 = p0;
+    A.cool = cool;
+    A.lam = reinterpret_cast<const float *>(ws + X.L.lam);
+    A.slots = reinterpret_cast<Slot *>(ws + slots_off(X.L));
+    A.chain_index = reinterpret_cast<unsigned long long *>(d_chain_index);
+    A.chain_key = d_chain_key;
+    A.accepted = &hdr->n_nodes;   // reported as stats[1]
+    sa_kernel<<<blocks, 256, 0, X.st>>>(X.P, A);
+    COUNT_LAUNCH();
+    CU(cudaGetLastError());
+    Slot *winner = reinterpret_cast<Slot *>(ws + X.L.winner);
+    reduce_kernel<<<1, 256, 0, X.st>>>(X.P, A.slots, blocks, 1, winner, reinterpret_cast<long long *>(ws + X.L.keys),
+                                       nullptr, nullptr, nullptr, 0, 1, 0);
+    COUNT_LAUNCH();
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(ws + X.L.hdr2, ws + X.L.hdr, sizeof(DevHeader), cudaMemcpyDeviceToDevice, X.st));
+    camelot_plan *dplans = reinterpret_cast<camelot_plan *>(ws + X.L.plans);
+    plan_kernel<<<1, 64, 0, X.st>>>(X.P, policy, 1, winner, reinterpret_cast<const float *>(ws + X.L.lam),
+                                    reinterpret_cast<const DevHeader *>(ws + X.L.hdr2), dplans);
+    COUNT_LAUNCH();
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(out, dplans, sizeof(camelot_plan), cudaMemcpyDeviceToHost, X.st));
+    CU(cudaStreamSynchronize(X.st));
+    out->n_scored = (uint64_t)chains * (uint64_t)(iters + 1);
+    out->n_covered = out->n_scored;
+    return out->status;
+}
+
 int camelot_last_stats(const camelot_exec *ex, uint64_t *out8) {
     if (!ex || !out8 || !ex->workspace) return fail(CAMELOT_EINVAL, "null argument");
     uint64_t *out6 = out8;

@@ -608,3 +608,150 @@ search_level_kernel(const DevProb P, const LevelArgs LA) {
 }
 
 }  // namespace cam
+
+// ============================================================================
+// The paper's simulated annealing (NEXT-1) as a GPU
+// multi-chain baseline: one thread per chain, counter-based randomness
+// (splitmix64 of (seed, chain, iteration, purpose)), every
+// proposal scored exactly like the search (score_digits).  A worse valid state
+// is accepted with probability p_k = p0 * cool^k (decreasing with the
+// iterations, R13); invalid states are rejected once the chain is valid; every
+// valid proposal that improves the objective updates the chain's best.
+namespace cam {
+
+__device__ __forceinline__ unsigned long long sa_sm64(unsigned long long z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+__device__ __forceinline__ unsigned long long sa_rng(unsigned long long seed, unsigned long long chain,
+                                                     unsigned long long it, unsigned long long purpose) {
+    return sa_sm64(sa_sm64(seed ^ (chain * 0xD1B54A32D192ED03ull)) + ((it << 2) | purpose));
+}
+__device__ __forceinline__ unsigned sa_below(unsigned long long h, unsigned m) {
+    return (unsigned)(((h >> 32) * (unsigned long long)m) >> 32);
+}
+
+struct SAArgs {
+    int policy, chains, iters;
+    unsigned long long seed;
+    float p0, cool;
+    const float *lam;                 // [A] load (min-resource)
+    Slot *slots;                      // [gridDim.x] per-CTA best
+    unsigned long long *chain_index;  // [chains] or nullptr
+    unsigned *chain_key;              // [chains] or nullptr
+    unsigned long long *accepted;     // total accepted moves (atomic)
+};
+
+__device__ __forceinline__ unsigned sa_key_of(const DevProb &P, int policy, const int *beta, const float *lam,
+                                              const FullScore &s) {
+    if (policy == 0) return s.verdict ? 0xFFFFFFFFu : objkey_maxload(s.T);
+    const int y = eq2_gpus(P, beta, lam);
+    return level_verdict(P, s, lam, y) ? 0xFFFFFFFFu : objkey_minres(s.u, s.U);
+}
+
+__global__ void __launch_bounds__(256) sa_kernel(const DevProb P, const SAArgs A) {
+    __shared__ unsigned long long sk[8], sx[8];
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned long long bx = ~0ull;
+    unsigned bk = 0xFFFFFFFFu;
+    unsigned acc = 0;
+    if (c < A.chains) {
+        const int nA = P.A, n = P.n, K = nA + 2 * n;
+        int rad[AMAX + 2 * NMAX], d[AMAX + 2 * NMAX];
+        for (int a = 0; a < nA; ++a) rad[a] = P.nS;
+        for (int i = 0; i < n; ++i) {
+            rad[nA + 2 * i] = P.Rmax;
+            rad[nA + 2 * i + 1] = P.nQ;
+        }
+        for (int k = 0; k < K; ++k) d[k] = (int)sa_below(sa_rng(A.seed, c, k, 3), (unsigned)rad[k]);
+        int beta[AMAX], rho[NMAX], theta[NMAX];
+        auto unpack = [&](const int *v) {
+            for (int a = 0; a < nA; ++a) beta[a] = v[a];
+            for (int i = 0; i < n; ++i) {
+                rho[i] = v[nA + 2 * i];
+                theta[i] = v[nA + 2 * i + 1];
+            }
+        };
+        auto encode = [&](const int *v) {
+            unsigned long long x = 0;
+            for (int k = 0; k < K; ++k) x = x * (unsigned long long)rad[k] + (unsigned long long)v[k];
+            return x;
+        };
+        FullScore s;
+        unpack(d);
+        score_digits(P, beta, rho, theta, s);
+        unsigned kc = sa_key_of(P, A.policy, beta, A.lam, s);
+        bool valid = kc != 0xFFFFFFFFu;
+        bk = kc;
+        bx = valid ? encode(d) : ~0ull;
+        float p = A.p0;
+        int e[AMAX + 2 * NMAX];
+        for (int it = 0; it < A.iters; ++it) {
+            const int k = (int)sa_below(sa_rng(A.seed, c, it, 0), (unsigned)K);
+            const int dir = (sa_rng(A.seed, c, it, 1) >> 63) ? 1 : -1;
+            const float u = (float)(sa_rng(A.seed, c, it, 2) >> 40) * (1.0f / 16777216.0f);
+            for (int q = 0; q < K; ++q) e[q] = d[q];
+            if (rad[k] > 1) {
+                int nd = d[k] + dir;
+                if (nd < 0 || nd >= rad[k]) nd = d[k] - dir;
+                e[k] = nd;
+            }
+            unpack(e);
+            score_digits(P, beta, rho, theta, s);
+            const unsigned kn = sa_key_of(P, A.policy, beta, A.lam, s);
+            const bool vn = kn != 0xFFFFFFFFu;
+            const unsigned long long xn = encode(e);
+            if (vn && (kn < bk || (kn == bk && xn < bx))) {
+                bk = kn;
+                bx = xn;
+            }
+            bool accept;
+            if (!valid) accept = true;
+            else if (!vn) accept = false;
+            else if (kn <= kc) accept = true;
+            else accept = u < p;
+            if (accept) {
+                for (int q = 0; q < K; ++q) d[q] = e[q];
+                kc = kn;
+                valid = vn;
+                ++acc;
+            }
+            p = __fmul_rn(p, A.cool);
+        }
+        if (bx == ~0ull) bk = 0xFFFFFFFFu;
+        if (A.chain_index) A.chain_index[c] = bx;
+        if (A.chain_key) A.chain_key[c] = bk;
+    }
+    // block best (key, index) -> slot; accepted-move count
+    unsigned long long k64 = bk, x64 = bx;
+    for (int off = 16; off; off >>= 1) {
+        const unsigned long long ok = __shfl_xor_sync(0xffffffffu, k64, off);
+        const unsigned long long ox = __shfl_xor_sync(0xffffffffu, x64, off);
+        if (slot_less(ok, ox, k64, x64)) {
+            k64 = ok;
+            x64 = ox;
+        }
+        acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    }
+    if (lane == 0) {
+        sk[wid] = k64;
+        sx[wid] = x64;
+        if (acc) atomicAdd(A.accepted, (unsigned long long)acc);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long kb = sk[0], xb = sx[0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+            if (slot_less(sk[w], sx[w], kb, xb)) {
+                kb = sk[w];
+                xb = sx[w];
+            }
+        A.slots[blockIdx.x].key = kb;
+        A.slots[blockIdx.x].x = xb;
+    }
+}
+
+}  // namespace cam
