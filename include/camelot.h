@@ -249,6 +249,15 @@ int camelot_finalize(const camelot_problem *p, const camelot_cluster *c, int pol
  * evaluated over the cascade and the main pass. */
 int camelot_last_stats(const camelot_exec *exec, uint64_t *out8);
 
+/* Phase trace of the last search on this workspace (profiling aid; host
+ * out[cap], synchronises the stream).  Block 0 of every search-level launch
+ * (incumbent cascade levels, then the main pass) records, after each grid-wide
+ * barrier, (tag << 48) | (%globaltimer ns & 2^48-1) with tag 0 = launch start,
+ * 1 = header reset, 2 = option filter, 3 = item offsets, 16+j = pass j,
+ * 32 = CTA reduction.  Returns the number of entries recorded (may exceed cap;
+ * at most 256 are kept) or a negative status. */
+int camelot_trace(const camelot_exec *exec, uint64_t *out, int cap);
+
 /* Process-wide number of kernels launched by this library so far. */
 uint64_t camelot_kernel_launches(void);
 

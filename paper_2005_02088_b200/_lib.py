@@ -8,6 +8,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import re
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -23,8 +24,9 @@ V_QUOTA, V_INST, V_MEM, V_BW, V_QOS, V_LOAD, V_EQ2 = 1, 2, 4, 8, 16, 32, 64
 POLICY_MAX_LOAD, POLICY_MIN_RESOURCE = 0, 1
 EXEC_RESIDENT = 1
 
-NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-fmad=false", "-Xcompiler", "-fPIC", "-shared", "-cudart", "static"]
+NVCC_FLAGS_OBJ = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+                  "-fmad=false", "-Xcompiler", "-fPIC"]
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-Xcompiler", "-fPIC", "-shared", "-cudart", "static"]
 
 
 def sources():
@@ -32,13 +34,48 @@ def sources():
             if f.endswith((".cu", ".cuh"))] + [HEADER]
 
 
+def _deps(path, seen=None):
+    """Transitive quoted #include files of a source (dependency tracking)."""
+    seen = set() if seen is None else seen
+    if path in seen or not os.path.exists(path):
+        return seen
+    seen.add(path)
+    with open(path) as f:
+        for line in f:
+            m = re.match(r'\s*#\s*include\s+"([^"]+)"', line)
+            if m:
+                _deps(os.path.normpath(os.path.join(os.path.dirname(path), m.group(1))), seen)
+    return seen
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile libcamelot.so for sm_100a (in-tree)."""
-    newest = max(os.path.getmtime(s) for s in sources())
-    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < newest:
-        cmd = ["nvcc"] + NVCC_FLAGS + (["-Xptxas", "-v"] if verbose else []) + \
-              ["-o", LIB, os.path.join(CSRC, "camelot_api.cu")]
-        subprocess.check_call(cmd)
+    """Compile libcamelot.so for sm_100a (in-tree): one object per translation
+    unit (rebuilt when it or an included header changed), compiled in parallel,
+    linked into one shared library."""
+    extra = os.environ.get("CAMELOT_NVCC_EXTRA", "").split()   # e.g. -DCAMELOT_FTRACE (profiling)
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+    stamp = os.path.join(objdir, "flags.txt")
+    flags = " ".join(NVCC_FLAGS_OBJ + extra)
+    if not os.path.exists(stamp) or open(stamp).read() != flags:
+        force = True
+    tus = sorted(f for f in os.listdir(CSRC) if f.endswith(".cu"))
+    objs, procs = [], []
+    for tu in tus:
+        src = os.path.join(CSRC, tu)
+        obj = os.path.join(objdir, tu[:-3] + ".o")
+        objs.append(obj)
+        newest = max(os.path.getmtime(d) for d in _deps(src))
+        if force or not os.path.exists(obj) or os.path.getmtime(obj) < newest:
+            cmd = ["nvcc"] + NVCC_FLAGS_OBJ + extra + (["-Xptxas", "-v"] if verbose else []) + ["-c", "-o", obj, src]
+            procs.append((cmd, subprocess.Popen(cmd)))
+    for cmd, pr in procs:
+        if pr.wait() != 0:
+            raise subprocess.CalledProcessError(pr.returncode, cmd)
+    with open(stamp, "w") as f:
+        f.write(flags)
+    if procs or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
+        subprocess.check_call(["nvcc"] + NVCC_FLAGS + ["-o", LIB] + objs)
     return LIB
 
 
@@ -81,7 +118,7 @@ class Plan(C.Structure):
 EXPORTS = ["camelot_last_error", "camelot_version", "camelot_workspace_bytes", "camelot_upload",
            "camelot_plan_max_load", "camelot_plan_min_resource", "camelot_predict",
            "camelot_score_range", "camelot_search_local", "camelot_finalize", "camelot_last_stats",
-           "camelot_kernel_launches", "camelot_sa"]
+           "camelot_kernel_launches", "camelot_sa", "camelot_trace"]
 
 _lib = None
 
@@ -115,6 +152,7 @@ def lib():
         L.camelot_search_local.argtypes = [P, Cl, C.c_int, fp, C.c_int, E, C.c_void_p]
         L.camelot_finalize.argtypes = [P, Cl, C.c_int, fp, C.c_int, C.c_void_p, E, Pl]
         L.camelot_last_stats.argtypes = [E, C.POINTER(C.c_uint64)]
+        L.camelot_trace.argtypes = [E, C.POINTER(C.c_uint64), C.c_int]
         L.camelot_kernel_launches.restype = C.c_uint64
         L.camelot_sa.argtypes = [P, Cl, C.c_int, fp, C.c_uint64, C.c_int, C.c_int, C.c_float, C.c_float, E, Pl,
                                  C.c_void_p, C.c_void_p]

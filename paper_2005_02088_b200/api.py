@@ -248,6 +248,18 @@ class Session:
         return dict(n_scored=out[0], n_nodes=out[1], n_feasible=out[2], t_ns=out[3], items=out[4],
                     launches=out[5], cum_scored=out[6], cum_nodes=out[7])
 
+    def trace(self):
+        """Phase timestamps of the last search: [(tag, ns since the first mark)]."""
+        out = (C.c_uint64 * 256)()
+        n = L.lib().camelot_trace(C.byref(self.exec()), out, 256)
+        L.check(min(n, 0), False)
+        if n == 0:
+            return []
+        t0 = out[0] & ((1 << 48) - 1)
+        m = (1 << 48) - 1
+        # tags < 64 are timestamps (ns since the first mark), tags >= 64 are values
+        return [(out[i] >> 48, (out[i] & m) - (t0 if (out[i] >> 48) < 64 else 0)) for i in range(min(n, 256))]
+
 
 # ---------------------------------------------------------------------- functional API
 def plan_max_load(problem, **kw) -> PlanResult:

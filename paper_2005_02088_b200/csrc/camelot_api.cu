@@ -17,6 +17,12 @@
 
 #include "../../include/camelot.h"
 #include "camelot_kernels.cuh"
+#include "camelot_sweep_args.h"
+
+namespace cam {   // camelot_sweep.cu
+bool sweep_supported(const DevProb &P, int policy, int nlev);
+cudaError_t sweep_launch(const DevProb &P, const SweepArgs &A, int dev, cudaStream_t st);
+}  // namespace cam
 
 using namespace cam;
 
@@ -512,6 +518,58 @@ int run_passes(const Ctx &X, int dev, int policy, SearchArgs S, bool timed, bool
     return CAMELOT_OK;
 }
 
+// exhaustive scan (NO_FILTER) through the leaf-sweep kernel: the option lists are
+// still built (full, unfiltered) for a possible chunk re-scan by the tree search
+int sweep_pass(const Ctx &X, int dev, int policy, int nlev, const Slot *inc, Slot *result, long long *keys,
+               int rank, int world, unsigned long long lo, unsigned long long hi) {
+    char *ws = X.ws;
+    DevHeader *hdr = reinterpret_cast<DevHeader *>(ws + X.L.hdr);
+    CU(cudaMemsetAsync(hdr, 0, offsetof(DevHeader, cum_scored), X.st));
+    CU(cudaMemsetAsync(&hdr->best_obj, 0xFF, sizeof(unsigned int), X.st));
+    FilterArgs F;
+    memset(&F, 0, sizeof(F));
+    F.policy = policy;
+    F.prune = 0;
+    F.stride = 1;
+    F.nlev = nlev;
+    F.inc = inc;
+    F.lam = reinterpret_cast<const float *>(ws + X.L.lam);
+    F.rec = reinterpret_cast<OptRec *>(ws + X.L.rec);
+    F.sb = reinterpret_cast<StageBound *>(ws + X.L.sb);
+    F.item_off = reinterpret_cast<unsigned long long *>(ws + X.L.item_off);
+    F.hdr = hdr;
+    F.d0 = X.d0;
+    filter_kernel<<<X.d.nS, FILTER_THREADS, 0, X.st>>>(X.P, F);
+    COUNT_LAUNCH();
+    CU(cudaGetLastError());
+    SweepArgs A;
+    memset(&A, 0, sizeof(A));
+    A.policy = policy;
+    A.rank = rank;
+    A.world = world;
+    A.d0 = X.d0;
+    A.lo = lo;
+    A.hi = hi;
+    const unsigned long long O2 = (unsigned long long)X.d.O * (unsigned long long)X.d.O;
+    A.nchunk = (X.d.O + 31) / 32;
+    if (hi > lo) {
+        A.g_lo = lo / O2;
+        A.n_items = ((hi - 1) / O2 + 1 - A.g_lo) * (unsigned long long)A.nchunk;
+    }
+    A.lam = reinterpret_cast<const float *>(ws + X.L.lam);
+    A.y = reinterpret_cast<const int *>(ws + X.L.y);
+    A.ystride = nlev;
+    A.yoff = 0;
+    A.inc = inc;
+    A.slots = reinterpret_cast<Slot *>(ws + slots_off(X.L));
+    A.hdr = hdr;
+    A.result = result;
+    A.keys = keys;
+    CU(sweep_launch(X.P, A, dev, X.st));
+    COUNT_LAUNCH();
+    return CAMELOT_OK;
+}
+
 int search_pass(const Ctx &X, int dev, int policy, int nlev, bool prune, int stride, const Slot *inc,
                 Slot *result, long long *keys, int rank, int world, unsigned long long lo, unsigned long long hi,
                 bool timed, Slot *inc_out = nullptr) {
@@ -520,6 +578,8 @@ int search_pass(const Ctx &X, int dev, int policy, int nlev, bool prune, int str
         return flat_pass(X, dev, policy, nlev, nlev, 0, reinterpret_cast<const float *>(ws + X.L.lam), inc, result,
                          keys, rank, world, lo, hi);
     DevHeader *hdr = reinterpret_cast<DevHeader *>(ws + X.L.hdr);
+    if (!prune && sweep_supported(X.P, policy, nlev) && !getenv("CAMELOT_NO_SWEEP"))
+        return sweep_pass(X, dev, policy, nlev, inc, result, keys, rank, world, lo, hi);
     const bool coop = use_coop();
     if (!coop) {
         CU(cudaMemsetAsync(hdr, 0, offsetof(DevHeader, cum_scored), X.st));
@@ -686,7 +746,7 @@ int local_search(const Ctx &X, const camelot_exec *ex, int policy, int nlev, lon
     int rc;
     {
         DevHeader *hdr = reinterpret_cast<DevHeader *>(ws + X.L.hdr);
-        CU(cudaMemsetAsync(&hdr->cum_scored, 0, 2 * sizeof(unsigned long long), X.st));
+        CU(cudaMemsetAsync(&hdr->cum_scored, 0, 2 * sizeof(unsigned long long) + 2 * sizeof(unsigned int), X.st));
     }
     if (t_ev.dev != dev) {
         if (t_ev.a) {
@@ -992,6 +1052,17 @@ int camelot_last_stats(const camelot_exec *ex, uint64_t *out8) {
     out8[6] = h.cum_scored;
     out8[7] = h.cum_nodes;
     return CAMELOT_OK;
+}
+
+int camelot_trace(const camelot_exec *ex, uint64_t *out, int cap) {
+    if (!ex || !out || cap < 0 || !ex->workspace) return fail(CAMELOT_EINVAL, "null argument");
+    DevHeader h;
+    cudaStream_t st = static_cast<cudaStream_t>(ex->stream);
+    CU(cudaMemcpyAsync(&h, static_cast<char *>(ex->workspace) + al(sizeof(DevHeader)), sizeof(h), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    const int n = (int)std::min<unsigned>(h.trace_n, (unsigned)TRACE_MAX);
+    for (int i = 0; i < n && i < cap; ++i) out[i] = h.trace[i];
+    return n;
 }
 
 }  // extern "C"

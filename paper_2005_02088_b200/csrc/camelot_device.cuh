@@ -12,6 +12,7 @@ namespace cam {
 constexpr int NMAX = 8;      // stages
 constexpr int AMAX = 2;      // applications
 constexpr int LMAX = 64;     // load levels
+constexpr int TRACE_MAX = 256;
 
 constexpr uint32_t F_NO_BW_CAP = 1u, F_NO_CONTENTION = 2u, F_SAT = 4u, F_PAPER_GLOBAL = 8u,
                    F_EQ2_BUDGET = 16u, F_NO_FILTER = 32u;
@@ -76,9 +77,27 @@ struct DevHeader {
     unsigned long long best_packed;      // (objective key << 32) | (index >> xshift), atomicMin (1 level)
     unsigned long long head[NMAX + 1];   // pop counter of pass j
     unsigned long long tail[NMAX + 1];   // size of the frontier at depth j (may exceed capacity)
+    unsigned long long dbg_batches[NMAX + 1], dbg_maxb[NMAX + 1];   // profiling (CAMELOT_FTRACE)
     // cumulative over the incumbent cascade + main search of one call (not reset per pass)
     unsigned long long cum_scored, cum_nodes;
+    // phase trace of the last search (camelot_trace): block 0 of every search-level
+    // launch appends (tag << 48 | %globaltimer ns) after each grid barrier
+    unsigned int trace_n, trace_pad;
+    unsigned long long trace[TRACE_MAX];
 };
+
+__device__ __forceinline__ void trace_value(DevHeader *h, unsigned tag, unsigned long long v) {
+    const unsigned i = h->trace_n;
+    if (i < (unsigned)TRACE_MAX) h->trace[i] = ((unsigned long long)tag << 48) | (v & 0xFFFFFFFFFFFFull);
+    h->trace_n = i + 1;
+}
+__device__ __forceinline__ void trace_mark(DevHeader *h, unsigned tag) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const unsigned i = h->trace_n;
+    if (i < (unsigned)TRACE_MAX) h->trace[i] = ((unsigned long long)tag << 48) | (t & 0xFFFFFFFFFFFFull);
+    h->trace_n = i + 1;
+}
 
 struct Slot {                      // (objective key, canonical index), smaller is better
     unsigned long long key, x;

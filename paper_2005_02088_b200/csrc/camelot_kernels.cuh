@@ -45,6 +45,11 @@ struct FilterSmem {
 };
 
 // Filter body for batch b, executed by one whole CTA (any blockDim multiple of 32).
+#ifdef CAMELOT_FTRACE
+#define FTRACE(t) if (blockIdx.x == 0 && threadIdx.x == 0) trace_mark(F.hdr, t)
+#else
+#define FTRACE(t)
+#endif
 __device__ void filter_body(const DevProb &P, const FilterArgs &F, int b, FilterSmem &fsm) {
     auto &keep = fsm.keep;
     auto &mindur = fsm.mindur;
@@ -56,6 +61,7 @@ __device__ void filter_body(const DevProb &P, const FilterArgs &F, int b, Filter
     for (int q = tid; q < n * nQ; q += blockDim.x) tabs[q] = P.tab[((size_t)(q / nQ) * P.nS + b) * nQ + q % nQ];
     for (int q = tid; q < nQ; q += blockDim.x) Qs[q] = P.Q[q];
     __syncthreads();
+    FTRACE(4);
     const bool cap = !(P.flags & F_NO_BW_CAP);
     // incumbent
     unsigned long long ikey = 0xFFFFFFFFull;
@@ -89,6 +95,7 @@ __device__ void filter_body(const DevProb &P, const FilterArgs &F, int b, Filter
         keep[i][o] = k;
     }
     __syncthreads();
+    FTRACE(5);
     const int rounds = F.prune ? 3 : 0;
     for (int it = 0; it <= rounds; ++it) {
         // per-stage minima over surviving options (warp w: stage w)
@@ -111,6 +118,7 @@ __device__ void filter_body(const DevProb &P, const FilterArgs &F, int b, Filter
             }
         }
         __syncthreads();
+        FTRACE(6);
         if (it == rounds) break;
         for (int idx = tid; idx < n * O; idx += blockDim.x) {
             const int i = idx / O, o = idx % O;
@@ -137,6 +145,7 @@ __device__ void filter_body(const DevProb &P, const FilterArgs &F, int b, Filter
             if (!k) keep[i][o] = 0;
         }
         __syncthreads();
+        FTRACE(7);
     }
     // compaction in ascending option code (warp w: stage w) + records
     for (int i = wid; i < n; i += (int)(blockDim.x >> 5)) {
@@ -179,6 +188,8 @@ __device__ void filter_body(const DevProb &P, const FilterArgs &F, int b, Filter
             F.sb[(size_t)i * P.nS + b] = s;
         }
     }
+    __syncthreads();
+    FTRACE(8);
 }
 
 // One CTA per batch index b: filters the options of every stage at batch b
@@ -542,6 +553,8 @@ search_level_kernel(const DevProb P, const LevelArgs LA) {
     SearchArgs S = LA.S;
     DevHeader *hdr = S.hdr;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const bool tr = blockIdx.x == 0 && threadIdx.x == 0;
+    if (tr) trace_mark(hdr, 0);
     // phase 0: reset this level's header state (the cumulative counters stay)
     if (blockIdx.x == 0) {
         unsigned *h = reinterpret_cast<unsigned *>(hdr);
@@ -553,6 +566,7 @@ search_level_kernel(const DevProb P, const LevelArgs LA) {
         }
     }
     grid.sync();
+    if (tr) trace_mark(hdr, 1);
     // phase 1: option filter (one CTA per batch) and slot reset
     for (int b = blockIdx.x; b < P.nS; b += gridDim.x) {
         filter_body(P, LA.F, b, *reinterpret_cast<FilterSmem *>(smem_raw));
@@ -563,9 +577,11 @@ search_level_kernel(const DevProb P, const LevelArgs LA) {
         S.slots[q].x = ~0ull;
     }
     grid.sync();
+    if (tr) trace_mark(hdr, 2);
     // phase 2: item offsets (chunk ownership)
     if (blockIdx.x == 0 && threadIdx.x == 0) item_offsets(P, S.sb, S.d0, LA.F.item_off, hdr);
     grid.sync();
+    if (tr) trace_mark(hdr, 3);
     // per-CTA copy of the (stage, batch) bounds in shared memory, after the search state
     {
         StageBound *sbs = reinterpret_cast<StageBound *>(smem_raw + search_smem_bytes<CM>());
@@ -596,9 +612,18 @@ search_level_kernel(const DevProb P, const LevelArgs LA) {
         S.grab = 1;
         pass_body<CM, NS, POLICY>(P, S, stack, ctl, wb, lane, cn);
         grid.sync();
+        if (tr) {
+            trace_mark(hdr, 16 + j);
+#ifdef CAMELOT_FTRACE
+            trace_value(hdr, 64 + j, j == 0 ? (unsigned long long)P.nbc : hdr->tail[j]);   // parents of pass j
+            trace_value(hdr, 80 + j, hdr->dbg_batches[j]);
+            trace_value(hdr, 96 + j, hdr->dbg_maxb[j]);
+#endif
+        }
     }
     cta_finish<CM>(S, wb_all, lane, wid, cn);
     grid.sync();
+    if (tr) trace_mark(hdr, 32);
     // phase 4: reduction of the CTA slots (block 0)
     if (blockIdx.x == 0) {
         unsigned long long *sk = reinterpret_cast<unsigned long long *>(smem_raw);

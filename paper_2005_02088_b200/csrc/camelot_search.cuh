@@ -927,11 +927,17 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
     Node<CM> *outf = reinterpret_cast<Node<CM> *>(S.out_nodes);
     const unsigned long long count = in ? min(*(volatile const unsigned long long *)S.in_count, S.in_cap)
                                         : (unsigned long long)P.nbc;
-    // few parents (shallow passes): each block of 32 children is its own work item
-    const int nblk = (P.O + 31) / 32;
+    // few parents (shallow passes): each block of 32 children is its own work item;
+    // the blocks per parent follow the largest surviving option count of stage jtop
+    int maxc = 0;
+    for (int b = 0; b < P.nS; ++b) maxc = max(maxc, (int)sb_at(P, S, jtop, b).cnt);
+    const int nblk = max(1, (maxc + 31) / 32);
     const int split = (count < 4ull * gridDim.x * SEARCH_WARPS) ? nblk : 1;
     const unsigned long long items = count * (unsigned long long)split;
 
+#ifdef CAMELOT_FTRACE
+    unsigned long long dbg_nb = 0;
+#endif
     while (true) {
         unsigned long long e0 = 0;
         if (lane == 0) e0 = atomicAdd(S.head, (unsigned long long)S.grab);
@@ -1022,6 +1028,9 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
                     continue;
                 }
                 const int endj = ctl->end[j];
+#ifdef CAMELOT_FTRACE
+                ++dbg_nb;
+#endif
                 __syncwarp();
                 if (lane == 0) {
                     ctl->base[j] = base;
@@ -1126,6 +1135,12 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
             }
         }
     }
+#ifdef CAMELOT_FTRACE
+    if (lane == 0 && dbg_nb) {
+        atomicAdd(&S.hdr->dbg_batches[jtop], dbg_nb);
+        atomicMax(&S.hdr->dbg_maxb[jtop], dbg_nb);
+    }
+#endif
 }
 
 // End of a search level for one CTA: merge the warps' bests into the CTA's slot

@@ -1,0 +1,541 @@
+// camelot_sweep.cuh -- the exhaustive (NO_FILTER) scan as an issue-bound
+// "leaf sweep" kernel for sm_100a.
+//
+// The flat scan scores EVERY candidate of [lo, hi) (the
+// state V = [N_1..N_n, p_1..p_n] plus the batch, L858) with the scoring of
+// DESIGN.md 3 (placement L929-945, contention R17, Constraint-5 L834).  Unlike
+// the pruned tree search it has no data-dependent work, so it is laid out for
+// instruction issue:
+//   * a warp owns one GRANDPARENT (batch combo + options of stages 0..n-3,
+//     warp-uniform state placed once) and 32 of its PARENTS (option of stage
+//     n-2): lane = parent, placed by the lane in registers;
+//   * each lane then sweeps ALL leaves (options (N, theta) of the last stage)
+//     of its parent: per quota theta the per-GPU capacities
+//     c_g = canHold(g, Rmax) are computed once and packed as a thermometer
+//     code in deployment order (4 bits per GPU), so for every replica count N
+//     pass 1 of the deployment heuristic is one shift+ffs and pass 2's greedy
+//     prefix is one popc;
+//   * contention: only the GPU(s) receiving the leaf's replicas change demand,
+//     so every placed stage's max demand is updated by a bit test + max;
+//   * every lane keeps its own best (objective key, index); one reduction at
+//     the end.  No shared-memory stacks, no warp synchronisation in the loop.
+// State is indexed by GPU id (no permutation): the deployment order
+// (remaining MiB, remaining quota, id) only enters through the rank shifts.
+#pragma once
+#include "camelot_device.cuh"
+#include "camelot_sweep_args.h"
+
+namespace cam {
+
+constexpr int SWEEP_THREADS = 256;
+
+// SweepArgs: camelot_sweep_args.h
+
+// Thread-level placement state indexed by GPU id.
+template <int CM, int NS>
+struct SwState {
+    int rq[CM], cnt[CM];
+    uint32_t rm[CM];
+    float dem[CM];
+    uint32_t hm[NS];     // GPU mask of stage i
+    float dm[NS];        // max demand over the GPUs hosting stage i
+    int u, U;
+};
+
+template <int CM, int NS>
+__device__ __forceinline__ void sw_init(const DevProb &P, SwState<CM, NS> &s) {
+#pragma unroll
+    for (int g = 0; g < CM; ++g) {
+        s.rq[g] = g < P.C ? P.R : 0;
+        s.cnt[g] = 0;
+        s.rm[g] = g < P.C ? P.FM : 0u;
+        s.dem[g] = 0.0f;
+    }
+#pragma unroll
+    for (int i = 0; i < NS; ++i) {
+        s.hm[i] = 0u;
+        s.dm[i] = 0.0f;
+    }
+    s.u = 0;
+    s.U = 0;
+}
+
+// Deploy stage i with N replicas of quota p:
+// pass 1 = the first GPU in (rm, rq, id) order that holds all N, pass 2 = greedy
+// min(canHold, remaining) in the same order.  Returns false if it does not fit.
+template <int CM, int NS>
+__device__ __forceinline__ bool sw_place(const DevProb &P, SwState<CM, NS> &s, int i, int N, int p,
+                                         uint32_t W, uint32_t As, float bw) {
+    const bool cap = !(P.flags & F_NO_BW_CAP);
+    int c[CM];
+    unsigned long long key[CM];
+#pragma unroll
+    for (int g = 0; g < CM; ++g) {
+        int k = 0;
+        if (g < P.C) {
+            k = min(N, s.rq[g] / p);
+            k = min(k, P.I - s.cnt[g]);
+            if (s.rm[g] < W) k = 0;
+            else if (As > 0u) k = min(k, (int)min((uint32_t)N, (s.rm[g] - W) / As));
+            if (cap)
+                while (k > 0 && __fadd_rn(s.dem[g], __fmul_rn((float)k, bw)) > P.BW) --k;
+            k = max(k, 0);
+        }
+        c[g] = k;
+        key[g] = ((unsigned long long)s.rm[g] << 12) | ((unsigned long long)s.rq[g] << 4) | (unsigned)g;
+    }
+    int gs = -1;
+    unsigned long long best = ~0ull;
+#pragma unroll
+    for (int g = 0; g < CM; ++g)
+        if (c[g] == N && key[g] < best) {
+            best = key[g];
+            gs = g;
+        }
+    int kk[CM];
+    if (gs >= 0) {
+#pragma unroll
+        for (int g = 0; g < CM; ++g) kk[g] = g == gs ? N : 0;
+    } else {
+        int tot = 0;
+#pragma unroll
+        for (int g = 0; g < CM; ++g) tot += c[g];
+        if (tot < N) return false;
+#pragma unroll
+        for (int g = 0; g < CM; ++g) {
+            int pre = 0;   // capacity of the GPUs before g in deployment order
+#pragma unroll
+            for (int h = 0; h < CM; ++h)
+                if (key[h] < key[g]) pre += c[h];
+            kk[g] = min(c[g], max(0, N - pre));
+        }
+    }
+#pragma unroll
+    for (int g = 0; g < CM; ++g) {
+        const int k = kk[g];
+        if (k > 0) {
+            s.u += s.cnt[g] == 0;
+            s.rq[g] -= k * p;
+            s.cnt[g] += k;
+            s.rm[g] -= W + (uint32_t)k * As;
+            s.dem[g] = __fadd_rn(s.dem[g], __fmul_rn((float)k, bw));
+            s.hm[i] |= 1u << g;
+        }
+    }
+    // max demand over the hosting GPUs of every placed stage (demand only grows)
+#pragma unroll
+    for (int i2 = 0; i2 < NS; ++i2) {
+        if (i2 <= i) {
+            float m = 0.0f;
+#pragma unroll
+            for (int g = 0; g < CM; ++g)
+                if ((s.hm[i2] >> g) & 1u) m = fmaxf(m, s.dem[g]);
+            s.dm[i2] = m;
+        }
+    }
+    s.U += N * p;
+    return true;
+}
+
+// kappa of DESIGN.md 3.3 without SAT (the sweep is not used with SAT); with
+// NO_CONTENTION the caller passes gamma = 0, and fl(1 + 0) = 1 exactly.
+__device__ __forceinline__ float sw_kappa(float dmax, float bw, float gamma, float invBW) {
+    return __fadd_rn(1.0f, __fmul_rn(gamma, __fmul_rn(__fsub_rn(dmax, bw), invBW)));
+}
+
+// cold paths of the leaf loop, out of line (instruction-cache footprint)
+__device__ __noinline__ uint32_t sw_fail_bits(const DevProb &P, int p, float bw, int minrq, int maxcnt, uint32_t need,
+                                              uint32_t minrm, float maxdem, bool cap) {
+    // first-failing dimensions of a failed deployment: OR over GPUs of fits(g, 1) failures
+    uint32_t v = 0;
+    if (p > minrq) v |= V_QUOTA;
+    if (maxcnt + 1 > P.I) v |= V_INST;
+    if (need > minrm) v |= V_MEM;
+    if (cap && __fadd_rn(maxdem, bw) > P.BW) v |= V_BW;
+    return v ? v : V_QUOTA;
+}
+
+// Largest float h with fl(dem + h) <= BW: fl(dem + y) is monotone in y, so
+// fl(dem + fl(k bw)) <= BW  <=>  fl(k bw) <= h  (exact).
+__device__ __forceinline__ float bw_threshold(float dem, float BW) {
+    float h = __fsub_rn(BW, dem);
+    while (__fadd_rn(dem, h) > BW) h = nextafterf(h, __int_as_float(0xff800000));
+    while (true) {
+        const float h2 = nextafterf(h, __int_as_float(0x7f800000));
+        if (!(__fadd_rn(dem, h2) <= BW) || h2 == h) break;
+        h = h2;
+    }
+    return __fadd_rn(h, 0.0f);   // -0 -> +0 (the sign-bit test of the sweep needs +0)
+}
+
+__device__ __forceinline__ void sw_better(unsigned long long key, unsigned long long x, unsigned long long &bk,
+                                          unsigned long long &bx) {
+    if (key < bk || (key == bk && x < bx)) {
+        bk = key;
+        bx = x;
+    }
+}
+
+// The sweep.  NS == n exactly (stage loops carry no runtime guards) unless n > 6.
+template <int CM, int NS, int POLICY, bool TWO>
+__global__ void __launch_bounds__(SWEEP_THREADS, 2) sweep_kernel(const DevProb P, const SweepArgs A) {
+    static_assert(CM <= 8, "thermometer code holds 8 GPUs x 4 bits");
+    __shared__ float dem_s[CM][SWEEP_THREADS];
+    __shared__ uint32_t qpm_s[CAMELOT_MAX_QUOTAS];   // p | ceil(2^16/p) << 7
+    __shared__ unsigned long long red_k[SWEEP_THREADS / 32], red_x[SWEEP_THREADS / 32];
+    __shared__ unsigned long long red_c[SWEEP_THREADS / 32][2];
+    __shared__ unsigned red_v[SWEEP_THREADS / 32];
+    __shared__ int is_last;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    // NS == n for n <= 6 (the host dispatches exact widths), so stage guards fold away
+    const int n = NS <= 6 ? NS : P.n;
+    const int nQ = P.nQ, O = P.O, Rmax = P.Rmax;
+    const int jl = n - 1;                     // leaf stage
+    const bool cont = !(P.flags & F_NO_CONTENTION);
+    const bool cap = !(P.flags & F_NO_BW_CAP);
+    for (int t = tid; t < nQ; t += blockDim.x) {
+        const uint32_t p = (uint32_t)P.Q[t];
+        qpm_s[t] = p | (((65536u + p - 1u) / p) << 7);
+    }
+    __syncthreads();
+    unsigned long long bk = A.inc[0].key, bx = A.inc[0].x;
+    unsigned long long n_sc = 0, n_fe = 0;
+    unsigned viol = 0;
+    while (true) {
+        unsigned long long it = 0;
+        if (lane == 0) it = atomicAdd(&A.hdr->chunk_counter, 1ull);
+        it = __shfl_sync(0xffffffffu, it, 0);
+        if (it >= A.n_items) break;
+        const unsigned long long gp = A.g_lo + it / (unsigned)A.nchunk;
+        const int ch = (int)(it % (unsigned)A.nchunk);
+        // bound: the best objective key found anywhere so far (a feasible candidate), so a
+        // leaf whose key bound is strictly worse cannot win (skips only the divisions)
+        unsigned long long gkey = 0;
+        if (lane == 0) gkey = *(volatile unsigned int *)&A.hdr->best_obj;
+        gkey = min(__shfl_sync(0xffffffffu, gkey, 0), bk);
+        // ---- grandparent (warp-uniform): batch combo + options of stages 0..n-3
+        int beta[AMAX];
+        int o[NS];
+        {
+            unsigned long long t = gp;
+#pragma unroll
+            for (int k = NS - 1; k >= 0; --k)
+                if (k < n - 2) {
+                    o[k] = (int)(t % (unsigned)O);
+                    t /= (unsigned)O;
+                }
+            int bc = (int)t;
+            for (int a = P.A - 1; a >= 0; --a) {
+                beta[a] = bc % P.nS;
+                bc /= P.nS;
+            }
+        }
+        SwState<CM, NS> st;
+        sw_init<CM, NS>(P, st);
+        bool ok = true;
+        float dur[NS], bwv[NS], ntv[NS];
+#pragma unroll
+        for (int i = 0; i < NS; ++i) {
+            dur[i] = 0.0f;
+            bwv[i] = 0.0f;
+            ntv[i] = 0.0f;
+            if (i < n - 2 && ok) {
+                const int b = beta[P.app[i]];
+                const int th = o[i] % nQ, N = o[i] / nQ + 1;
+                const float4 e = __ldg(&P.tab[((size_t)i * P.nS + b) * nQ + th]);
+                const uint32_t As = P.Am[i] * (uint32_t)P.S[b];
+                ok = sw_place<CM, NS>(P, st, i, N, (int)(qpm_s[th] & 127u), P.W[i], As, e.z);
+                dur[i] = e.x;
+                bwv[i] = e.z;
+                ntv[i] = __fmul_rn((float)N, e.y);
+            }
+        }
+        if (!ok) continue;   // the whole grandparent is infeasible (uniform)
+        // ---- parent (per lane): option of stage n-2
+        const int op = ch * 32 + lane;
+        const unsigned long long xp = gp * (unsigned long long)O + (unsigned long long)min(op, O - 1);   // parent index
+        const unsigned long long xpO = xp * (unsigned long long)O;
+        int clo = 0, chi = O;
+        if (A.lo > xpO) clo = (int)min(A.lo - xpO, (unsigned long long)O);
+        if (A.hi < xpO + O) chi = A.hi > xpO ? (int)(A.hi - xpO) : 0;
+        bool act = op < O && clo < chi;
+        if (act && A.world > 1) {
+            const unsigned long long item = xp / P.opow[n - 1 - A.d0];
+            act = ((item / 64ull) % (unsigned long long)A.world) == (unsigned long long)A.rank;
+        }
+        if (act && n >= 2) {
+            const int i = n - 2;
+            const int b = beta[P.app[i]];
+            const int th = op % nQ, N = op / nQ + 1;
+            const float4 e = __ldg(&P.tab[((size_t)i * P.nS + b) * nQ + th]);
+            const uint32_t As = P.Am[i] * (uint32_t)P.S[b];
+            act = sw_place<CM, NS>(P, st, i, N, (int)(qpm_s[th] & 127u), P.W[i], As, e.z);
+            dur[i] = e.x;
+            bwv[i] = e.z;
+            ntv[i] = __fmul_rn((float)N, e.y);
+        }
+        if (act) {
+        // ---- leaf context: capacities, deployment order, bounds (per lane)
+        const int bL = beta[P.app[jl]];
+        const uint32_t WL = P.W[jl], AsL = P.Am[jl] * (uint32_t)P.S[bL];
+        const float gL = cont ? P.gamma[jl] : 0.0f;
+        int kim[CM], sh[CM];
+        float hb[CM];      // bandwidth threshold: fits(k) <=> fl(k bw) <= hb
+        uint32_t perm = 0u, E = 0u;
+        int minrq = 0x7fffffff, maxcnt = 0;
+        uint32_t minrm = 0xffffffffu;
+        float maxdem = 0.0f;
+#pragma unroll
+        for (int g = 0; g < CM; ++g) {
+            int k = 0;
+            hb[g] = __int_as_float(0xff800000);   // -inf: nothing fits (padding GPUs)
+            if (g < P.C) {
+                k = min(Rmax, P.I - st.cnt[g]);
+                if (st.rm[g] < WL) k = 0;
+                else if (AsL > 0u) k = min(k, (int)min((uint32_t)Rmax, (st.rm[g] - WL) / AsL));
+                k = max(k, 0);
+                minrq = min(minrq, st.rq[g]);
+                maxcnt = max(maxcnt, st.cnt[g]);
+                minrm = min(minrm, st.rm[g]);
+                maxdem = fmaxf(maxdem, st.dem[g]);
+                if (st.cnt[g] == 0) E |= 1u << g;
+                hb[g] = cap ? bw_threshold(st.dem[g], P.BW) : __int_as_float(0x7f800000);
+            }
+            kim[g] = k;
+            int r = 0;
+            if (g < P.C) {
+#pragma unroll
+                for (int h = 0; h < CM; ++h)
+                    if (h < P.C && h != g) {
+                        const bool lt = st.rm[h] < st.rm[g] ||
+                                        (st.rm[h] == st.rm[g] && (st.rq[h] < st.rq[g] || (st.rq[h] == st.rq[g] && h < g)));
+                        r += lt;
+                    }
+            } else {
+                r = g;
+            }
+            sh[g] = 4 * r;
+            perm |= (uint32_t)g << (4 * r);
+            dem_s[g][tid] = st.dem[g];
+        }
+        float ptub = __int_as_float(0x7f800000);
+#pragma unroll
+        for (int i = 0; i < NS; ++i)
+            if (i < jl) {
+                const float k = sw_kappa(st.dm[i], bwv[i], cont ? P.gamma[i] : 0.0f, P.invBW);
+                ptub = fminf(ptub, k == 1.0f ? ntv[i] : __fdiv_rn(ntv[i], k));
+            }
+        const float4 *tabL = P.tab + ((size_t)jl * P.nS + bL) * nQ;
+        const float qos0 = P.qos[0], qos1 = TWO ? P.qos[1] : 0.0f;
+        const int f1 = TWO ? P.first_of_app[1] : n;   // first stage of application 2
+        float gam[NS];
+#pragma unroll
+        for (int i = 0; i < NS; ++i) gam[i] = (cont && i < n) ? P.gamma[i] : 0.0f;
+        int ybud = 0x7fffffff;
+        float lam0 = 0.0f, lam1 = 0.0f;
+        if (POLICY == 1) {
+            lam0 = A.lam[0];
+            lam1 = TWO ? A.lam[1] : 0.0f;
+            if (P.flags & F_EQ2_BUDGET) {
+                int bc = 0;
+                for (int a = 0; a < P.A; ++a) bc = bc * P.nS + beta[a];
+                ybud = A.y[bc * A.ystride + A.yoff];
+            }
+        }
+        const unsigned span = (unsigned)(chi - clo);
+        const bool full = span == (unsigned)O;
+        unsigned c_sc = 0, c_fe = 0;
+        // ---- the leaves: quota theta outer (capacities once), replicas N inner.
+        // Kept compact (rolled N loop, no per-GPU branches): the hot loop must stay
+        // within the ~6 KB L0 instruction cache.
+        for (int th = 0; th < nQ; ++th) {
+            const float4 e = __ldg(&tabL[th]);
+            const uint32_t qp = qpm_s[th];
+            const uint32_t pmul = qp >> 7;
+            const float bw = e.z;
+            // fl(k bw) for k = 1..4 (the bandwidth fit test)
+            const float nb2 = __fmul_rn(2.0f, bw), nb3 = __fmul_rn(3.0f, bw), nb4 = __fmul_rn(4.0f, bw);
+            uint32_t M = 0u;   // thermometer code of c_g = canHold(g, Rmax), 4 bits per GPU in deployment order
+#pragma unroll
+            for (int g = 0; g < CM; ++g) {
+                // fl(k bw) <= h  <=>  fl(h - fl(k bw)) has a clear sign bit (exact: RN keeps
+                // the sign and gradual underflow never rounds a non-zero difference to 0)
+                const float h = hb[g];
+                const uint32_t nf = (__float_as_uint(__fsub_rn(h, bw)) >> 31) + (__float_as_uint(__fsub_rn(h, nb2)) >> 31) +
+                                    (__float_as_uint(__fsub_rn(h, nb3)) >> 31) + (__float_as_uint(__fsub_rn(h, nb4)) >> 31);
+                const int c = min(min(kim[g], (int)(((uint32_t)st.rq[g] * pmul) >> 16)), 4 - (int)nf);
+                M |= (0xFu >> (4 - c)) << sh[g];
+            }
+            // deployment succeeds iff the total capacity holds N (pass 1 or pass 2)
+            const int sumc = __popc(M);
+            const int nok = min(sumc, Rmax);
+            if (full) {
+                c_sc += Rmax;
+            } else {
+                for (int N = 1; N <= Rmax; ++N) c_sc += (unsigned)((N - 1) * nQ + th - clo) < span;
+            }
+            if (nok < Rmax) {   // the failing leaves: first-failing dimensions (OR over GPUs, k = 1)
+                bool any = full;
+                for (int N = nok + 1; N <= Rmax && !any; ++N) any = (unsigned)((N - 1) * nQ + th - clo) < span;
+                if (any) viol |= sw_fail_bits(P, (int)(qp & 127u), bw, minrq, maxcnt, WL + AsL, minrm, maxdem, cap);
+            }
+#pragma unroll 1
+            for (int N = 1; N <= nok; ++N) {
+                const int code = (N - 1) * nQ + th;
+                if ((unsigned)(code - clo) >= span) continue;
+                // receiving GPUs in deployment order: pass 1 = the first with c >= N (k = N);
+                // pass 2 = greedy k = min(c, remaining) over those with c >= 1
+                const uint32_t mN = (M >> (N - 1)) & 0x11111111u;
+                float dmx[NS];
+#pragma unroll
+                for (int i = 0; i < NS; ++i) dmx[i] = st.dm[i];
+                float dl = 0.0f;
+                int du = 0;
+                uint32_t mm = mN ? (mN & (0u - mN)) : (M & 0x11111111u);
+                int rem = N;
+                do {
+                    const int r = __ffs(mm) - 1;
+                    mm &= mm - 1u;
+                    const int k = min(rem, __popc((M >> r) & 15u));
+                    rem -= k;
+                    const int g = (perm >> r) & 15u;
+                    const float d = __fadd_rn(dem_s[g][tid], __fmul_rn((float)k, bw));
+                    dl = fmaxf(dl, d);
+                    du += (E >> g) & 1u;
+#pragma unroll
+                    for (int i = 0; i < NS; ++i)
+                        if (i < jl && ((st.hm[i] >> g) & 1u)) dmx[i] = fmaxf(dmx[i], d);
+                } while (rem > 0);
+                // contention-aware latencies and the per-application ordered sums (Constraint-5)
+                float kap[NS];
+                float l0 = 0.0f, l1 = 0.0f;
+#pragma unroll
+                for (int i = 0; i < NS; ++i) {
+                    if (i < n) {
+                        const float k = (i == jl) ? sw_kappa(dl, bw, gL, P.invBW)
+                                                  : sw_kappa(dmx[i], bwv[i], gam[i], P.invBW);
+                        kap[i] = k;
+                        const float L = __fmul_rn(i == jl ? e.x : dur[i], k);
+                        if (!TWO || i < f1) l0 = (i == 0) ? L : __fadd_rn(l0, L);
+                        else l1 = (i == f1) ? L : __fadd_rn(l1, L);
+                    }
+                }
+                if (!(l0 <= qos0 && (!TWO || l1 <= qos1))) {
+                    viol |= V_QOS;
+                    continue;
+                }
+                ++c_fe;
+                const unsigned long long x = xpO + (unsigned long long)code;
+                const float ntl = __fmul_rn((float)N, e.y);
+                if (POLICY == 0) {
+                    // T <= min(parent bound, fl(N thr)): the divisions only when it can win
+                    const unsigned long long kub = objkey_maxload(fminf(ptub, ntl));
+                    if (kub <= gkey && (kub < bk || (kub == bk && x < bx))) {
+                        float T = __int_as_float(0x7f800000);
+#pragma unroll
+                        for (int i = 0; i < NS; ++i)
+                            if (i < n) {
+                                const float nt = i == jl ? ntl : ntv[i];
+                                T = fminf(T, kap[i] == 1.0f ? nt : __fdiv_rn(nt, kap[i]));
+                            }
+                        sw_better(objkey_maxload(T), x, bk, bx);
+                    }
+                } else {
+                    const int u2 = st.u + du;
+                    const unsigned long long key = objkey_minres(u2, st.U + N * (int)(qp & 127u));
+                    if (key <= gkey && (key < bk || (key == bk && x < bx)) && u2 <= ybud) {
+                        float t0 = __int_as_float(0x7f800000), t1 = __int_as_float(0x7f800000);
+#pragma unroll
+                        for (int i = 0; i < NS; ++i)
+                            if (i < n) {
+                                const float nt = i == jl ? ntl : ntv[i];
+                                const float ti = kap[i] == 1.0f ? nt : __fdiv_rn(nt, kap[i]);
+                                if (!TWO || i < f1) t0 = fminf(t0, ti);
+                                else t1 = fminf(t1, ti);
+                            }
+                        if (t0 >= lam0 && (!TWO || t1 >= lam1)) sw_better(key, x, bk, bx);
+                    }
+                }
+            }
+        }
+        n_sc += c_sc;
+        n_fe += c_fe;
+        if (bk < gkey) atomicMin(&A.hdr->best_obj, (unsigned int)bk);
+        }   // act
+    }
+    // ---- reduction: lane -> warp -> CTA slot; the last CTA reduces the slots
+    for (int off = 16; off; off >>= 1) {
+        const unsigned long long ok2 = __shfl_xor_sync(0xffffffffu, bk, off);
+        const unsigned long long ox = __shfl_xor_sync(0xffffffffu, bx, off);
+        sw_better(ok2, ox, bk, bx);
+        n_sc += __shfl_xor_sync(0xffffffffu, n_sc, off);
+        n_fe += __shfl_xor_sync(0xffffffffu, n_fe, off);
+        viol |= __shfl_xor_sync(0xffffffffu, viol, off);
+    }
+    if (lane == 0) {
+        red_k[wid] = bk;
+        red_x[wid] = bx;
+        red_c[wid][0] = n_sc;
+        red_c[wid][1] = n_fe;
+        red_v[wid] = viol;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        unsigned long long k2 = red_k[0], x2 = red_x[0], sc = 0, fe = 0;
+        unsigned vi = 0;
+        for (int w = 0; w < SWEEP_THREADS / 32; ++w) {
+            sw_better(red_k[w], red_x[w], k2, x2);
+            sc += red_c[w][0];
+            fe += red_c[w][1];
+            vi |= red_v[w];
+        }
+        A.slots[blockIdx.x].key = k2;
+        A.slots[blockIdx.x].x = x2;
+        if (sc) {
+            atomicAdd(&A.hdr->n_scored, sc);
+            atomicAdd(&A.hdr->cum_scored, sc);
+        }
+        if (fe) atomicAdd(&A.hdr->n_feasible, fe);
+        if (vi) atomicOr(&A.hdr->viol_or, vi);
+        __threadfence();
+        is_last = atomicAdd(&A.hdr->done_ctas, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    unsigned long long k2 = ~0ull, x2 = ~0ull;
+    for (int s = tid; s < (int)gridDim.x; s += blockDim.x) {
+        const unsigned long long vk = *(volatile unsigned long long *)&A.slots[s].key;
+        const unsigned long long vx = *(volatile unsigned long long *)&A.slots[s].x;
+        sw_better(vk, vx, k2, x2);
+    }
+    for (int off = 16; off; off >>= 1) {
+        const unsigned long long ok2 = __shfl_xor_sync(0xffffffffu, k2, off);
+        const unsigned long long ox = __shfl_xor_sync(0xffffffffu, x2, off);
+        sw_better(ok2, ox, k2, x2);
+    }
+    if (lane == 0) {
+        red_k[wid] = k2;
+        red_x[wid] = x2;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        for (int w = 1; w < SWEEP_THREADS / 32; ++w) sw_better(red_k[w], red_x[w], k2, x2);
+        if (k2 >= 0xFFFFFFFFull) {
+            k2 = 0xFFFFFFFFull;
+            x2 = ~0ull;
+        }
+        A.result[0].key = k2;
+        A.result[0].x = x2;
+        unsigned long long packed = ~0ull;
+        if (k2 != 0xFFFFFFFFull) {
+            // chunk id = 64 depth-d0 items (NO_FILTER: item = x / O^(n-d0)), as the tree search
+            const unsigned long long low = P.ntot <= (1ull << 32) ? x2 : (x2 / P.opow[n - A.d0]) / 64ull;
+            packed = (k2 << 32) | (low & 0xFFFFFFFFull);
+        }
+        A.keys[0] = (long long)(packed ^ 0x8000000000000000ull);
+        A.hdr->done_ctas = 0;
+    }
+}
+
+}  // namespace cam

@@ -1,0 +1,25 @@
+// camelot_sweep_args.h -- launch arguments of the exhaustive leaf-sweep kernel
+// (camelot_sweep.cuh); shared with the host launcher in camelot_api.cu.
+#pragma once
+#include "camelot_device.cuh"
+
+namespace cam {
+
+struct SweepArgs {
+    int policy;                       // 0 max-load, 1 min-resource (one load level)
+    int rank, world, d0;              // chunk ownership: chunk = (x / O^(n-d0)) / 64
+    unsigned long long lo, hi;        // canonical index range [lo, hi)
+    unsigned long long g_lo;          // first grandparent
+    unsigned long long n_items;       // grandparents x nchunk
+    int nchunk;                       // ceil(O / 32) parent chunks per grandparent
+    const float *lam;                 // [A] load level (min-resource)
+    const int *y;                     // Eq. 2 estimates [nbc][ystride] at + yoff
+    int ystride, yoff;
+    const Slot *inc;                  // incumbent (key, x) (none: key 0xFFFFFFFF)
+    Slot *slots;                      // [gridDim.x]
+    DevHeader *hdr;
+    Slot *result;                     // exact local best
+    long long *keys;                  // packed key (NCCL transport)
+};
+
+}  // namespace cam

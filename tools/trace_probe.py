@@ -1,0 +1,45 @@
+"""Phase trace of the C4 plan calls (development aid): per search-level launch,
+the time between grid barriers.   python tools/trace_probe.py [config] [reps]"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from gen import problems as G  # noqa: E402
+from paper_2005_02088_b200 import api  # noqa: E402
+
+NAMES = {0: "start", 1: "reset", 2: "filter", 3: "offsets", 32: "cta-red", 4: "f.stage", 5: "f.static", 6: "f.min", 7: "f.round", 8: "f.compact"}
+
+
+def show(tag, tr, st):
+    print(f"== {tag}: kernel {st['t_ns']/1e3:.1f} us, leaves {st['cum_scored']}, nodes {st['cum_nodes']}")
+    line, prev = [], None
+    t0s = [0]
+    for t, ns in tr:
+        if t == 0:
+            if line:
+                print("   " + " ".join(line))
+            line = []
+            if prev is not None:
+                line.append(f"[gap {(ns - prev)/1e3:.1f}]")
+        elif t >= 64:
+            line.append(f"{['par', 'bat', 'maxb'][(t - 64) // 16]}{t % 16}={ns}")
+            continue
+        else:
+            line.append(f"{NAMES.get(t, 'p%d' % (t - 16))}={(ns - prev)/1e3:.1f}")
+        prev = ns
+    if line:
+        print("   " + " ".join(line))
+
+
+cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+p = G.config_problems(cfg)[0]
+s = api.Session(p, n_loads=1)
+for rep in range(reps):
+    r = s.plan_max_load()
+    show(f"max-load rep {rep}", s.trace(), s.last_stats())
+    m = s.plan_min_resource([[0.3 * r.objective] * p.n_apps])[0]
+    show(f"min-res rep {rep}", s.trace(), s.last_stats())
+torch.cuda.synchronize()
