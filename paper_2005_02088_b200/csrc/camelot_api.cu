@@ -521,7 +521,7 @@ int run_passes(const Ctx &X, int dev, int policy, SearchArgs S, bool timed, bool
 // exhaustive scan (NO_FILTER) through the leaf-sweep kernel: the option lists are
 // still built (full, unfiltered) for a possible chunk re-scan by the tree search
 int sweep_pass(const Ctx &X, int dev, int policy, int nlev, const Slot *inc, Slot *result, long long *keys,
-               int rank, int world, unsigned long long lo, unsigned long long hi) {
+               int rank, int world, unsigned long long lo, unsigned long long hi, int qstride = 1) {
     char *ws = X.ws;
     DevHeader *hdr = reinterpret_cast<DevHeader *>(ws + X.L.hdr);
     CU(cudaMemsetAsync(hdr, 0, offsetof(DevHeader, cum_scored), X.st));
@@ -539,9 +539,11 @@ int sweep_pass(const Ctx &X, int dev, int policy, int nlev, const Slot *inc, Slo
     F.item_off = reinterpret_cast<unsigned long long *>(ws + X.L.item_off);
     F.hdr = hdr;
     F.d0 = X.d0;
-    filter_kernel<<<X.d.nS, FILTER_THREADS, 0, X.st>>>(X.P, F);
-    COUNT_LAUNCH();
-    CU(cudaGetLastError());
+    if (qstride == 1 && world > 1) {   // full option lists + item offsets for a chunk re-scan (finalize)
+        filter_kernel<<<X.d.nS, FILTER_THREADS, 0, X.st>>>(X.P, F);
+        COUNT_LAUNCH();
+        CU(cudaGetLastError());
+    }
     SweepArgs A;
     memset(&A, 0, sizeof(A));
     A.policy = policy;
@@ -550,11 +552,22 @@ int sweep_pass(const Ctx &X, int dev, int policy, int nlev, const Slot *inc, Slo
     A.d0 = X.d0;
     A.lo = lo;
     A.hi = hi;
-    const unsigned long long O2 = (unsigned long long)X.d.O * (unsigned long long)X.d.O;
-    A.nchunk = (X.d.O + 31) / 32;
-    if (hi > lo) {
-        A.g_lo = lo / O2;
-        A.n_items = ((hi - 1) / O2 + 1 - A.g_lo) * (unsigned long long)A.nchunk;
+    A.qstride = qstride;
+    A.nQs = (X.d.nQ - 1) / qstride + 1;
+    if (qstride == 1) {
+        const unsigned long long O2 = (unsigned long long)X.d.O * (unsigned long long)X.d.O;
+        A.nchunk = (X.d.O + 31) / 32;
+        if (hi > lo) {
+            A.g_lo = lo / O2;
+            A.n_items = ((hi - 1) / O2 + 1 - A.g_lo) * (unsigned long long)A.nchunk;
+        }
+    } else {   // sub-grid (incumbent cascade): the whole sub-space, world 1
+        const unsigned long long Os = (unsigned long long)X.d.Rmax * A.nQs;
+        A.nchunk = (int)((Os + 31) / 32);
+        unsigned long long ngp = (unsigned long long)X.d.nbc;
+        for (int i = 0; i < X.d.n - 2; ++i) ngp *= Os;
+        A.g_lo = 0;
+        A.n_items = ngp * (unsigned long long)A.nchunk;
     }
     A.lam = reinterpret_cast<const float *>(ws + X.L.lam);
     A.y = reinterpret_cast<const int *>(ws + X.L.y);
@@ -623,6 +636,7 @@ int search_pass(const Ctx &X, int dev, int policy, int nlev, bool prune, int str
     S.sb = F.sb;
     S.item_off = reinterpret_cast<const unsigned long long *>(ws + X.L.item_off);
     S.lam = F.lam;
+    S.lam_stride = X.d.A;
     S.y = reinterpret_cast<const int *>(ws + X.L.y);
     S.ystride = nlev;
     S.yoff = 0;
@@ -672,6 +686,7 @@ int rescan_pass(const Ctx &X, int dev, int policy, int nlev, bool prune, int k, 
     S.sb = reinterpret_cast<const StageBound *>(ws + X.L.sb);
     S.item_off = reinterpret_cast<const unsigned long long *>(ws + X.L.item_off);
     S.lam = reinterpret_cast<const float *>(ws + X.L.lam) + k * X.d.A;
+    S.lam_stride = X.d.A;
     S.y = reinterpret_cast<const int *>(ws + X.L.y);
     S.ystride = nlev;
     S.yoff = k;
@@ -760,8 +775,30 @@ int local_search(const Ctx &X, const camelot_exec *ex, int policy, int nlev, lon
     CU(cudaEventRecord(t_ev.a, X.st));
     if (use_coarse(X, prune)) {
         // incumbent: exact optimum of coarse quota sub-grids, coarsest first (each
-        // pass seeds the next); replicated on every rank
-        for (int stride : coarse_strides(X)) {
+        // pass seeds the next); replicated on every rank.  The coarse levels small
+        // enough for an exhaustive scan are replaced by ONE leaf sweep of the finest
+        // of them (its optimum is at least as good as any coarser level's).
+        std::vector<int> strides = coarse_strides(X);
+        if (sweep_supported(X.P, policy, nlev) && lo == 0 && hi == X.d.ntot && !getenv("CAMELOT_NO_SWEEP")) {
+            int flat_s = 0;
+            for (int s2 : strides) {
+                long double sub = (long double)X.d.nbc;
+                for (int i = 0; i < X.d.n; ++i) sub *= (long double)X.d.Rmax * ((X.d.nQ - 1) / s2 + 1);
+                // measured (C4): a sub-grid of <= 2^20 candidates sweeps faster than a pruned
+                // level; larger ones lose to the pruned search (per-parent setup dominates)
+                if (sub <= (long double)(1ull << 20)) flat_s = s2;   // strides are descending
+            }
+            if (flat_s) {
+                rc = sweep_pass(X, dev, policy, nlev, inc, inc, reinterpret_cast<long long *>(ws + X.L.keys), 0, 1, lo,
+                                hi, flat_s);
+                if (rc) return rc;
+                std::vector<int> rest;
+                for (int s2 : strides)
+                    if (s2 < flat_s) rest.push_back(s2);
+                strides.swap(rest);
+            }
+        }
+        for (int stride : strides) {
             rc = search_pass(X, dev, policy, nlev, true, stride, inc, result,
                              reinterpret_cast<long long *>(ws + X.L.keys), 0, 1, lo, hi, false, inc);
             if (rc) return rc;

@@ -611,8 +611,18 @@ search_level_kernel(const DevProb P, const LevelArgs LA) {
         S.head = &hdr->head[j];
         S.grab = 1;
         pass_body<CM, NS, POLICY>(P, S, stack, ctl, wb, lane, cn);
+#ifdef CAMELOT_FTRACE
+        if (lane == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            atomicMax(&hdr->dbg_tend[j], t);
+        }
+#endif
         grid.sync();
         if (tr) {
+#ifdef CAMELOT_FTRACE
+            trace_value(hdr, 48 + j, hdr->dbg_tend[j]);
+#endif
             trace_mark(hdr, 16 + j);
 #ifdef CAMELOT_FTRACE
             trace_value(hdr, 64 + j, j == 0 ? (unsigned long long)P.nbc : hdr->tail[j]);   // parents of pass j

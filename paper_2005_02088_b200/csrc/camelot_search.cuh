@@ -22,6 +22,7 @@
 #pragma once
 #include "camelot_device.cuh"
 #include "camelot_score.cuh"
+#include <cstddef>
 
 namespace cam {
 
@@ -43,6 +44,7 @@ struct SearchArgs {
     const StageBound *sb;       // [n][nS]
     const unsigned long long *item_off;  // [nbc + 1]
     const float *lam;           // [nlev][A] load levels (min-resource)
+    int lam_stride;             // A (row stride of lam)
     const int *y;               // [nbc][ystride] Eq. 2 estimates (min-resource), level k at yoff + k
     int ystride, yoff;
     const Slot *inc;            // [nlev] incumbent (key, x); key 0xFFFFFFFF.. = none
@@ -84,6 +86,20 @@ struct Node {
     int b[AMAX];
     float tub;              // min fl(N thr) over placed stages
 };
+
+// The global frontier is a structure of arrays: 32-bit word w of node k lives at
+// base[w * cap + k], so the lanes of a warp that emit consecutive slots write
+// every field with one coalesced store (an array-of-structs frontier costs one
+// memory transaction per lane and field).
+template <int CM>
+struct Frontier {
+    uint32_t *base;
+    unsigned long long cap;
+    static constexpr int WORDS = (int)(sizeof(Node<CM>) / 4);
+    __device__ __forceinline__ void put(int w, unsigned long long k, uint32_t v) const { base[(size_t)w * cap + k] = v; }
+    __device__ __forceinline__ void putf(int w, unsigned long long k, float v) const { put(w, k, __float_as_uint(v)); }
+};
+#define NODE_W(CM, field) ((int)(offsetof(Node<CM>, field) / 4))
 
 // per-warp DFS bookkeeping (shared memory)
 struct WarpCtl {
@@ -298,6 +314,7 @@ struct WarpBest {
     unsigned long long x[LMAX];
     unsigned long long bound;       // pruning bound: max over levels of key (conservative)
     unsigned long long gpack;       // device-wide (key << 32 | x >> xshift) best (1 level)
+    float lmin;                     // min-resource, one application: the smallest load level
 };
 
 // Can a subtree whose keys are >= kl and whose indices are >= xs still hold
@@ -679,11 +696,10 @@ __device__ __forceinline__ bool owns(const DevProb &P, const SearchArgs &S, cons
 }
 
 template <int CM>
-__device__ __forceinline__ void copy_node(Node<CM> &dst, const Node<CM> &src, int lane) {
+__device__ __forceinline__ void copy_node(Node<CM> &dst, const Frontier<CM> &F, unsigned long long k, int lane) {
     static_assert(sizeof(Node<CM>) % 4 == 0, "node size");
-    const uint32_t *s = reinterpret_cast<const uint32_t *>(&src);
     uint32_t *d = reinterpret_cast<uint32_t *>(&dst);
-    for (int w = lane; w < (int)(sizeof(Node<CM>) / 4); w += 32) d[w] = s[w];
+    for (int w = lane; w < Frontier<CM>::WORDS; w += 32) d[w] = __ldcg(F.base + (size_t)w * F.cap + k);
     __syncwarp();
 }
 
@@ -707,7 +723,9 @@ __device__ __forceinline__ bool owns_child(const DevProb &P, const SearchArgs &S
 template <int CM, int NS>
 __device__ __forceinline__ void emit_child(const DevProb &P, const Node<CM> &nd, const PCtx<CM, NS> &c, int j,
                                            const OptRec &r, uint32_t p, uint32_t W, uint32_t As, int kopt,
-                                           Node<CM> *out) {
+                                           const Frontier<CM> &F, unsigned long long k) {
+#define OUT_PUT(field, idx, v) F.put(NODE_W(CM, field) + (idx), k, (uint32_t)(v))
+#define OUT_PUTF(field, idx, v) F.putf(NODE_W(CM, field) + (idx), k, (v))
     int kk[CM];
     fast_place<CM, NS>(P, c, r, kk);
     int rq[CM], cnt[CM], g[CM];
@@ -761,12 +779,12 @@ __device__ __forceinline__ void emit_child(const DevProb &P, const Node<CM> &nd,
                 else if (As2 > 0) km = (int)min((uint32_t)P.Rmax, (rm[q] - W2) / As2);
                 kim = max(0, min(km, min(P.Rmax, P.I - cnt[q])));
             }
-            out->prq[rank] = rq[q];
-            out->pcnt[rank] = cnt[q];
-            out->prm[rank] = rm[q];
-            out->pkim[rank] = kim;
-            out->pgid[rank] = g[q];
-            out->pdem[rank] = dem[q];
+            OUT_PUT(prq, rank, rq[q]);
+            OUT_PUT(pcnt, rank, cnt[q]);
+            OUT_PUT(prm, rank, rm[q]);
+            OUT_PUT(pkim, rank, kim);
+            OUT_PUT(pgid, rank, g[q]);
+            OUT_PUTF(pdem, rank, dem[q]);
         }
     }
 #pragma unroll
@@ -777,29 +795,33 @@ __device__ __forceinline__ void emit_child(const DevProb &P, const Node<CM> &nd,
 #pragma unroll
             for (int q = 0; q < CM; ++q)
                 if (q < P.C && kk[q] > 0 && ((hmi >> g[q]) & 1u)) dm = fmaxf(dm, dem[q]);
-            out->dur[i] = nd.dur[i];
-            out->bw[i] = nd.bw[i];
-            out->nt[i] = nd.nt[i];
-            out->dmax[i] = dm;
-            out->hmask[i] = hmi;
-            out->kidx[i] = nd.kidx[i];
+            OUT_PUTF(dur, i, nd.dur[i]);
+            OUT_PUTF(bw, i, nd.bw[i]);
+            OUT_PUTF(nt, i, nd.nt[i]);
+            OUT_PUTF(dmax, i, dm);
+            OUT_PUT(hmask, i, hmi);
+            OUT_PUT(kidx, i, nd.kidx[i]);
         } else if (i == j) {
-            out->dur[i] = r.dur;
-            out->bw[i] = r.bw;
-            out->nt[i] = r.NT;
-            out->dmax[i] = dself;
-            out->hmask[i] = hm;
-            out->kidx[i] = kopt;
+            OUT_PUTF(dur, i, r.dur);
+            OUT_PUTF(bw, i, r.bw);
+            OUT_PUTF(nt, i, r.NT);
+            OUT_PUTF(dmax, i, dself);
+            OUT_PUT(hmask, i, hm);
+            OUT_PUT(kidx, i, kopt);
         }
     }
-    out->x = nd.x * (unsigned long long)P.O + r.code;
-    out->U = nd.U + (int)r.NP;
-    out->u = nd.u + unew;
-    out->rqsum = nd.rqsum - (int)r.NP;
-    out->bc = nd.bc;
-    out->b[0] = nd.b[0];
-    out->b[AMAX - 1] = nd.b[AMAX - 1];
-    out->tub = fminf(nd.tub, r.NT);
+    {
+        const unsigned long long xv = nd.x * (unsigned long long)P.O + r.code;
+        OUT_PUT(x, 0, (uint32_t)xv);
+        OUT_PUT(x, 1, (uint32_t)(xv >> 32));
+    }
+    OUT_PUT(U, 0, nd.U + (int)r.NP);
+    OUT_PUT(u, 0, nd.u + unew);
+    OUT_PUT(rqsum, 0, nd.rqsum - (int)r.NP);
+    OUT_PUT(bc, 0, nd.bc);
+    OUT_PUT(b, 0, nd.b[0]);
+    OUT_PUT(b, AMAX - 1, nd.b[AMAX - 1]);
+    OUT_PUTF(tub, 0, fminf(nd.tub, r.NT));
 }
 
 // the same item offsets, but an "empty" batch combo still has a well-defined
@@ -911,6 +933,14 @@ __device__ __forceinline__ void init_warp_best(const SearchArgs &S, WarpBest *wb
         wb->gpack = *(volatile unsigned long long *)&S.hdr->best_packed;
         if (nlev == 1 && wb->key[0] < 0xFFFFFFFFull)
             wb->gpack = min(wb->gpack, (wb->key[0] << 32) | min(wb->x[0] >> S.xshift, 0xFFFFFFFFull));
+        // load floor with contention (min-resource, A = 1): every completion of a node
+        // whose placed stages already throttle below the SMALLEST level fails LOAD
+        float lm = 0.0f;
+        if (S.policy == 1 && S.lam) {
+            lm = __int_as_float(0x7f800000);
+            for (int k = 0; k < nlev; ++k) lm = fminf(lm, S.lam[k * S.lam_stride]);
+        }
+        wb->lmin = lm;
     }
     __syncwarp();
 }
@@ -923,9 +953,10 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
     const int nlev = S.nlev;
     const int n = P.n;
     const int jtop = S.level;
-    const Node<CM> *in = reinterpret_cast<const Node<CM> *>(S.in_nodes);
-    Node<CM> *outf = reinterpret_cast<Node<CM> *>(S.out_nodes);
-    const unsigned long long count = in ? min(*(volatile const unsigned long long *)S.in_count, S.in_cap)
+    const bool have_in = S.in_nodes != nullptr;
+    const Frontier<CM> in{const_cast<uint32_t *>(reinterpret_cast<const uint32_t *>(S.in_nodes)), S.in_cap};
+    const Frontier<CM> outf{reinterpret_cast<uint32_t *>(S.out_nodes), S.out_cap};
+    const unsigned long long count = have_in ? min(*(volatile const unsigned long long *)S.in_count, S.in_cap)
                                         : (unsigned long long)P.nbc;
     // few parents (shallow passes): each block of 32 children is its own work item;
     // the blocks per parent follow the largest surviving option count of stage jtop
@@ -937,11 +968,36 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
 
 #ifdef CAMELOT_FTRACE
     unsigned long long dbg_nb = 0;
+    unsigned long long dbg_t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int dbg_item = 0;
+    const bool dbg_me = blockIdx.x == 0 && threadIdx.x == 0;
+#define PTM(k) \
+    if (dbg_me && dbg_item == 1 && dbg_t[k] == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(dbg_t[k]));
+#else
+#define PTM(k)
 #endif
+    PTM(0);
+    // the first item of every warp is assigned statically (no atomic queueing at the
+    // start of a pass: with few items the pass is latency bound); the rest is dynamic
+    // Heavy passes (many parents, one block of children each): a warp takes 32
+    // parents at a time and screens them lane-parallel against the current bound
+    // from a few coalesced frontier words before copying any survivor.
+    const unsigned long long nwarps = (unsigned long long)gridDim.x * SEARCH_WARPS;
+    const bool screen = S.prune && have_in && split == 1 && count >= 16ull * nwarps;
+    const unsigned grab = screen ? 8u : (unsigned)S.grab;
+    const unsigned long long nw = nwarps * grab;
+    unsigned long long e0 = ((unsigned long long)blockIdx.x * SEARCH_WARPS + (threadIdx.x >> 5)) * grab;
+    bool first = true;
     while (true) {
-        unsigned long long e0 = 0;
-        if (lane == 0) e0 = atomicAdd(S.head, (unsigned long long)S.grab);
-        e0 = __shfl_sync(0xffffffffu, e0, 0);
+        if (!first) {
+            if (lane == 0) e0 = nw + atomicAdd(S.head, (unsigned long long)grab);
+            e0 = __shfl_sync(0xffffffffu, e0, 0);
+        }
+        first = false;
+#ifdef CAMELOT_FTRACE
+        ++dbg_item;
+#endif
+        PTM(1);
         if (e0 >= items) break;
         if (lane == 0) {   // refresh the pruning bounds from the device-wide best
             const unsigned long long g = (unsigned long long)(*(volatile unsigned int *)&S.hdr->best_obj);
@@ -950,17 +1006,59 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
             if (gp < wb->gpack) wb->gpack = gp;
         }
         __syncwarp();
-        const unsigned long long e1 = min(e0 + (unsigned long long)S.grab, items);
+        const unsigned long long e1 = min(e0 + (unsigned long long)grab, items);
+        unsigned live = 0xffffffffu;
+        if (screen) {
+            const unsigned long long ei = e0 + lane;
+            bool lv = ei < e1;
+            if (lv) {
+                auto word = [&](int w) { return __ldcg(in.base + (size_t)w * in.cap + ei); };
+                const int Uq = (int)word(NODE_W(CM, U)), uq = (int)word(NODE_W(CM, u));
+                const float tq = __uint_as_float(word(NODE_W(CM, tub)));
+                const unsigned long long xq = (unsigned long long)word(NODE_W(CM, x)) |
+                                              ((unsigned long long)word(NODE_W(CM, x) + 1) << 32);
+                int bq[AMAX];
+                bq[0] = (int)word(NODE_W(CM, b));
+                bq[AMAX - 1] = (int)word(NODE_W(CM, b) + AMAX - 1);
+                float rT = __int_as_float(0x7f800000);
+                int rU = 0;
+                for (int i2 = jtop + 1; i2 < n; ++i2) {
+                    const StageBound &bb = sb_at(P, S, i2, bq[P.app[i2]]);
+                    rT = fminf(rT, bb.maxNT);
+                    rU += (int)bb.minNP;
+                }
+                const StageBound &bj = sb_at(P, S, jtop, bq[P.app[jtop]]);
+                unsigned long long kl;
+                if (POLICY == 0) kl = objkey_maxload(fminf(tq, fminf(bj.maxNT, rT)));
+                else {
+                    const int Ulb = Uq + (int)bj.minNP + rU;
+                    kl = objkey_minres(max(uq, (Ulb + P.R - 1) / P.R), Ulb);
+                }
+                lv = can_win(kl, xq * P.opow[n - jtop], wb, nlev, S.xshift);
+            }
+            live = __ballot_sync(0xffffffffu, lv);
+        }
         for (unsigned long long it = e0; it < e1; ++it) {
+            if (!((live >> (unsigned)(it - e0)) & 1u)) continue;
+            if (screen && it > e0) {   // refresh the bounds per parent
+                if (lane == 0) {
+                    const unsigned long long g = (unsigned long long)(*(volatile unsigned int *)&S.hdr->best_obj);
+                    if (g < wb->bound) wb->bound = g;
+                    const unsigned long long gp = *(volatile unsigned long long *)&S.hdr->best_packed;
+                    if (gp < wb->gpack) wb->gpack = gp;
+                }
+                __syncwarp();
+            }
             const unsigned long long e = it / (unsigned)split;
             const int blk = (int)(it % (unsigned)split);
-            if (!in) {
+            if (!have_in) {
                 build_root<CM>(P, (int)e, stack[0], lane);
                 if (lane < NMAX) stack[0].kidx[lane] = 0;
                 __syncwarp();
             } else {
-                copy_node<CM>(stack[jtop], in[e], lane);
+                copy_node<CM>(stack[jtop], in, e, lane);
             }
+            PTM(2);
             {
                 const int cnt0 = (int)sb_at(P, S, jtop, stack[jtop].b[P.app[jtop]]).cnt;
                 __syncwarp();
@@ -983,6 +1081,7 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
                 if (reload) {
                     reload = false;
                     load_ctx<CM, NS>(P, S, nd, j, c);
+                    PTM(3);
                     // re-check the node against the current bound (it may have tightened)
                     if (S.prune) {
                         unsigned long long kl;
@@ -991,7 +1090,10 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
                             const int Ulb = c.U + (int)sb_at(P, S, j, bj).minNP + c.restU;
                             kl = objkey_minres(max(c.u, (Ulb + P.R - 1) / P.R), Ulb);
                         }
-                        if (!can_win(kl, c.x * P.opow[n - j], wb, nlev, S.xshift)) {
+                        bool live = can_win(kl, c.x * P.opow[n - j], wb, nlev, S.xshift);
+                        // T_i <= fl(N_i thr_i / kappa_i(now)) (kappa only grows): below the load floor -> dead
+                        if (POLICY == 1 && P.A == 1 && c.tub < wb->lmin) live = false;
+                        if (!live) {
                             __syncwarp();
                             if (lane == 0) {
                                 ctl->cur[j] = ctl->end[j];
@@ -1088,6 +1190,7 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
                 FastEval fe;
                 fe.placed = false;
                 if (go) fast_eval<CM, NS>(P, c, j, r, fe);
+                PTM(4);
                 if (leaf) {
                     // violation diagnostics are exact (and computed) only in flat mode
                     if (!S.prune && go && !fe.placed) cn.viol |= place_fail_bits<CM>(P, nd, list[opt]);
@@ -1109,6 +1212,11 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
                         auto ntf2 = [&](int i) { return i < jj ? c.nt[i] : r.NT; };
                         if (t_certainly_below<NS>(P, j, fe.kap, ntf2, Tbest)) sv = false;
                     }
+                    if (sv && POLICY == 1 && P.A == 1) {
+                        const int jj = j;
+                        auto ntf3 = [&](int i) { return i < jj ? c.nt[i] : r.NT; };
+                        if (t_certainly_below<NS>(P, j, fe.kap, ntf3, wb->lmin)) sv = false;
+                    }
                     if (sv && POLICY == 1) {
                         const int Ulb = fe.U + c.restU;
                         sv = (unsigned long long)objkey_minres(max(fe.u, (Ulb + P.R - 1) / P.R), Ulb) <= wb->bound;
@@ -1125,17 +1233,22 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
                     const bool fits = sv && slot < S.out_cap;
                     if (fits) {
                         const OptRec &full = list[opt];
-                        emit_child<CM, NS>(P, nd, c, j, r, full.p, full.W, full.As, opt, outf + slot);
+                        emit_child<CM, NS>(P, nd, c, j, r, full.p, full.W, full.As, opt, outf, slot);
                     }
+                    PTM(5);
                     m = __ballot_sync(0xffffffffu, sv && !fits);   // frontier full: descend inline
                 }
                 __syncwarp();
                 if (lane == 0) ctl->msk[j] = m;
                 __syncwarp();
             }
+            PTM(6);
         }
     }
+    PTM(7);
 #ifdef CAMELOT_FTRACE
+    if (dbg_me)
+        for (int k = 1; k < 8; ++k) trace_value(S.hdr, 112 + k, dbg_t[k] ? dbg_t[k] - dbg_t[0] : 0);
     if (lane == 0 && dbg_nb) {
         atomicAdd(&S.hdr->dbg_batches[jtop], dbg_nb);
         atomicMax(&S.hdr->dbg_maxb[jtop], dbg_nb);

@@ -158,11 +158,23 @@ __device__ __noinline__ uint32_t sw_fail_bits(const DevProb &P, int p, float bw,
 // Largest float h with fl(dem + h) <= BW: fl(dem + y) is monotone in y, so
 // fl(dem + fl(k bw)) <= BW  <=>  fl(k bw) <= h  (exact).
 __device__ __forceinline__ float bw_threshold(float dem, float BW) {
+    // start at fl(BW - dem) and step by one ulp (integer steps on the bit pattern of
+    // the non-negative / negative float) until the largest admissible value is found
+    auto up = [](float v) {   // next float towards +inf
+        const uint32_t b = __float_as_uint(v);
+        if (b == 0x80000000u) return __uint_as_float(1u);                 // -0 -> +min subnormal
+        return __uint_as_float((b >> 31) ? b - 1u : b + 1u);
+    };
+    auto down = [](float v) {   // next float towards -inf
+        const uint32_t b = __float_as_uint(v);
+        if (b == 0u) return __uint_as_float(0x80000001u);                 // +0 -> -min subnormal
+        return __uint_as_float((b >> 31) ? b + 1u : b - 1u);
+    };
     float h = __fsub_rn(BW, dem);
-    while (__fadd_rn(dem, h) > BW) h = nextafterf(h, __int_as_float(0xff800000));
+    while (__fadd_rn(dem, h) > BW) h = down(h);
     while (true) {
-        const float h2 = nextafterf(h, __int_as_float(0x7f800000));
-        if (!(__fadd_rn(dem, h2) <= BW) || h2 == h) break;
+        const float h2 = up(h);
+        if (!(__fadd_rn(dem, h2) <= BW) || isinf(h2)) break;
         h = h2;
     }
     return __fadd_rn(h, 0.0f);   // -0 -> +0 (the sign-bit test of the sweep needs +0)
@@ -190,6 +202,9 @@ __global__ void __launch_bounds__(SWEEP_THREADS, 2) sweep_kernel(const DevProb P
     // NS == n for n <= 6 (the host dispatches exact widths), so stage guards fold away
     const int n = NS <= 6 ? NS : P.n;
     const int nQ = P.nQ, O = P.O, Rmax = P.Rmax;
+    // quota sub-grid (incumbent cascade): sub index t -> canonical theta; Os options per stage
+    const int nQs = A.nQs, qs = A.qstride, Os = Rmax * nQs;
+    auto canon = [&](int os) { return (os / nQs) * nQ + (nQ - 1 - qs * (nQs - 1 - os % nQs)); };
     const int jl = n - 1;                     // leaf stage
     const bool cont = !(P.flags & F_NO_CONTENTION);
     const bool cap = !(P.flags & F_NO_BW_CAP);
@@ -221,8 +236,8 @@ __global__ void __launch_bounds__(SWEEP_THREADS, 2) sweep_kernel(const DevProb P
 #pragma unroll
             for (int k = NS - 1; k >= 0; --k)
                 if (k < n - 2) {
-                    o[k] = (int)(t % (unsigned)O);
-                    t /= (unsigned)O;
+                    o[k] = canon((int)(t % (unsigned)Os));
+                    t /= (unsigned)Os;
                 }
             int bc = (int)t;
             for (int a = P.A - 1; a >= 0; --a) {
@@ -252,13 +267,23 @@ __global__ void __launch_bounds__(SWEEP_THREADS, 2) sweep_kernel(const DevProb P
         }
         if (!ok) continue;   // the whole grandparent is infeasible (uniform)
         // ---- parent (per lane): option of stage n-2
-        const int op = ch * 32 + lane;
-        const unsigned long long xp = gp * (unsigned long long)O + (unsigned long long)min(op, O - 1);   // parent index
+        const int ops = ch * 32 + lane;              // parent option in the (sub-)grid
+        const int op = canon(min(ops, Os - 1));      // canonical option code
+        unsigned long long gpc = 0;                  // canonical grandparent index
+        {
+            int bc = 0;
+            for (int a = 0; a < P.A; ++a) bc = bc * P.nS + beta[a];
+            gpc = (unsigned long long)bc;
+#pragma unroll
+            for (int k = 0; k < NS; ++k)
+                if (k < n - 2) gpc = gpc * (unsigned long long)O + (unsigned long long)o[k];
+        }
+        const unsigned long long xp = gpc * (unsigned long long)O + (unsigned long long)op;   // parent index
         const unsigned long long xpO = xp * (unsigned long long)O;
         int clo = 0, chi = O;
         if (A.lo > xpO) clo = (int)min(A.lo - xpO, (unsigned long long)O);
         if (A.hi < xpO + O) chi = A.hi > xpO ? (int)(A.hi - xpO) : 0;
-        bool act = op < O && clo < chi;
+        bool act = ops < Os && clo < chi;
         if (act && A.world > 1) {
             const unsigned long long item = xp / P.opow[n - 1 - A.d0];
             act = ((item / 64ull) % (unsigned long long)A.world) == (unsigned long long)A.rank;
@@ -348,7 +373,8 @@ __global__ void __launch_bounds__(SWEEP_THREADS, 2) sweep_kernel(const DevProb P
         // ---- the leaves: quota theta outer (capacities once), replicas N inner.
         // Kept compact (rolled N loop, no per-GPU branches): the hot loop must stay
         // within the ~6 KB L0 instruction cache.
-        for (int th = 0; th < nQ; ++th) {
+        for (int ts = 0; ts < nQs; ++ts) {
+            const int th = nQ - 1 - qs * (nQs - 1 - ts);
             const float4 e = __ldg(&tabL[th]);
             const uint32_t qp = qpm_s[th];
             const uint32_t pmul = qp >> 7;

@@ -11,7 +11,9 @@ struct SweepArgs {
     unsigned long long lo, hi;        // canonical index range [lo, hi)
     unsigned long long g_lo;          // first grandparent
     unsigned long long n_items;       // grandparents x nchunk
-    int nchunk;                       // ceil(O / 32) parent chunks per grandparent
+    int nchunk;                       // ceil(Os / 32) parent chunks per grandparent
+    int qstride;                      // quota sub-grid: every qstride-th quota from the top (1 = all)
+    int nQs;                          // sub-grid size (nQ - 1) / qstride + 1; Os = Rmax * nQs
     const float *lam;                 // [A] load level (min-resource)
     const int *y;                     // Eq. 2 estimates [nbc][ystride] at + yoff
     int ystride, yoff;

@@ -23,6 +23,12 @@ def show(tag, tr, st):
             line = []
             if prev is not None:
                 line.append(f"[gap {(ns - prev)/1e3:.1f}]")
+        elif 48 <= t < 64:
+            line.append(f"fin{t - 48}={(ns - prev)/1e3:.1f}")
+            continue
+        elif t >= 112:
+            line.append(f"w{t - 112}={ns/1e3:.1f}")
+            continue
         elif t >= 64:
             line.append(f"{['par', 'bat', 'maxb'][(t - 64) // 16]}{t % 16}={ns}")
             continue
