@@ -357,7 +357,8 @@ int launch_search(const Ctx &X, const SearchArgs &S, int grid) {
 
 template <int CM>
 size_t level_smem() {   // filter scratch, then search state + StageBound cache (n x nS <= 8 x 64)
-    return std::max(search_smem_bytes<CM>() + (size_t)NMAX * CAMELOT_MAX_BATCHES * sizeof(StageBound),
+    return std::max(search_smem_bytes<CM>() + (size_t)NMAX * CAMELOT_MAX_BATCHES * sizeof(StageBound) +
+                        (ITEM_SMEM + 1) * sizeof(unsigned long long),
                     sizeof(FilterSmem));
 }
 

@@ -15,6 +15,7 @@ namespace cam {
 
 constexpr int FILTER_THREADS = 512;
 constexpr int OMAX = 16 * 128;   // Rmax * nQ upper bound
+constexpr int ITEM_SMEM = 256;   // batch combos whose item offsets live in shared memory
 
 struct FilterArgs {
     int policy, prune, stride, nlev;
@@ -42,6 +43,7 @@ struct FilterSmem {
     float mindur[NMAX];
     int minNP[NMAX];
     int Qs[CAMELOT_MAX_QUOTAS];
+    unsigned char oth[OMAX], oN[OMAX];        // option code -> (theta, N) (no divisions in the rounds)
 };
 
 // Filter body for batch b, executed by one whole CTA (any blockDim multiple of 32).
@@ -60,6 +62,10 @@ __device__ void filter_body(const DevProb &P, const FilterArgs &F, int b, Filter
     const int n = P.n, O = P.O, nQ = P.nQ;
     for (int q = tid; q < n * nQ; q += blockDim.x) tabs[q] = P.tab[((size_t)(q / nQ) * P.nS + b) * nQ + q % nQ];
     for (int q = tid; q < nQ; q += blockDim.x) Qs[q] = P.Q[q];
+    for (int o = tid; o < O; o += blockDim.x) {
+        fsm.oth[o] = (unsigned char)(o % nQ);
+        fsm.oN[o] = (unsigned char)(o / nQ + 1);
+    }
     __syncthreads();
     FTRACE(4);
     const bool cap = !(P.flags & F_NO_BW_CAP);
@@ -77,9 +83,9 @@ __device__ void filter_body(const DevProb &P, const FilterArgs &F, int b, Filter
             lam_min[a] = m;
         }
     // static conditions
-    for (int idx = tid; idx < n * O; idx += blockDim.x) {
-        const int i = idx / O, o = idx % O;
-        const int th = o % nQ, N = o / nQ + 1;
+    for (int i = 0; i < n; ++i)
+    for (int o = tid; o < O; o += blockDim.x) {
+        const int th = fsm.oth[o], N = fsm.oN[o];
         const float4 e = tabs[i * nQ + th];
         const uint32_t As = P.Am[i] * (uint32_t)P.S[b];
         bool k = true;
@@ -104,7 +110,7 @@ __device__ void filter_body(const DevProb &P, const FilterArgs &F, int b, Filter
             int mn = 0x7fffffff;
             for (int o = lane; o < O; o += 32)
                 if (keep[i][o]) {
-                    const int th = o % nQ, N = o / nQ + 1;
+                    const int th = fsm.oth[o], N = fsm.oN[o];
                     md = fminf(md, tabs[i * nQ + th].x);
                     mn = min(mn, N * Qs[th]);
                 }
@@ -120,10 +126,11 @@ __device__ void filter_body(const DevProb &P, const FilterArgs &F, int b, Filter
         __syncthreads();
         FTRACE(6);
         if (it == rounds) break;
-        for (int idx = tid; idx < n * O; idx += blockDim.x) {
-            const int i = idx / O, o = idx % O;
+        bool changed = false;
+        for (int i = 0; i < n; ++i)
+        for (int o = tid; o < O; o += blockDim.x) {
             if (!keep[i][o]) continue;
-            const int th = o % nQ, N = o / nQ + 1;
+            const int th = fsm.oth[o], N = fsm.oN[o];
             const int a = P.app[i];
             const float dur = tabs[i * nQ + th].x;
             // QoS: ordered fp32 sum with this option's duration and the others' minima
@@ -142,10 +149,15 @@ __device__ void filter_body(const DevProb &P, const FilterArgs &F, int b, Filter
                 const long long ulb = (U + P.R - 1) / P.R;
                 if (ulb > uinc || (ulb >= uinc && U > Uinc)) k = false;
             }
-            if (!k) keep[i][o] = 0;
+            if (!k) {
+                keep[i][o] = 0;
+                changed = true;
+            }
         }
-        __syncthreads();
+        // fixpoint reached: the minima of the next round would be the same
+        const bool any = __syncthreads_or(changed);
         FTRACE(7);
+        if (!any) break;
     }
     // compaction in ascending option code (warp w: stage w) + records
     for (int i = wid; i < n; i += (int)(blockDim.x >> 5)) {
@@ -158,7 +170,7 @@ __device__ void filter_body(const DevProb &P, const FilterArgs &F, int b, Filter
             const bool k = o < O && keep[i][o];
             const unsigned m = __ballot_sync(0xffffffffu, k);
             if (k) {
-                const int th = o % nQ, N = o / nQ + 1;
+                const int th = fsm.oth[o], N = fsm.oN[o];
                 const float4 e = tabs[i * nQ + th];
                 OptRec r;
                 r.code = (uint32_t)o;
@@ -247,6 +259,37 @@ __device__ void item_offsets(const DevProb &P, const StageBound *sb, int d0, uns
     }
     item_off[P.nbc] = acc;
     hdr->items_total = acc;
+}
+
+// The same offsets computed by a whole CTA from shared-memory bounds into shared
+// memory (nbc <= ITEM_SMEM): per-combo counts in parallel, then an inclusive scan.
+__device__ void item_offsets_block(const DevProb &P, const StageBound *sb, int d0, unsigned long long *out) {
+    for (int bc = threadIdx.x; bc < P.nbc; bc += blockDim.x) {
+        int bb[AMAX];
+        int t = bc;
+        for (int a = P.A - 1; a >= 0; --a) {
+            bb[a] = t % P.nS;
+            t /= P.nS;
+        }
+        unsigned long long it = 1;
+        bool empty = false;
+        for (int i = 0; i < P.n; ++i) {
+            const unsigned c = sb[(size_t)i * P.nS + bb[P.app[i]]].cnt;
+            if (c == 0) empty = true;
+            if (i < d0) it *= c;
+        }
+        out[bc + 1] = empty ? 0ull : it;
+    }
+    if (threadIdx.x == 0) out[0] = 0;
+    __syncthreads();
+    const int q = threadIdx.x;   // nbc <= ITEM_SMEM <= blockDim.x
+    for (int off = 1; off < P.nbc; off <<= 1) {   // Hillis-Steele inclusive scan of out[1..nbc]
+        const bool act = q < P.nbc && q >= off;
+        const unsigned long long v = act ? out[q + 1 - off] : 0ull;
+        __syncthreads();
+        if (act) out[q + 1] += v;
+        __syncthreads();
+    }
 }
 
 __global__ void eq2_kernel(const DevProb P, const float *lam, int nlev, int *y) {
@@ -578,16 +621,29 @@ search_level_kernel(const DevProb P, const LevelArgs LA) {
     }
     grid.sync();
     if (tr) trace_mark(hdr, 2);
-    // phase 2: item offsets (chunk ownership)
-    if (blockIdx.x == 0 && threadIdx.x == 0) item_offsets(P, S.sb, S.d0, LA.F.item_off, hdr);
-    grid.sync();
-    if (tr) trace_mark(hdr, 3);
-    // per-CTA copy of the (stage, batch) bounds in shared memory, after the search state
+    // per-CTA copy of the (stage, batch) bounds in shared memory, after the search state,
+    // and (phase 2) the item offsets of the chunk ownership: computed by every CTA from
+    // its copy (no grid barrier) when there are few batch combos; block 0 also writes
+    // them to global memory for a later chunk re-scan
     {
         StageBound *sbs = reinterpret_cast<StageBound *>(smem_raw + search_smem_bytes<CM>());
         for (int q = threadIdx.x; q < P.n * P.nS; q += blockDim.x) sbs[q] = S.sb[q];
         __syncthreads();
         S.sb = sbs;
+        if (P.nbc <= ITEM_SMEM) {
+            unsigned long long *ioff = reinterpret_cast<unsigned long long *>(sbs + NMAX * CAMELOT_MAX_BATCHES);
+            item_offsets_block(P, sbs, S.d0, ioff);
+            if (blockIdx.x == 0) {
+                for (int t = threadIdx.x; t <= P.nbc; t += blockDim.x) LA.F.item_off[t] = ioff[t];
+                if (threadIdx.x == 0) hdr->items_total = ioff[P.nbc];
+            }
+            S.item_off = ioff;
+        } else {
+            grid.sync();
+            if (blockIdx.x == 0 && threadIdx.x == 0) item_offsets(P, S.sb, S.d0, LA.F.item_off, hdr);
+            grid.sync();
+        }
+        if (tr) trace_mark(hdr, 3);
     }
     // phase 3: the passes (shared memory now holds the search state)
     Node<CM> *stack_all = reinterpret_cast<Node<CM> *>(smem_raw);

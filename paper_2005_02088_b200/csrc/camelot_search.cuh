@@ -26,10 +26,19 @@
 
 namespace cam {
 
+// testing knob (compile time): -DCAMELOT_NO_TMODE keeps every pass in the warp mode
+__device__ __forceinline__ bool getenv_tmode_off() {
+#ifdef CAMELOT_NO_TMODE
+    return true;
+#else
+    return false;
+#endif
+}
+
 constexpr int SEARCH_THREADS = 256;
 constexpr int SEARCH_WARPS = SEARCH_THREADS / 32;
 #ifndef SEARCH_MINB
-#define SEARCH_MINB 2   // measured: 128 regs x 2 CTAs beats 200 regs x 1 CTA (C4 2.8 vs 3.3 ms)
+#define SEARCH_MINB 1   // measured with the thread-per-parent mode: 255 regs x 1 CTA (no spills) beats 128 x 2 (C4 1.51 vs 1.75 ms)
 #endif
 
 struct SearchArgs {
@@ -100,6 +109,56 @@ struct Frontier {
     __device__ __forceinline__ void putf(int w, unsigned long long k, float v) const { put(w, k, __float_as_uint(v)); }
 };
 #define NODE_W(CM, field) ((int)(offsetof(Node<CM>, field) / 4))
+
+// Read-only view of node k of a structure-of-arrays frontier with the field syntax
+// of Node<CM> (nd.prq[q], nd.x, ...), for the thread-per-parent mode: the lanes of
+// a warp view consecutive nodes, so every field read is coalesced.
+template <typename T>
+struct FieldView {
+    const uint32_t *p;
+    unsigned long long cap;
+    __device__ __forceinline__ T operator[](int i) const {
+        // read-only during the pass; written by the previous pass, and the grid barrier
+        // between the two invalidates L1, so the L1-cached read-only path is coherent
+        const uint32_t v = __ldg(p + (size_t)i * cap);
+        T t;
+        memcpy(&t, &v, 4);
+        return t;
+    }
+};
+template <int CM>
+struct NodeSoA {
+    FieldView<int> prq, pcnt, pkim, pgid, kidx, b;
+    FieldView<uint32_t> prm, hmask;
+    FieldView<float> pdem, dur, bw, nt, dmax;
+    unsigned long long x;
+    int U, u, rqsum, bc;
+    float tub;
+    __device__ __forceinline__ NodeSoA(const Frontier<CM> &F, unsigned long long k) {
+        const uint32_t *B = F.base + k;
+        const unsigned long long c = F.cap;
+        auto at = [&](int w) { return B + (size_t)w * c; };
+        prq = {at(NODE_W(CM, prq)), c};
+        pcnt = {at(NODE_W(CM, pcnt)), c};
+        pkim = {at(NODE_W(CM, pkim)), c};
+        pgid = {at(NODE_W(CM, pgid)), c};
+        kidx = {at(NODE_W(CM, kidx)), c};
+        b = {at(NODE_W(CM, b)), c};
+        prm = {at(NODE_W(CM, prm)), c};
+        hmask = {at(NODE_W(CM, hmask)), c};
+        pdem = {at(NODE_W(CM, pdem)), c};
+        dur = {at(NODE_W(CM, dur)), c};
+        bw = {at(NODE_W(CM, bw)), c};
+        nt = {at(NODE_W(CM, nt)), c};
+        dmax = {at(NODE_W(CM, dmax)), c};
+        x = (unsigned long long)__ldg(at(NODE_W(CM, x))) | ((unsigned long long)__ldg(at(NODE_W(CM, x) + 1)) << 32);
+        U = (int)__ldg(at(NODE_W(CM, U)));
+        u = (int)__ldg(at(NODE_W(CM, u)));
+        rqsum = (int)__ldg(at(NODE_W(CM, rqsum)));
+        bc = (int)__ldg(at(NODE_W(CM, bc)));
+        tub = __uint_as_float(__ldg(at(NODE_W(CM, tub))));
+    }
+};
 
 // per-warp DFS bookkeeping (shared memory)
 struct WarpCtl {
@@ -381,8 +440,8 @@ struct PCtx {
     unsigned long long x;
 };
 
-template <int CM, int NS>
-__device__ __forceinline__ void load_ctx(const DevProb &P, const SearchArgs &S, const Node<CM> &nd, int j,
+template <int CM, int NS, typename ND = Node<CM>>
+__device__ __forceinline__ void load_ctx(const DevProb &P, const SearchArgs &S, const ND &nd, int j,
                                          PCtx<CM, NS> &c) {
     c.empty = 0;
 #pragma unroll
@@ -704,8 +763,8 @@ __device__ __forceinline__ void copy_node(Node<CM> &dst, const Frontier<CM> &F, 
 }
 
 // Ownership of the child (stage j, option index kopt) of nd at depth S.d0 = j+1.
-template <int CM>
-__device__ __forceinline__ bool owns_child(const DevProb &P, const SearchArgs &S, const Node<CM> &nd, int j,
+template <int CM, typename ND = Node<CM>>
+__device__ __forceinline__ bool owns_child(const DevProb &P, const SearchArgs &S, const ND &nd, int j,
                                            int kopt) {
     unsigned long long it = 0;
     for (int i = 0; i <= j; ++i)
@@ -720,8 +779,8 @@ __device__ __forceinline__ bool owns_child(const DevProb &P, const SearchArgs &S
 // writes it to the global frontier: the same state as build_child (warp
 // version), computed independently per lane so that all survivors of a batch
 // are emitted in parallel.
-template <int CM, int NS>
-__device__ __forceinline__ void emit_child(const DevProb &P, const Node<CM> &nd, const PCtx<CM, NS> &c, int j,
+template <int CM, int NS, typename ND = Node<CM>>
+__device__ __forceinline__ void emit_child(const DevProb &P, const ND &nd, const PCtx<CM, NS> &c, int j,
                                            const OptRec &r, uint32_t p, uint32_t W, uint32_t As, int kopt,
                                            const Frontier<CM> &F, unsigned long long k) {
 #define OUT_PUT(field, idx, v) F.put(NODE_W(CM, field) + (idx), k, (uint32_t)(v))
@@ -945,6 +1004,199 @@ __device__ __forceinline__ void init_warp_best(const SearchArgs &S, WarpBest *wb
     __syncwarp();
 }
 
+// Thread-per-parent mode of a heavy pass (many parents, one block of children
+// each): lane l evaluates ALL children of parent e0 + l sequentially, reading the
+// parent from the structure-of-arrays frontier with coalesced loads.  Same bounds
+// and scoring as the warp mode (one load level for leaf passes); the lanes' bests
+// are merged into the warp best at the end of the chunk.
+template <int CM, int NS, int POLICY>
+__device__ __forceinline__ void thread_chunk(const DevProb &P, const SearchArgs &S, const Frontier<CM> &in,
+                                          const Frontier<CM> &outf, unsigned long long e0, unsigned live, int j,
+                                          WarpBest *wb, int lane, Counters &cn) {
+    const int n = P.n, nlev = S.nlev;
+    const bool leaf = j == n - 1;
+    const unsigned long long span = P.opow[n - 1 - j];
+    unsigned long long bk = wb->key[0], bx = wb->x[0];   // lane-local best (leaf passes: one level)
+    const bool mine = (live >> lane) & 1u;
+    {
+        // dead lanes view node e0 (valid memory) and have no children
+        const NodeSoA<CM> nd(in, e0 + (mine ? lane : 0));
+        PCtx<CM, NS> c;
+        load_ctx<CM, NS>(P, S, nd, j, c);
+        const int bj = nd.b[P.app[j]];
+        bool go_node = mine;
+        if (go_node) {
+            unsigned long long kl;
+            if (POLICY == 0) kl = objkey_maxload(fminf(c.tub, fminf(sb_at(P, S, j, bj).maxNT, c.restT)));
+            else {
+                const int Ulb = c.U + (int)sb_at(P, S, j, bj).minNP + c.restU;
+                kl = objkey_minres(max(c.u, (Ulb + P.R - 1) / P.R), Ulb);
+            }
+            go_node = can_win(kl, c.x * P.opow[n - j], wb, nlev, S.xshift);
+            if (POLICY == 1 && P.A == 1 && c.tub < wb->lmin) go_node = false;
+        }
+        const int cnt = go_node ? (int)sb_at(P, S, j, bj).cnt : 0;
+        const OptRec *list = S.rec + ((size_t)j * P.nS + bj) * P.O;
+        unsigned smask = 0u;   // surviving children of this lane's parent (inner passes)
+        const int cntw = __reduce_max_sync(0xffffffffu, cnt);
+        for (int k = 0; k < cntw; ++k) {
+            const bool valid = k < cnt;
+            OptRec r;
+            {
+                const uint4 *src = reinterpret_cast<const uint4 *>(list + (valid ? k : 0));
+                const uint4 a = __ldg(src), b = __ldg(src + 1);
+                r.code = a.x;
+                r.NP = a.y;
+                r.N = a.z;
+                r.pmul = a.w;
+                r.NB = __uint_as_float(b.x);
+                r.NT = __uint_as_float(b.y);
+                r.bw = __uint_as_float(b.z);
+                r.dur = __uint_as_float(b.w);
+            }
+            const unsigned long long x = c.x * (unsigned long long)P.O + r.code;
+            bool go = valid;
+            if (go) {
+                unsigned long long kl;
+                if (POLICY == 0) {
+                    const float t = leaf ? fminf(c.tub, r.NT) : fminf(fminf(c.tub, r.NT), c.restT);
+                    kl = objkey_maxload(t);
+                } else {
+                    const int Ulb = c.U + (int)r.NP + c.restU;
+                    kl = objkey_minres(max(c.u, (Ulb + P.R - 1) / P.R), Ulb);
+                }
+                go = can_win(kl, x * span, wb, nlev, S.xshift);
+                if (go && leaf && POLICY == 0) go = kl < bk || (kl == bk && x < bx);   // the lane's own best
+                if (go && !leaf && c.rqsum - (int)r.NP < c.restU) go = false;
+            }
+            if (go) {
+                const int aj = P.app[j];
+                float lb = c.lpre < 0.0f ? r.dur : __fadd_rn(c.lpre, r.dur);
+#pragma unroll
+                for (int i = 0; i < NS; ++i)
+                    if (i > j && i < n && P.app[i] == aj) lb = __fadd_rn(lb, c.dur[i]);
+                go = lb <= P.qos[aj];
+            }
+            if (go) {
+                const unsigned long long xs = x * span;
+                if (xs >= S.hi || xs + span <= S.lo) go = false;
+            }
+            FastEval fe;
+            fe.placed = false;
+            if (go) fast_eval<CM, NS>(P, c, j, r, fe);
+            const int jj = j;
+            auto ntf = [&](int i) { return i < jj ? c.nt[i] : r.NT; };
+            if (leaf) {
+                if (!go) continue;
+                cn.scored += 1;
+                bool feas = fe.placed;
+                if (feas) {
+                    bool q = fe.lsum[0] <= P.qos[0];
+                    if (P.A > 1) q &= fe.lsum[1] <= P.qos[1];
+                    if (!q) cn.viol |= V_QOS;
+                    feas = q;
+                }
+                cn.feasible += feas;
+                if (!feas) continue;
+                if (POLICY == 0) {
+                    if (bk < 0xFFFFFFFFull) {
+                        const float Tb = __uint_as_float(0xFFFFFFFFu - (unsigned)bk);
+                        if (t_certainly_below<NS>(P, n - 1, fe.kap, ntf, Tb)) continue;
+                    }
+                    float T = __int_as_float(0x7f800000);
+#pragma unroll
+                    for (int i = 0; i < NS; ++i)
+                        if (i < n) T = fminf(T, fe.kap[i] == 1.0f ? ntf(i) : __fdiv_rn(ntf(i), fe.kap[i]));
+                    const unsigned long long key = objkey_maxload(T);
+                    if (key < bk || (key == bk && x < bx)) {
+                        bk = key;
+                        bx = x;
+                    }
+                } else {
+                    const unsigned long long key = objkey_minres(fe.u, fe.U);
+                    if (key > wb->bound || !(key < bk || (key == bk && x < bx))) continue;
+                    float tm0 = __int_as_float(0x7f800000), tm1 = __int_as_float(0x7f800000);
+#pragma unroll
+                    for (int i = 0; i < NS; ++i)
+                        if (i < n) {
+                            const float ti = fe.kap[i] == 1.0f ? ntf(i) : __fdiv_rn(ntf(i), fe.kap[i]);
+                            if (P.app[i] == 0) tm0 = fminf(tm0, ti);
+                            else tm1 = fminf(tm1, ti);
+                        }
+                    bool fk = tm0 >= S.lam[0];
+                    if (P.A > 1) fk &= tm1 >= S.lam[1];
+                    if ((P.flags & F_EQ2_BUDGET) && fe.u > S.y[c.bc * S.ystride + S.yoff]) fk = false;
+                    if (fk) {
+                        bk = key;
+                        bx = x;
+                    }
+                }
+                continue;
+            }
+            // ---- inner node: bounds with the current contention, then emit
+            cn.nodes += go;
+            bool sv = go && fe.placed;
+            if (sv) {
+                sv &= fe.lsum[0] <= P.qos[0];
+                if (P.A > 1) sv &= fe.lsum[1] <= P.qos[1];
+                if (sv && POLICY == 0 && wb->bound < 0xFFFFFFFFull) {
+                    const float Tbest = __uint_as_float(0xFFFFFFFFu - (unsigned)wb->bound);
+                    if (t_certainly_below<NS>(P, j, fe.kap, ntf, Tbest)) sv = false;
+                }
+                if (sv && POLICY == 1 && P.A == 1 && t_certainly_below<NS>(P, j, fe.kap, ntf, wb->lmin)) sv = false;
+                if (sv && POLICY == 1) {
+                    const int Ulb = fe.U + c.restU;
+                    sv = (unsigned long long)objkey_minres(max(fe.u, (Ulb + P.R - 1) / P.R), Ulb) <= wb->bound;
+                }
+            }
+            if (sv && j + 1 == S.d0) sv = owns_child<CM>(P, S, nd, j, k);
+            if (sv) smask |= 1u << k;   // emitted after the loop (cnt <= 32)
+        }
+        // emission rounds: every lane emits its next survivor in the same round, with
+        // warp-aggregated consecutive slots (coalesced structure-of-arrays stores;
+        // capacity checked by the caller)
+        while (true) {
+            const unsigned m = __ballot_sync(0xffffffffu, smask != 0u);
+            if (!m) break;
+            unsigned long long fbase = 0;
+            if (lane == 0) fbase = atomicAdd(S.out_tail, (unsigned long long)__popc(m));
+            fbase = __shfl_sync(0xffffffffu, fbase, 0);
+            if (smask) {
+                const int k = __ffs(smask) - 1;
+                smask &= smask - 1u;
+                OptRec r;
+                {
+                    const uint4 *src = reinterpret_cast<const uint4 *>(list + k);
+                    const uint4 a = __ldg(src), b = __ldg(src + 1);
+                    r.code = a.x;
+                    r.NP = a.y;
+                    r.N = a.z;
+                    r.pmul = a.w;
+                    r.NB = __uint_as_float(b.x);
+                    r.NT = __uint_as_float(b.y);
+                    r.bw = __uint_as_float(b.z);
+                    r.dur = __uint_as_float(b.w);
+                }
+                const OptRec &full = list[k];
+                emit_child<CM, NS>(P, nd, c, j, r, full.p, full.W, full.As, k, outf, fbase + __popc(m & ((1u << lane) - 1u)));
+            }
+        }
+    }
+    __syncwarp();
+    if (leaf) {   // merge the lanes' bests (converged)
+        const bool imp = bk < 0xFFFFFFFFull && slot_less(bk, bx, wb->key[0], wb->x[0]);
+        warp_improve(wb, 0, imp, bk, bx, lane);
+        if (lane == 0) {
+            if (wb->key[0] < wb->bound) {
+                wb->bound = wb->key[0];
+                atomicMin(&S.hdr->best_obj, (unsigned int)wb->key[0]);
+            }
+            publish_best(S, wb);
+        }
+        __syncwarp();
+    }
+}
+
 // One level-synchronous pass (parents at depth S.level), executed by one warp
 // of a persistent grid until the pass's work is exhausted.
 template <int CM, int NS, int POLICY>
@@ -984,7 +1236,13 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
     // from a few coalesced frontier words before copying any survivor.
     const unsigned long long nwarps = (unsigned long long)gridDim.x * SEARCH_WARPS;
     const bool screen = S.prune && have_in && split == 1 && count >= 16ull * nwarps;
-    const unsigned grab = screen ? 8u : (unsigned)S.grab;
+    // thread-per-parent mode: leaf passes with one level, or inner passes whose children
+    // all fit in the output frontier (no inline descent possible in this mode)
+    // (measured: leaf passes with more than 32 options per parent are faster in the warp mode)
+    const bool tmode = S.prune && have_in && split == 1 && count >= 2ull * nwarps && maxc <= 32 && !getenv_tmode_off() &&
+                       ((S.flevel < 0 && jtop == n - 1 && nlev == 1) ||
+                        (S.flevel == jtop + 1 && count * (unsigned long long)maxc <= S.out_cap));
+    const unsigned grab = tmode ? 32u : screen ? 8u : (unsigned)S.grab;
     const unsigned long long nw = nwarps * grab;
     unsigned long long e0 = ((unsigned long long)blockIdx.x * SEARCH_WARPS + (threadIdx.x >> 5)) * grab;
     bool first = true;
@@ -1008,7 +1266,7 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
         __syncwarp();
         const unsigned long long e1 = min(e0 + (unsigned long long)grab, items);
         unsigned live = 0xffffffffu;
-        if (screen) {
+        if (screen || tmode) {
             const unsigned long long ei = e0 + lane;
             bool lv = ei < e1;
             if (lv) {
@@ -1037,6 +1295,10 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
                 lv = can_win(kl, xq * P.opow[n - jtop], wb, nlev, S.xshift);
             }
             live = __ballot_sync(0xffffffffu, lv);
+        }
+        if (tmode) {
+            thread_chunk<CM, NS, POLICY>(P, S, in, outf, e0, live, jtop, wb, lane, cn);
+            continue;
         }
         for (unsigned long long it = e0; it < e1; ++it) {
             if (!((live >> (unsigned)(it - e0)) & 1u)) continue;
