@@ -368,7 +368,8 @@ __global__ void plan_kernel(const DevProb P, int policy, int nlev, const Slot *w
     int beta[AMAX], rho[NMAX], theta[NMAX];
     decode_index(P, w.x, beta, rho, theta);
     FullScore s;
-    score_digits(P, beta, rho, theta, s);
+    __shared__ ScoreScratch scr[64];   // blockDim <= 64: shared instead of local memory (serial path)
+    score_digits(P, beta, rho, theta, s, &scr[threadIdx.x]);
     pl.index = w.x;
     pl.status = CAMELOT_OK;
     for (int a = 0; a < P.A; ++a) {

@@ -49,8 +49,18 @@ __device__ __forceinline__ uint32_t fit_viol(const DevProb &P, int rq, int cnt, 
     return v;
 }
 
+// Per-thread scratch of the placement in score_digits; kernels that score few
+// candidates on a long serial path (plan_kernel) pass it in shared memory.
+struct ScoreScratch {
+    int rq[SCORE_CMAX], cnt[SCORE_CMAX], order[SCORE_CMAX];
+    uint32_t rm[SCORE_CMAX];
+    float dem[SCORE_CMAX];
+    uint32_t hmask[NMAX];
+    uint8_t hcnt[NMAX][SCORE_CMAX];
+};
+
 __device__ void score_digits(const DevProb &P, const int *beta, const int *rho, const int *theta,
-                             FullScore &out) {
+                             FullScore &out, ScoreScratch *scr = nullptr) {
     const int n = P.n, C = P.C;
     float dur[NMAX], thr[NMAX], bwv[NMAX];
     int U = 0;
@@ -83,11 +93,13 @@ __device__ void score_digits(const DevProb &P, const int *beta, const int *rho, 
         if (!(P.flags & F_NO_BW_CAP) && bsum > __fmul_rn((float)C, P.BW)) pv |= V_BW;
         if (mem > (long long)C * (long long)P.FM) pv |= V_MEM;
     } else {
-        int rq[SCORE_CMAX], cnt[SCORE_CMAX];
-        uint32_t rm[SCORE_CMAX];
-        float dem[SCORE_CMAX];
-        uint32_t hmask[NMAX];
-        uint8_t hcnt[NMAX][SCORE_CMAX];
+        ScoreScratch loc;
+        ScoreScratch &X = scr ? *scr : loc;
+        int *rq = X.rq, *cnt = X.cnt;
+        uint32_t *rm = X.rm;
+        float *dem = X.dem;
+        uint32_t *hmask = X.hmask;
+        auto &hcnt = X.hcnt;
         for (int g = 0; g < C; ++g) {
             rq[g] = P.R;
             cnt[g] = 0;
@@ -103,7 +115,7 @@ __device__ void score_digits(const DevProb &P, const int *beta, const int *rho, 
             const uint32_t W = P.W[i];
             const float bw = bwv[i];
             // snapshot order: by (remaining MiB, remaining quota, index) ascending
-            int order[SCORE_CMAX];
+            int *order = X.order;
             for (int g = 0; g < C; ++g) {
                 int r = 0;
                 for (int h = 0; h < C; ++h) {

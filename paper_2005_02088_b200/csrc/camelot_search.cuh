@@ -746,6 +746,7 @@ __device__ __forceinline__ void score_leaf(const DevProb &P, const SearchArgs &S
 // item = canonical position of (beta combo, option indices of stages < d0))?
 template <int CM>
 __device__ __forceinline__ bool owns(const DevProb &P, const SearchArgs &S, const Node<CM> &nd) {
+    if (S.world == 1 && S.chunk_lo == 0 && S.chunk_hi == 0) return true;
     unsigned long long it = 0;
     for (int i = 0; i < S.d0; ++i) it = it * sb_at(P, S, i, nd.b[P.app[i]]).cnt + (unsigned long long)nd.kidx[i];
     const unsigned long long chunk = (S.item_off[nd.bc] + it) / (unsigned long long)S.chunk_items;
@@ -766,6 +767,7 @@ __device__ __forceinline__ void copy_node(Node<CM> &dst, const Frontier<CM> &F, 
 template <int CM, typename ND = Node<CM>>
 __device__ __forceinline__ bool owns_child(const DevProb &P, const SearchArgs &S, const ND &nd, int j,
                                            int kopt) {
+    if (S.world == 1 && S.chunk_lo == 0 && S.chunk_hi == 0) return true;   // one rank, no chunk restriction
     unsigned long long it = 0;
     for (int i = 0; i <= j; ++i)
         it = it * sb_at(P, S, i, nd.b[P.app[i]]).cnt + (unsigned long long)(i < j ? nd.kidx[i] : kopt);
@@ -821,22 +823,30 @@ __device__ __forceinline__ void emit_child(const DevProb &P, const ND &nd, const
         W2 = P.W[i2];
         As2 = P.Am[i2] * (uint32_t)P.S[nd.b[P.app[i2]]];
     }
+    // deployment order for the next stage: (remaining MiB, remaining quota, id) packed
+    // into one orderable 64-bit key (rq <= 127, id < 16)
+    unsigned long long okey[CM];
+#pragma unroll
+    for (int q = 0; q < CM; ++q)
+        okey[q] = ((unsigned long long)rm[q] << 12) | ((unsigned long long)(uint32_t)rq[q] << 4) | (unsigned)g[q];
 #pragma unroll
     for (int q = 0; q < CM; ++q) {
         if (q < P.C) {
             int rank = 0;
 #pragma unroll
             for (int h = 0; h < CM; ++h)
-                if (h < P.C && h != q) {
-                    const bool lt = rm[h] < rm[q] || (rm[h] == rm[q] && (rq[h] < rq[q] || (rq[h] == rq[q] && g[h] < g[q])));
-                    rank += lt ? 1 : 0;
-                }
+                if (h < P.C && h != q) rank += okey[h] < okey[q];
             int kim = 0;
             if (more) {
-                int km = P.Rmax;
-                if (rm[q] < W2) km = 0;
-                else if (As2 > 0) km = (int)min((uint32_t)P.Rmax, (rm[q] - W2) / As2);
-                kim = max(0, min(km, min(P.Rmax, P.I - cnt[q])));
+                // largest k <= min(Rmax, I - cnt) with W2 + k As2 <= rm (binary search, no division)
+                const int lim = min(P.Rmax, P.I - cnt[q]);
+                if (lim > 0 && rm[q] >= W2) {
+#pragma unroll
+                    for (int step = 16; step >= 1; step >>= 1) {
+                        const int t = kim + step;
+                        if (t <= lim && (unsigned long long)W2 + (unsigned long long)t * As2 <= rm[q]) kim = t;
+                    }
+                }
             }
             OUT_PUT(prq, rank, rq[q]);
             OUT_PUT(pcnt, rank, cnt[q]);
@@ -1311,8 +1321,8 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
                 }
                 __syncwarp();
             }
-            const unsigned long long e = it / (unsigned)split;
-            const int blk = (int)(it % (unsigned)split);
+            const unsigned long long e = split == 1 ? it : it / (unsigned)split;
+            const int blk = split == 1 ? 0 : (int)(it % (unsigned)split);
             if (!have_in) {
                 build_root<CM>(P, (int)e, stack[0], lane);
                 if (lane < NMAX) stack[0].kidx[lane] = 0;
