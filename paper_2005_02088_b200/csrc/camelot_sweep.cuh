@@ -28,6 +28,9 @@
 namespace cam {
 
 constexpr int SWEEP_THREADS = 256;
+#ifndef SWEEP_MINB
+#define SWEEP_MINB 2
+#endif
 
 // SweepArgs: camelot_sweep_args.h
 
@@ -190,7 +193,7 @@ __device__ __forceinline__ void sw_better(unsigned long long key, unsigned long 
 
 // The sweep.  NS == n exactly (stage loops carry no runtime guards) unless n > 6.
 template <int CM, int NS, int POLICY, bool TWO>
-__global__ void __launch_bounds__(SWEEP_THREADS, 2) sweep_kernel(const DevProb P, const SweepArgs A) {
+__global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const DevProb P, const SweepArgs A) {
     static_assert(CM <= 8, "thermometer code holds 8 GPUs x 4 bits");
     __shared__ float dem_s[CM][SWEEP_THREADS];
     __shared__ uint32_t qpm_s[CAMELOT_MAX_QUOTAS];   // p | ceil(2^16/p) << 7
