@@ -43,6 +43,7 @@ F_SAT = 4
 F_PAPER_GLOBAL = 8
 F_EQ2_BUDGET = 16
 F_NO_FILTER = 32
+F_COMM = 64          # NEXT-2: communication-aware QoS (R29)
 
 SEED_BASE = 200502088 * 1000
 
@@ -55,6 +56,11 @@ class Cluster:
     bw_gbs: float          # BW
     mem_mib: int           # F
     gflops: float          # G
+    # NEXT-2 (R29/R30): cross-GPU hand-over = D2H + H2D memcpy at 3,150 MB/s each
+    # -> 1.575 GB/s; same-GPU IPC hand-over = the 0.02 MB
+    # crossover of the two mechanisms (L626): 2 x 0.02 MB / 3.15 GB/s = 0.0127 ms
+    link_gbs: float = 1.575
+    ipc_ms: float = 0.0127
 
 
 PRESETS = {
@@ -89,6 +95,7 @@ class Problem:
     cluster: Cluster
     flags: int = 0
     meta: Optional[dict] = None
+    comm_mb_per_item: Optional[np.ndarray] = None   # float32[n] MB per item to the next stage (F_COMM)
 
     @property
     def n_stages(self) -> int:
@@ -104,6 +111,9 @@ class Problem:
         h.update(repr((self.n_apps, self.max_replicas, self.flags, c.n_gpus,
                        c.quota_per_gpu, c.max_instances, c.bw_gbs, c.mem_mib,
                        c.gflops)).encode())
+        if self.flags & F_COMM:
+            h.update(np.ascontiguousarray(self.comm_mb_per_item, np.float32).tobytes())
+            h.update(repr((c.link_gbs, c.ipc_ms)).encode())
         return h.hexdigest()
 
     def with_(self, **kw) -> "Problem":
@@ -248,6 +258,14 @@ def config_problems(config: int, preset: str = "v100-dgx2") -> List[Problem]:
     else:
         raise ValueError(f"unknown config {config}")
     return out
+
+
+def with_comm(prob: Problem, seed: int = 0, mb_range=(0.05, 0.5)) -> Problem:
+    """The same problem with NEXT-2 hand-over sizes (MB per item to the next stage,
+    drawn uniformly; an image-sized activation per item) and the F_COMM flag."""
+    rng = np.random.Generator(np.random.PCG64(SEED_BASE + 950000 + seed))
+    mb = rng.uniform(*mb_range, size=prob.n_stages).astype(np.float32)
+    return prob.with_(comm_mb_per_item=mb, flags=prob.flags | F_COMM)
 
 
 def custom_problem(name: str, table: np.ndarray, quota_pct: Sequence[int],

@@ -94,6 +94,11 @@ typedef enum {
 #define CAMELOT_F_PAPER_GLOBAL 8u   /* literal Eq. 1 global sums, no placement (R3; pins only)   */
 #define CAMELOT_F_EQ2_BUDGET 16u    /* min-resource: enforce GPUs used <= Eq. 2's y (R9)         */
 #define CAMELOT_F_NO_FILTER 32u     /* exhaustive scan without pruning (flat mode)               */
+#define CAMELOT_F_COMM 64u          /* NEXT-2: communication-aware QoS (R29): the hand-over from
+                                       stage i to i+1 of an app is added to the latency sum;
+                                       same-GPU (global-memory IPC) only when
+                                       both stages run entirely on one and the same GPU, else a
+                                       host-staged copy (L442-448).  Not with PAPER_GLOBAL.     */
 
 /* first-failing-check bits (camelot_plan.violations, score vectors) */
 #define CAMELOT_V_QUOTA 1u  /* placement: SM quota per GPU                 */
@@ -115,6 +120,9 @@ typedef struct {
     float bw_gbs;          /* BW, global memory bandwidth per GPU (GB/s, > 0)   */
     uint32_t mem_mib;      /* F, global memory per GPU (MiB), < 2^21            */
     float gflops;          /* G, GFLOPS per GPU (Eq. 2 only, > 0)               */
+    float link_gbs;        /* CAMELOT_F_COMM: cross-GPU hand-over bandwidth (GB/s, > 0);
+                              t = fl(fl(comm_mb_i * s) * fl(1/link_gbs)) ms         */
+    float ipc_ms;          /* CAMELOT_F_COMM: same-GPU hand-over time (ms, >= 0)     */
 } camelot_cluster;
 
 /* The allocation problem.  Per-stage predictions are tabulated on the
@@ -137,6 +145,9 @@ typedef struct {
     const float *gflop_per_item;   /* [n] c_i:  C(i,s) = c_i*s (Eq. 2 only)            */
     const float *bw_sensitivity;   /* [n] gamma_i >= 0 (R17; 0 = paper-strict)         */
     uint32_t flags;                /* CAMELOT_F_*                                      */
+    const float *comm_mb_per_item; /* [n] CAMELOT_F_COMM: MB per batch item sent from stage i
+                                      to stage i+1 of its app (>= 0; unused for the last
+                                      stage of an app); may be NULL without the flag   */
 } camelot_problem;
 
 /* Execution context.  rank/world shard the candidate space (chunk c is searched
@@ -180,6 +191,7 @@ typedef struct {
     uint64_t n_feasible;      /* feasible candidates seen (exact in NO_FILTER mode)  */
     uint64_t n_scored;        /* candidates fully scored by the search               */
     uint64_t n_covered;       /* candidates covered (scored or excluded by a bound)  */
+    float comm_ms[CAMELOT_MAX_STAGES];  /* CAMELOT_F_COMM: hand-over time of edge i -> i+1 (ms) */
 } camelot_plan;
 
 /* ------------------------------------------------------------------ entry points */

@@ -50,6 +50,7 @@
 #define OC_SAT 4u
 #define OC_PAPER_GLOBAL 8u
 #define OC_EQ2_BUDGET 16u
+#define OC_COMM 64u   /* NEXT-2: communication-aware QoS (R29) */
 
 /* first-failing-check bits */
 #define OC_V_QUOTA 1u
@@ -79,6 +80,10 @@ typedef struct {
     float BW;             /* GB/s per GPU */
     uint32_t FM;          /* MiB per GPU */
     float G;              /* GFLOPS per GPU */
+    /* NEXT-2 (flag OC_COMM; reading R29) */
+    const float *comm_mb; /* [n] MB per batch item sent from stage i to stage i+1 of its app */
+    float link_gbs;       /* cross-GPU transfer bandwidth (GB/s): data staged through host memory */
+    float ipc_ms;         /* same-GPU hand-over (global-memory IPC handle) time (ms) */
 } oc_problem;
 
 typedef struct {
@@ -92,6 +97,7 @@ typedef struct {
     double L64[OC_MAX_STAGES], T64[OC_MAX_STAGES], Lsum64[OC_MAX_APPS];
     int8_t gpu_of_instance[OC_MAX_STAGES * OC_MAX_REPL];  /* -1 = unused */
     float dem[OC_MAX_GPUS];
+    float comm[OC_MAX_STAGES];             /* COMM: hand-over time of edge i -> i+1 (0: none) */
     uint32_t level_verdict[OC_MAX_LOADS];  /* min-resource: first failing check per load level */
     int32_t eq2_y[OC_MAX_LOADS];
 } oc_score_t;
@@ -131,6 +137,12 @@ int oc_validate(const oc_problem *P) {
         if (!fin(P->cflop[i]) || P->cflop[i] < 0.0f) return -1;
     }
     if (P->app[0] != 0 || P->app[P->n - 1] != P->A - 1) return -1;
+    if (P->flags & OC_COMM) {
+        if (P->flags & OC_PAPER_GLOBAL) return -1;   /* no placement, no co-location */
+        if (!(P->link_gbs > 0.0f) || !fin(P->link_gbs) || !(P->ipc_ms >= 0.0f) || !fin(P->ipc_ms)) return -1;
+        for (int i = 0; i < P->n; i++)
+            if (!(P->comm_mb[i] >= 0.0f) || !fin(P->comm_mb[i])) return -1;
+    }
     for (int a = 0; a < P->A; a++)
         if (!(P->qos[a] > 0.0f) || !fin(P->qos[a])) return -1;
     for (long e = 0; e < (long)P->n * P->nS * P->nQ; e++) {
@@ -186,7 +198,8 @@ typedef struct {
     int32_t rq[OC_MAX_GPUS];     /* remaining quota (%) */
     int32_t cnt[OC_MAX_GPUS];    /* instances hosted */
     int64_t rm[OC_MAX_GPUS];     /* remaining memory (MiB) */
-    float dem[OC_MAX_GPUS];      /* accumulated bandwidth demand (GB/s) */
+    float dem[OC_MAX_GPUS];
+    float comm[OC_MAX_STAGES];             /* COMM: hand-over time of edge i -> i+1 (0: none) */      /* accumulated bandwidth demand (GB/s) */
     int32_t host[OC_MAX_STAGES][OC_MAX_GPUS];
 } oc_state;
 
@@ -407,7 +420,36 @@ int oc_score(const oc_problem *P, const int32_t *beta, const int32_t *rho, const
             out->T64[i] = (double)Nn[i] * (double)thr[i] / km;
         }
     }
-    /* per app: ordered latency sum vs QoS (Constraint-5, reading R1) and Tmin */
+    /* NEXT-2, reading R29: the hand-over from stage i to stage i+1 of the same app
+     * stays on the GPU (global-memory IPC, ipc_ms) only if both stages run on one
+     * and the same GPU (every replica pair co-located; the tail takes the worst
+     * pair), otherwise the batch's data crosses GPUs through host memory:
+     * fl(fl(comm_mb_i * s) * fl(1 / link_gbs)) ms (MB / (GB/s) = ms). */
+    float comm[OC_MAX_STAGES];
+    for (int i = 0; i < n; i++) comm[i] = 0.0f;
+    if ((P->flags & OC_COMM) && !pv) {
+        const float inv_link = 1.0f / P->link_gbs;
+        for (int i = 0; i + 1 < n; i++) {
+            if (P->app[i] != P->app[i + 1]) continue;
+            int gi = -1, same = 1, cnt_gpus = 0;
+            for (int g = 0; g < P->C; g++) {
+                const int hi = st.host[i][g] > 0, hj = st.host[i + 1][g] > 0;
+                if (hi != hj) same = 0;
+                if (hi) {
+                    cnt_gpus++;
+                    gi = g;
+                }
+            }
+            (void)gi;
+            const int local = same && cnt_gpus == 1;
+            const float s = (float)P->S[beta[P->app[i]]];
+            const float bytes = P->comm_mb[i] * s;
+            comm[i] = local ? P->ipc_ms : bytes * inv_link;
+        }
+    }
+    for (int i = 0; i < n; i++) out->comm[i] = comm[i];
+    /* per app: ordered latency sum vs QoS (Constraint-5, reading R1; with COMM the
+     * hand-over times are interleaved: L_f, t_f, L_f+1, t_f+1, ...) and Tmin */
     uint32_t qos_fail = 0;
     float T = 0.0f;
     for (int a = 0; a < P->A; a++) {
@@ -421,10 +463,11 @@ int oc_score(const oc_problem *P, const int32_t *beta, const int32_t *rho, const
                 tm = out->Ti[i];
                 first = 0;
             } else {
+                if (P->flags & OC_COMM) ls = ls + comm[i - 1];
                 ls = ls + out->L[i];
                 if (out->Ti[i] < tm) tm = out->Ti[i];
             }
-            ls64 += out->L64[i];
+            ls64 += out->L64[i] + (i + 1 < n && P->app[i + 1] == a ? (double)comm[i] : 0.0);
         }
         out->Lsum[a] = ls;
         out->Lsum64[a] = ls64;

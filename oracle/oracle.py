@@ -47,6 +47,7 @@ class OcProblem(C.Structure):
         ("flags", C.c_uint32),
         ("C", C.c_int32), ("R", C.c_int32), ("I", C.c_int32),
         ("BW", C.c_float), ("FM", C.c_uint32), ("G", C.c_float),
+        ("comm_mb", C.POINTER(C.c_float)), ("link_gbs", C.c_float), ("ipc_ms", C.c_float),
     ]
 
 
@@ -61,6 +62,7 @@ class OcScore(C.Structure):
         ("Lsum64", C.c_double * MAX_APPS),
         ("gpu_of_instance", C.c_int8 * (MAX_STAGES * MAX_REPL)),
         ("dem", C.c_float * MAX_GPUS),
+        ("comm", C.c_float * MAX_STAGES),
         ("level_verdict", C.c_uint32 * MAX_LOADS),
         ("eq2_y", C.c_int32 * MAX_LOADS),
     ]
@@ -103,6 +105,8 @@ class Handle:
             Am=np.ascontiguousarray(p.act_mib_per_item, np.uint32),
             cflop=np.ascontiguousarray(p.gflop_per_item, np.float32),
             gamma=np.ascontiguousarray(p.bw_sensitivity, np.float32),
+            comm=np.ascontiguousarray(p.comm_mb_per_item if p.comm_mb_per_item is not None
+                                      else np.zeros(p.n_stages), np.float32),
         )
         k = self.keep
         ptr = lambda a, t: a.ctypes.data_as(C.POINTER(t))
@@ -116,7 +120,8 @@ class Handle:
             gamma=ptr(k["gamma"], C.c_float),
             flags=p.flags if flags is None else flags,
             C=c.n_gpus, R=c.quota_per_gpu, I=c.max_instances, BW=c.bw_gbs,
-            FM=c.mem_mib, G=c.gflops)
+            FM=c.mem_mib, G=c.gflops,
+            comm_mb=ptr(k["comm"], C.c_float), link_gbs=c.link_gbs, ipc_ms=c.ipc_ms)
         self.A, self.n = p.n_apps, p.n_stages
         self.Rmax = p.max_replicas
 
@@ -171,6 +176,7 @@ class Score:
     dem: List[float]
     level_verdict: List[int]
     eq2_y: List[int]
+    comm: List[float] = None   # COMM: hand-over time of edge i -> i+1 (ms)
 
 
 def _loads_arr(loads, A):
@@ -202,7 +208,7 @@ def score(prob, x: int = None, digits=None, loads=None, flags=None) -> Score:
                  list(out.Ti[:n]), list(out.kappa[:n]), list(out.L64[:n]),
                  list(out.T64[:n]), list(out.Lsum64[:A]), goi,
                  list(out.dem[:prob.cluster.n_gpus]), list(out.level_verdict[:L]),
-                 list(out.eq2_y[:L]))
+                 list(out.eq2_y[:L]), list(out.comm[:n]))
 
 
 def score_range(prob, lo: int, hi: int, flags=None):

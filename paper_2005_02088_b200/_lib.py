@@ -19,7 +19,7 @@ HEADER = os.path.join(ROOT, "include", "camelot.h")
 
 MAX_STAGES, MAX_APPS, MAX_GPUS, MAX_REPLICAS, MAX_LOADS = 8, 2, 16, 16, 64
 OK, INFEASIBLE, EINVAL, ERANGE, ECUDA, ENODEV, ENOMEM = 0, 1, -1, -2, -3, -4, -5
-F_NO_BW_CAP, F_NO_CONTENTION, F_SAT, F_PAPER_GLOBAL, F_EQ2_BUDGET, F_NO_FILTER = 1, 2, 4, 8, 16, 32
+F_NO_BW_CAP, F_NO_CONTENTION, F_SAT, F_PAPER_GLOBAL, F_EQ2_BUDGET, F_NO_FILTER, F_COMM = 1, 2, 4, 8, 16, 32, 64
 V_QUOTA, V_INST, V_MEM, V_BW, V_QOS, V_LOAD, V_EQ2 = 1, 2, 4, 8, 16, 32, 64
 POLICY_MAX_LOAD, POLICY_MIN_RESOURCE = 0, 1
 EXEC_RESIDENT = 1
@@ -81,7 +81,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 class Cluster(C.Structure):
     _fields_ = [("n_gpus", C.c_int32), ("quota_per_gpu", C.c_int32), ("max_instances", C.c_int32),
-                ("bw_gbs", C.c_float), ("mem_mib", C.c_uint32), ("gflops", C.c_float)]
+                ("bw_gbs", C.c_float), ("mem_mib", C.c_uint32), ("gflops", C.c_float),
+                ("link_gbs", C.c_float), ("ipc_ms", C.c_float)]
 
 
 class Problem(C.Structure):
@@ -92,7 +93,7 @@ class Problem(C.Structure):
                 ("max_replicas", C.c_int32), ("table", C.POINTER(C.c_float)),
                 ("weights_mib", C.POINTER(C.c_uint32)), ("act_mib_per_item", C.POINTER(C.c_uint32)),
                 ("gflop_per_item", C.POINTER(C.c_float)), ("bw_sensitivity", C.POINTER(C.c_float)),
-                ("flags", C.c_uint32)]
+                ("flags", C.c_uint32), ("comm_mb_per_item", C.POINTER(C.c_float))]
 
 
 class Exec(C.Structure):
@@ -112,7 +113,8 @@ class Plan(C.Structure):
                 ("e2e_latency_ms", C.c_float * MAX_APPS), ("throughput_qps", C.c_float * MAX_APPS),
                 ("objective", C.c_float), ("quota_used", C.c_int32), ("gpus_used", C.c_int32),
                 ("eq2_gpus", C.c_int32), ("violations", C.c_uint32),
-                ("n_feasible", C.c_uint64), ("n_scored", C.c_uint64), ("n_covered", C.c_uint64)]
+                ("n_feasible", C.c_uint64), ("n_scored", C.c_uint64), ("n_covered", C.c_uint64),
+                ("comm_ms", C.c_float * MAX_STAGES)]
 
 
 EXPORTS = ["camelot_last_error", "camelot_version", "camelot_workspace_bytes", "camelot_upload",

@@ -39,6 +39,7 @@ class PlanResult:
     n_feasible: int
     n_scored: int
     n_covered: int
+    comm_ms: List[float] = None   # COMM: hand-over time of edge i -> i+1 (ms)
 
     @property
     def feasible(self) -> bool:
@@ -54,7 +55,7 @@ def _plan(p: L.Plan, n: int, A: int) -> PlanResult:
                       list(p.stage_latency_ms[:n]), list(p.stage_throughput_qps[:n]),
                       list(p.kappa[:n]), list(p.e2e_latency_ms[:A]), list(p.throughput_qps[:A]),
                       p.objective, p.quota_used, p.gpus_used, p.eq2_gpus, p.violations,
-                      int(p.n_feasible), int(p.n_scored), int(p.n_covered))
+                      int(p.n_feasible), int(p.n_scored), int(p.n_covered), list(p.comm_ms[:n]))
 
 
 class Session:
@@ -79,6 +80,9 @@ class Session:
             Am=np.ascontiguousarray(problem.act_mib_per_item, np.uint32),
             cf=np.ascontiguousarray(problem.gflop_per_item, np.float32),
             gm=np.ascontiguousarray(problem.bw_sensitivity, np.float32),
+            cm=np.ascontiguousarray(getattr(problem, "comm_mb_per_item", None)
+                                    if getattr(problem, "comm_mb_per_item", None) is not None
+                                    else np.zeros(self.n), np.float32),
         )
         tab = np.ascontiguousarray(problem.table, np.float32)
         # pinned host copy of the predictor tables (the only sizeable input)
@@ -92,11 +96,12 @@ class Session:
             table=C.cast(self._tab.data_ptr(), C.POINTER(C.c_float)),
             weights_mib=ptr(k["W"], C.c_uint32), act_mib_per_item=ptr(k["Am"], C.c_uint32),
             gflop_per_item=ptr(k["cf"], C.c_float), bw_sensitivity=ptr(k["gm"], C.c_float),
-            flags=int(problem.flags if flags is None else flags))
+            flags=int(problem.flags if flags is None else flags), comm_mb_per_item=ptr(k["cm"], C.c_float))
         c = problem.cluster
         self.ccl = L.Cluster(n_gpus=int(c.n_gpus), quota_per_gpu=int(c.quota_per_gpu),
                              max_instances=int(c.max_instances), bw_gbs=float(c.bw_gbs),
-                             mem_mib=int(c.mem_mib), gflops=float(c.gflops))
+                             mem_mib=int(c.mem_mib), gflops=float(c.gflops),
+                             link_gbs=float(getattr(c, "link_gbs", 1.0)), ipc_ms=float(getattr(c, "ipc_ms", 0.0)))
         self.ws = None
         self._ensure(n_loads)
 

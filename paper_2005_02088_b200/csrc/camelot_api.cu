@@ -95,6 +95,15 @@ int check_problem(const camelot_problem *p, const camelot_cluster *c, Dims &d) {
     if (!p->app_of_stage || !p->qos_ms || !p->quota_pct || !p->batch || !p->table || !p->weights_mib ||
         !p->act_mib_per_item || !p->gflop_per_item || !p->bw_sensitivity)
         return fail(CAMELOT_EINVAL, "null array in problem");
+    if (p->flags & CAMELOT_F_COMM) {
+        if (p->flags & CAMELOT_F_PAPER_GLOBAL) return fail(CAMELOT_EINVAL, "COMM needs a placement (not with PAPER_GLOBAL)");
+        if (!p->comm_mb_per_item) return fail(CAMELOT_EINVAL, "COMM needs comm_mb_per_item");
+        if (!(c->link_gbs > 0.0f) || !std::isfinite(c->link_gbs)) return fail(CAMELOT_EINVAL, "link_gbs must be > 0");
+        if (!(c->ipc_ms >= 0.0f) || !std::isfinite(c->ipc_ms)) return fail(CAMELOT_EINVAL, "ipc_ms must be >= 0");
+        for (int i = 0; i < p->n_stages; ++i)
+            if (!(p->comm_mb_per_item[i] >= 0.0f) || !std::isfinite(p->comm_mb_per_item[i]))
+                return fail(CAMELOT_EINVAL, "comm_mb_per_item[%d] must be finite and >= 0", i);
+    }
     for (int k = 0; k < p->n_quota; ++k) {
         if (p->quota_pct[k] < 1 || p->quota_pct[k] > c->quota_per_gpu) return fail(CAMELOT_EINVAL, "quota_pct[%d] not in [1,R]", k);
         if (k && p->quota_pct[k] <= p->quota_pct[k - 1]) return fail(CAMELOT_EINVAL, "quota grid not strictly ascending");
@@ -246,6 +255,10 @@ DevProb make_devprob(const camelot_problem *p, const camelot_cluster *c, const D
         P.gamma[i] = p->bw_sensitivity[i];
         P.cflop[i] = p->gflop_per_item[i];
     }
+    volatile float link = (p->flags & CAMELOT_F_COMM) ? c->link_gbs : 1.0f;
+    P.inv_link = one / link;   // IEEE binary32 division, as the oracle
+    P.ipc_ms = (p->flags & CAMELOT_F_COMM) ? c->ipc_ms : 0.0f;
+    for (int i = 0; i < d.n; ++i) P.comm_mb[i] = (p->flags & CAMELOT_F_COMM) ? p->comm_mb_per_item[i] : 0.0f;
     P.ntot = d.ntot;
     P.opow[0] = 1;
     for (int k = 1; k <= NMAX; ++k) P.opow[k] = P.opow[k - 1] * (unsigned long long)d.O;

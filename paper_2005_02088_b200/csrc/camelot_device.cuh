@@ -15,7 +15,7 @@ constexpr int LMAX = 64;     // load levels
 constexpr int TRACE_MAX = 256;
 
 constexpr uint32_t F_NO_BW_CAP = 1u, F_NO_CONTENTION = 2u, F_SAT = 4u, F_PAPER_GLOBAL = 8u,
-                   F_EQ2_BUDGET = 16u, F_NO_FILTER = 32u;
+                   F_EQ2_BUDGET = 16u, F_NO_FILTER = 32u, F_COMM = 64u;
 constexpr uint32_t V_QUOTA = 1u, V_INST = 2u, V_MEM = 4u, V_BW = 8u, V_QOS = 16u,
                    V_LOAD = 32u, V_EQ2 = 64u;
 
@@ -31,6 +31,10 @@ struct DevProb {
     float gamma[NMAX], cflop[NMAX];
     unsigned long long ntot;
     unsigned long long opow[NMAX + 1];       // O^k
+    // NEXT-2 (F_COMM, R29): hand-over of edge i -> i+1 at batch s: local (both stages
+    // entirely on one and the same GPU) ipc_ms, else fl(fl(comm_mb[i] * s) * inv_link)
+    float comm_mb[NMAX];
+    float inv_link, ipc_ms;
     const float4 *tab;                       // [n][nS][nQ] (dur, thr, bw, 0)
     const int *Q, *S;                        // grids
 };

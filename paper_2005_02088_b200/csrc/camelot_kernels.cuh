@@ -137,6 +137,8 @@ __device__ void filter_body(const DevProb &P, const FilterArgs &F, int b, Filter
             float ls = 0.0f;
             for (int k2 = P.first_of_app[a]; k2 <= P.last_of_app[a]; ++k2) {
                 const float t = (k2 == i) ? dur : mindur[k2];
+                if (k2 > P.first_of_app[a] && (P.flags & F_COMM))   // hand-over lower bound (R29)
+                    ls = __fadd_rn(ls, fminf(P.ipc_ms, __fmul_rn(__fmul_rn(P.comm_mb[k2 - 1], (float)P.S[b]), P.inv_link)));
                 ls = (k2 == P.first_of_app[a]) ? t : __fadd_rn(ls, t);
             }
             bool k = ls <= P.qos[a];
@@ -383,6 +385,7 @@ __global__ void plan_kernel(const DevProb P, int policy, int nlev, const Slot *w
         pl.stage_latency_ms[i] = s.L[i];
         pl.stage_throughput_qps[i] = s.Ti[i];
         pl.kappa[i] = s.kappa[i];
+        pl.comm_ms[i] = s.comm[i];
         for (int r = 0; r < CAMELOT_MAX_REPLICAS && r < SCORE_RMAX; ++r)
             pl.gpu_of_instance[i * CAMELOT_MAX_REPLICAS + r] = s.goi[i * SCORE_RMAX + r];
     }
@@ -540,6 +543,7 @@ __global__ void predict_kernel(const DevProb P, unsigned long long x, const floa
         pl.stage_latency_ms[i] = s.L[i];
         pl.stage_throughput_qps[i] = s.Ti[i];
         pl.kappa[i] = s.kappa[i];
+        pl.comm_ms[i] = s.comm[i];
         for (int r = 0; r < CAMELOT_MAX_REPLICAS && r < SCORE_RMAX; ++r)
             pl.gpu_of_instance[i * CAMELOT_MAX_REPLICAS + r] = s.goi[i * SCORE_RMAX + r];
     }

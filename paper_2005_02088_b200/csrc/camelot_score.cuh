@@ -20,6 +20,7 @@ struct FullScore {
     float Tmin[AMAX], Lsum[AMAX];
     float L[NMAX], Ti[NMAX], kappa[NMAX];
     int8_t goi[NMAX * SCORE_RMAX];
+    float comm[NMAX];      // COMM: hand-over time of edge i -> i+1 (ms)
 };
 
 __device__ inline void decode_index(const DevProb &P, unsigned long long x, int *beta, int *rho, int *theta) {
@@ -74,6 +75,8 @@ __device__ void score_digits(const DevProb &P, const int *beta, const int *rho, 
     for (int k = 0; k < NMAX * SCORE_RMAX; ++k) out.goi[k] = -1;
     out.U = U;
     float kmax[NMAX];
+    uint32_t out_hmask[NMAX];
+    for (int i = 0; i < NMAX; ++i) out_hmask[i] = 0u;
     uint32_t pv = 0;
     int u = 0;
     if (P.flags & F_PAPER_GLOBAL) {
@@ -171,6 +174,7 @@ __device__ void score_digits(const DevProb &P, const int *beta, const int *rho, 
                 for (int g = 0; g < C; ++g)
                     if (hmask[i] >> g & 1u) dm = fmaxf(dm, dem[g]);
                 kmax[i] = kappa_of(dm, bwv[i], P.gamma[i], P.invBW, P.flags);
+                out_hmask[i] = hmask[i];
             }
         } else {
             for (int i = 0; i < n; ++i) kmax[i] = 1.0f;
@@ -183,6 +187,17 @@ __device__ void score_digits(const DevProb &P, const int *beta, const int *rho, 
         out.L[i] = __fmul_rn(dur[i], kmax[i]);
         out.Ti[i] = __fdiv_rn(__fmul_rn((float)(rho[i] + 1), thr[i]), kmax[i]);
     }
+    // COMM (R29): hand-over of edge i -> i+1 = ipc when both stages run entirely on
+    // one and the same GPU, else the host-staged copy of the batch's data
+    for (int i = 0; i < NMAX; ++i) out.comm[i] = 0.0f;
+    if ((P.flags & F_COMM) && !pv && !(P.flags & F_PAPER_GLOBAL)) {
+        for (int i = 0; i + 1 < n; ++i) {
+            if (P.app[i] != P.app[i + 1]) continue;
+            const bool local = out_hmask[i] == out_hmask[i + 1] && __popc(out_hmask[i]) == 1;
+            out.comm[i] = local ? P.ipc_ms
+                                : __fmul_rn(__fmul_rn(P.comm_mb[i], (float)P.S[beta[P.app[i]]]), P.inv_link);
+        }
+    }
     bool qos_fail = false;
     float T = 0.0f;
     for (int a = 0; a < P.A; ++a) {
@@ -192,6 +207,7 @@ __device__ void score_digits(const DevProb &P, const int *beta, const int *rho, 
                 ls = out.L[i];
                 tm = out.Ti[i];
             } else {
+                if (P.flags & F_COMM) ls = __fadd_rn(ls, out.comm[i - 1]);
                 ls = __fadd_rn(ls, out.L[i]);
                 tm = fminf(tm, out.Ti[i]);
             }

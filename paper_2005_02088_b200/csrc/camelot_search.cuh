@@ -435,6 +435,7 @@ struct PCtx {
     float dmax[NS], dur[NS], bw[NS], nt[NS];   // i < j: placed stage; i > j: dur = min duration
     float tub, restT;
     float lpre;                     // ordered fp32 sum of current L of placed stages of app(j) (-1: none)
+    float tx[NS];                   // COMM: cross-GPU hand-over time of edge i -> i+1 (at its app's batch)
     float lother;                   // lower bound of the other application's latency sum (A = 2)
     int u, U, rqsum, restU, bc;
     unsigned long long x;
@@ -516,6 +517,14 @@ __device__ __forceinline__ void load_ctx(const DevProb &P, const SearchArgs &S, 
             }
         c.lpre = lp;
         c.lother = lo_started ? lo : 0.0f;
+    }
+    if (P.flags & F_COMM) {
+#pragma unroll
+        for (int i = 0; i < NS; ++i) {
+            c.tx[i] = 0.0f;
+            if (i + 1 < P.n && P.app[i] == P.app[i + 1])
+                c.tx[i] = __fmul_rn(__fmul_rn(P.comm_mb[i], (float)P.S[nd.b[P.app[i]]]), P.inv_link);
+        }
     }
     c.u = nd.u;
     c.U = nd.U;
@@ -614,9 +623,28 @@ __device__ __forceinline__ void fast_eval(const DevProb &P, const PCtx<CM, NS> &
     }
     fe.u = c.u + unew;
     float l0 = 0.0f, l1 = 0.0f;
+    // COMM (R29): positions hosting stage j; an edge whose both stages are placed has
+    // its exact hand-over time, otherwise its lower bound min(ipc, cross)
+    const bool comm = (P.flags & F_COMM) != 0;
+    unsigned jm = 0u;
+    if (comm) {
+#pragma unroll
+        for (int q = 0; q < CM; ++q) jm |= (kk[q] > 0 ? 1u : 0u) << q;
+    }
 #pragma unroll
     for (int i = 0; i < NS; ++i) {
         if (i < P.n) {
+            if (comm && i > 0 && P.app[i - 1] == P.app[i]) {
+                float t;
+                if (i <= j) {   // both i-1 and i placed
+                    const unsigned mp = c.hp[i - 1], mi = (i == j) ? jm : c.hp[i];
+                    t = (mp == mi && __popc(mi) == 1) ? P.ipc_ms : c.tx[i - 1];
+                } else {
+                    t = fminf(P.ipc_ms, c.tx[i - 1]);
+                }
+                if (P.app[i] == 0) l0 = __fadd_rn(l0, t);
+                else l1 = __fadd_rn(l1, t);
+            }
             float L;
             if (i < j) {
                 const float k = kappa_of(dm[i], c.bw[i], P.gamma[i], P.invBW, P.flags);
@@ -1079,7 +1107,7 @@ __device__ __forceinline__ void thread_chunk(const DevProb &P, const SearchArgs 
                 if (go && leaf && POLICY == 0) go = kl < bk || (kl == bk && x < bx);   // the lane's own best
                 if (go && !leaf && c.rqsum - (int)r.NP < c.restU) go = false;
             }
-            if (go) {
+            if (go && !(P.flags & F_COMM)) {
                 const int aj = P.app[j];
                 float lb = c.lpre < 0.0f ? r.dur : __fadd_rn(c.lpre, r.dur);
 #pragma unroll
@@ -1446,7 +1474,7 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
                 }
                 // QoS lower bound before placement: L_j >= dur, placed stages' L
                 // only grow, unplaced stages >= their minimum duration (ordered sum)
-                if (S.prune && go) {
+                if (S.prune && go && !(P.flags & F_COMM)) {
                     const int aj = P.app[j];
                     float lb = c.lpre < 0.0f ? r.dur : __fadd_rn(c.lpre, r.dur);
 #pragma unroll

@@ -147,7 +147,7 @@ __device__ __forceinline__ float sw_kappa(float dmax, float bw, float gamma, flo
 }
 
 // cold paths of the leaf loop, out of line (instruction-cache footprint)
-__device__ __noinline__ uint32_t sw_fail_bits(const DevProb &P, int p, float bw, int minrq, int maxcnt, uint32_t need,
+static __device__ __noinline__ uint32_t sw_fail_bits(const DevProb &P, int p, float bw, int minrq, int maxcnt, uint32_t need,
                                               uint32_t minrm, float maxdem, bool cap) {
     // first-failing dimensions of a failed deployment: OR over GPUs of fits(g, 1) failures
     uint32_t v = 0;
@@ -192,7 +192,7 @@ __device__ __forceinline__ void sw_better(unsigned long long key, unsigned long 
 }
 
 // The sweep.  NS == n exactly (stage loops carry no runtime guards) unless n > 6.
-template <int CM, int NS, int POLICY, bool TWO>
+template <int CM, int NS, int POLICY, bool TWO, bool COMM>
 __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const DevProb P, const SweepArgs A) {
     static_assert(CM <= 8, "thermometer code holds 8 GPUs x 4 bits");
     __shared__ float dem_s[CM][SWEEP_THREADS];
@@ -307,6 +307,17 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
         const int bL = beta[P.app[jl]];
         const uint32_t WL = P.W[jl], AsL = P.Am[jl] * (uint32_t)P.S[bL];
         const float gL = cont ? P.gamma[jl] : 0.0f;
+        // COMM (R29): hand-over times of the edges between placed stages (exact), and the
+        // cross-GPU time of the edge into the leaf stage (local or not is decided per leaf)
+        float te[NS];
+#pragma unroll
+        for (int i = 0; i < NS; ++i) {
+            te[i] = 0.0f;
+            if (COMM && i + 1 < n && P.app[i] == P.app[i + 1]) {
+                const float tx = __fmul_rn(__fmul_rn(P.comm_mb[i], (float)P.S[beta[P.app[i]]]), P.inv_link);
+                te[i] = (i + 1 < jl && st.hm[i] == st.hm[i + 1] && __popc(st.hm[i]) == 1) ? P.ipc_ms : tx;
+            }
+        }
         int kim[CM], sh[CM];
         float hb[CM];      // bandwidth threshold: fits(k) <=> fl(k bw) <= hb
         uint32_t perm = 0u, E = 0u;
@@ -420,6 +431,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
                 for (int i = 0; i < NS; ++i) dmx[i] = st.dm[i];
                 float dl = 0.0f;
                 int du = 0;
+                uint32_t lm = 0u;   // GPUs receiving the leaf stage (COMM)
                 uint32_t mm = mN ? (mN & (0u - mN)) : (M & 0x11111111u);
                 int rem = N;
                 do {
@@ -431,6 +443,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
                     const float d = __fadd_rn(dem_s[g][tid], __fmul_rn((float)k, bw));
                     dl = fmaxf(dl, d);
                     du += (E >> g) & 1u;
+                    if (COMM) lm |= 1u << g;
 #pragma unroll
                     for (int i = 0; i < NS; ++i)
                         if (i < jl && ((st.hm[i] >> g) & 1u)) dmx[i] = fmaxf(dmx[i], d);
@@ -441,6 +454,12 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
 #pragma unroll
                 for (int i = 0; i < NS; ++i) {
                     if (i < n) {
+                        if (COMM && i > 0 && P.app[i - 1] == P.app[i]) {   // hand-over before stage i
+                            const float t = (i == jl) ? ((st.hm[jl - 1] == lm && __popc(lm) == 1) ? P.ipc_ms : te[jl - 1])
+                                                      : te[i - 1];
+                            if (!TWO || i < f1) l0 = __fadd_rn(l0, t);
+                            else l1 = __fadd_rn(l1, t);
+                        }
                         const float k = (i == jl) ? sw_kappa(dl, bw, gL, P.invBW)
                                                   : sw_kappa(dmx[i], bwv[i], gam[i], P.invBW);
                         kap[i] = k;

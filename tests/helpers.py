@@ -6,7 +6,7 @@ G = GP
 
 FLAG = {"NO_BW_CAP": G.F_NO_BW_CAP, "NO_CONTENTION": G.F_NO_CONTENTION, "SAT": G.F_SAT,
         "PAPER_GLOBAL": G.F_PAPER_GLOBAL, "EQ2_BUDGET": G.F_EQ2_BUDGET,
-        "NO_FILTER": G.F_NO_FILTER}
+        "NO_FILTER": G.F_NO_FILTER, "COMM": G.F_COMM}
 
 
 def flags_of(spec):
