@@ -34,6 +34,24 @@ WORKLOAD = "C4: 5-stage p1-c2-m2-c3-m1 pipeline, 8 modeled V100 (BW 897 GB/s), 1
 LOW_LOAD = 0.3   # low load = 30% of the peak
 
 
+def ncu_traffic(name):
+    """dram__bytes_read.sum + dram__bytes_write.sum summed over the launches of a
+    committed ncu --page raw --csv capture under profiles/ (None if absent)."""
+    import csv
+    path = os.path.join(ROOT, "profiles", name)
+    try:
+        rows = list(csv.reader(open(path)))
+        hdr, units, data = rows[0], rows[1], rows[2:]
+        tot = 0.0
+        for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            i = hdr.index(key)
+            scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(units[i], 1.0)
+            tot += sum(float(r[i]) * scale for r in data if r[i] not in ("", "n/a"))
+        return tot, "profiles/" + name
+    except (OSError, ValueError, IndexError):
+        return None, None
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -135,6 +153,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-flat", action="store_true", help="skip the flat-scan roofline leg")
     ap.add_argument("--no-sa", action="store_true", help="skip the simulated-annealing baseline")
+    ap.add_argument("--no-comm", action="store_true", help="skip the NEXT-2 communication-aware leg")
     ap.add_argument("--sa-chains", type=int, default=4096)
     ap.add_argument("--sa-iters", type=int, default=500)
     ap.add_argument("--flat-config", type=int, default=4, help="config of the flat scan (4 = C4)")
@@ -268,8 +287,12 @@ def main():
     k_ns = sum(s1["t_ns"] + s2["t_ns"] for s1, s2 in kt) / args.steps
     achieved = ops_per_eval * evals / (k_ns * 1e-9) / 1e12 if k_ns else None
     peak = n_sm * 4 * 32 * sm_max * 1e6 / 1e12          # lane-instructions/s (issue bound)
+    traffic, traffic_src = ncu_traffic("r01_v6_ncu_search_raw.csv")
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s",
-            "frac": (achieved / peak) if achieved else None, "traffic": None,
+            "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+            "traffic_note": f"DRAM bytes read+written per step (sum over the search-level launches of one step) "
+                            f"from the committed ncu --set full capture {traffic_src}; algorithmic bytes ~0 "
+                            f"(64 KB of tables, L2/SMEM resident)" if traffic else None,
             "kernel": "search_kernel + filter (incumbent cascade and main pass, both policies)",
             "ops_per_eval": ops_per_eval, "evals_per_step": evals,
             "kernel_ms_per_step": k_ns / 1e6,
@@ -331,6 +354,30 @@ def main():
                                "same_plan_as_exact": r2.index == pr.index},
               "note": "PAPER.md L880-888 solver, reading R13; chains bit-identical to the oracle SA"}
 
+    # NEXT-2 on the same workload: the communication-aware QoS (flag COMM, R29) with
+    # the generator's hand-over sizes; both policies, exact, time of the step
+    comm = None
+    if not args.no_comm and rank == 0:
+        cp = G.with_comm(prob, 4)
+        cs = api.Session(cp, device=local, n_loads=1)
+        cts = []
+        for rep in range(4):
+            torch.cuda.synchronize()
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record()
+            c1 = cs.plan_max_load()
+            c2 = cs.plan_min_resource([[LOW_LOAD * c1.objective] * cp.n_apps])[0]
+            ev1.record()
+            torch.cuda.synchronize()
+            if rep:
+                cts.append(ev0.elapsed_time(ev1))
+        comm = {"ms_both_policies": statistics.median(cts), "link_gbs": cp.cluster.link_gbs,
+                "ipc_ms": cp.cluster.ipc_ms,
+                "max_load": {"index": c1.index, "T": c1.objective, "comm_ms": c1.comm_ms,
+                             "e2e_latency_ms": c1.e2e_latency_ms, "same_plan_as_paper_qos": c1.index == pm.index},
+                "min_resource": {"index": c2.index, "gpus_used": c2.gpus_used, "quota_used": c2.quota_used},
+                "note": "NEXT-2, reading R29/R30: hand-over times in Constraint-5's ordered sum"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         r = cpu_reference_leg(prob, args, rank, world, as_main=False)
@@ -350,7 +397,7 @@ def main():
                           "min_resource": {"index": pr.index, "gpus_used": pr.gpus_used,
                                            "quota_used": pr.quota_used, "load": LOW_LOAD * pm.objective}},
                 "scored_per_step": evals, "gpu_launches": launches, "roofline": roof, "flat_scan": flat,
-                "sa_baseline": sa,
+                "sa_baseline": sa, "comm_qos": comm,
                 "clocks": clocks,
                 "e2e": e2e, "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)
