@@ -275,6 +275,24 @@ def test_sharded_equals_single(api, oracle, cfg, world):
         assert pl.index == single.index and fb(pl.objective) == fb(single.objective)
 
 
+@pytest.mark.parametrize("cfg,world", [(2, 2), (3, 3), (6, 2), (4, 3)])
+def test_sharded_flat_equals_single(api, oracle, cfg, world):
+    """The same with NO_FILTER (the leaf sweep: chunk ownership per parent; for
+    C4, Ntot > 2^32, so the winning chunk is re-scanned by the tree search)."""
+    prob = G.config_problems(cfg)[0]
+    flags = prob.flags | G.F_NO_FILTER
+    lo, hi = (0, 0) if cfg != 4 else (10 ** 12, 10 ** 12 + (1 << 27))
+    single = api.Session(prob, flags=flags).plan_max_load(lo=lo, hi=hi)
+    keys = []
+    sess = [api.Session(prob, flags=flags) for _ in range(world)]
+    for r in range(world):
+        keys.append(sess[r].search_local(0, rank=r, world=world, lo=lo, hi=hi).clone())
+    red = torch.stack(keys).min(dim=0).values
+    for r in range(world):
+        pl = sess[r].finalize(0, red, rank=r, world=world, lo=lo, hi=hi)[0]
+        assert pl.index == single.index and fb(pl.objective) == fb(single.objective)
+
+
 def test_repeatable(api):
     prob = G.config_problems(3)[0]
     s = api.Session(prob)
