@@ -81,7 +81,7 @@ struct DevHeader {
     unsigned long long best_packed;      // (objective key << 32) | (index >> xshift), atomicMin (1 level)
     unsigned long long head[NMAX + 1];   // pop counter of pass j
     unsigned long long tail[NMAX + 1];   // size of the frontier at depth j (may exceed capacity)
-    unsigned long long dbg_batches[NMAX + 1], dbg_maxb[NMAX + 1], dbg_tend[NMAX + 1];   // profiling (CAMELOT_FTRACE)
+    unsigned long long dbg_batches[NMAX + 1], dbg_maxb[NMAX + 1], dbg_tend[NMAX + 1], dbg_tc[NMAX + 1][4];   // profiling (CAMELOT_FTRACE)
     // cumulative over the incumbent cascade + main search of one call (not reset per pass)
     unsigned long long cum_scored, cum_nodes;
     // phase trace of the last search (camelot_trace): block 0 of every search-level

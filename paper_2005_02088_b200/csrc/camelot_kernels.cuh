@@ -689,6 +689,9 @@ search_level_kernel(const DevProb P, const LevelArgs LA) {
             trace_value(hdr, 64 + j, j == 0 ? (unsigned long long)P.nbc : hdr->tail[j]);   // parents of pass j
             trace_value(hdr, 80 + j, hdr->dbg_batches[j]);
             trace_value(hdr, 96 + j, hdr->dbg_maxb[j]);
+            if (hdr->dbg_tc[j][3]) {   // thread-per-parent chunk of block 0 warp 0: ctx / children / emission ns, parents
+                for (int q = 0; q < 4; ++q) trace_value(hdr, 120 + q, hdr->dbg_tc[j][q]);
+            }
 #endif
         }
     }

@@ -1056,6 +1056,11 @@ __device__ __forceinline__ void thread_chunk(const DevProb &P, const SearchArgs 
     const unsigned long long span = P.opow[n - 1 - j];
     unsigned long long bk = wb->key[0], bx = wb->x[0];   // lane-local best (leaf passes: one level)
     const bool mine = (live >> lane) & 1u;
+#ifdef CAMELOT_FTRACE
+    const bool tme = lane == 0;
+    unsigned long long tt[4] = {0, 0, 0, 0};
+    if (tme) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt[0]));
+#endif
     {
         // dead lanes view node e0 (valid memory) and have no children
         const NodeSoA<CM> nd(in, e0 + (mine ? lane : 0));
@@ -1075,6 +1080,9 @@ __device__ __forceinline__ void thread_chunk(const DevProb &P, const SearchArgs 
         }
         const int cnt = go_node ? (int)sb_at(P, S, j, bj).cnt : 0;
         const OptRec *list = S.rec + ((size_t)j * P.nS + bj) * P.O;
+#ifdef CAMELOT_FTRACE
+        if (tme) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt[1]));
+#endif
         unsigned smask = 0u;   // surviving children of this lane's parent (inner passes)
         const int cntw = __reduce_max_sync(0xffffffffu, cnt);
         for (int k = 0; k < cntw; ++k) {
@@ -1190,6 +1198,10 @@ __device__ __forceinline__ void thread_chunk(const DevProb &P, const SearchArgs 
             if (sv && j + 1 == S.d0) sv = owns_child<CM>(P, S, nd, j, k);
             if (sv) smask |= 1u << k;   // emitted after the loop (cnt <= 32)
         }
+#ifdef CAMELOT_FTRACE
+        __syncwarp();
+        if (tme) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt[2]));
+#endif
         // emission rounds: every lane emits its next survivor in the same round, with
         // warp-aggregated consecutive slots (coalesced structure-of-arrays stores;
         // capacity checked by the caller)
@@ -1221,6 +1233,15 @@ __device__ __forceinline__ void thread_chunk(const DevProb &P, const SearchArgs 
         }
     }
     __syncwarp();
+#ifdef CAMELOT_FTRACE
+    if (tme) {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt[3]));
+        atomicMax(&S.hdr->dbg_tc[j][0], tt[1] - tt[0]);   // max over chunks of each phase
+        atomicMax(&S.hdr->dbg_tc[j][1], tt[2] - tt[1]);
+        atomicMax(&S.hdr->dbg_tc[j][2], tt[3] - tt[2]);
+        atomicAdd(&S.hdr->dbg_tc[j][3], 1ull);
+    }
+#endif
     if (leaf) {   // merge the lanes' bests (converged)
         const bool imp = bk < 0xFFFFFFFFull && slot_less(bk, bx, wb->key[0], wb->x[0]);
         warp_improve(wb, 0, imp, bk, bx, lane);

@@ -26,6 +26,9 @@ def show(tag, tr, st):
         elif 48 <= t < 64:
             line.append(f"fin{t - 48}={(ns - prev)/1e3:.1f}")
             continue
+        elif t >= 120:
+            line.append(f"tc{t - 120}={ns / 1e3 if t < 123 else ns:.1f}")
+            continue
         elif t >= 112:
             line.append(f"w{t - 112}={ns/1e3:.1f}")
             continue
