@@ -200,7 +200,7 @@ def build_problem(name: str, apps: Sequence[Sequence[str]], n_gpus: int,
         bw_sensitivity=np.asarray(gamma, dtype=np.float32),
         cluster=cl, flags=flags,
         meta=dict(stages=[st["kind"] for st in stages], seed=seed, rho=qos_rho,
-                  preset=preset),
+                  preset=preset, params=[{k: st[k] for k in ("tc", "tm", "alpha", "o")} for st in stages]),
     )
 
 

@@ -270,6 +270,35 @@ int camelot_last_stats(const camelot_exec *exec, uint64_t *out8);
  * at most 256 are kept) or a negative status. */
 int camelot_trace(const camelot_exec *exec, uint64_t *out, int cap);
 
+/* NEXT-3: the paper's decision-tree performance models (one
+ * regression tree per microservice and target, features batch size s and SM
+ * quota p; trained offline, L706).  Flattened tree: node k is a leaf when
+ * feature[k] < 0 (prediction value[k]); otherwise x = (feature[k] == 0 ? s : p)
+ * goes to left[k] when x <= threshold[k], else to right[k]; child indices must
+ * be larger than their parent's (so every walk ends within n_nodes steps). */
+typedef struct {
+    int32_t n_nodes;          /* >= 1                                                */
+    const int32_t *feature;   /* [n_nodes] 0 = batch size, 1 = SM quota (%), -1 = leaf */
+    const int32_t *threshold; /* [n_nodes]                                           */
+    const int32_t *left;      /* [n_nodes] child index (internal nodes)              */
+    const int32_t *right;     /* [n_nodes]                                           */
+    const float *value;       /* [n_nodes] leaf prediction                           */
+} camelot_tree;
+
+/* Workspace bytes camelot_tables_from_trees needs (0 on invalid arguments). */
+size_t camelot_trees_workspace_bytes(int n_trees, const camelot_tree *trees, int n_batch, int n_quota);
+
+/* Build the predictor table of a problem on the device from its trees: for every
+ * stage i, trees[3i + c] (c = 0 duration ms, 1 throughput QPS, 2 bandwidth GB/s)
+ * are evaluated at every (batch[b], quota_pct[q]) grid point -- any grid, not
+ * only the profiling one -- into d_table[i][b][q][c] (float, [n][nS][nQ][4],
+ * component 3 = 0), a DEVICE pointer owned by the caller.  Host inputs are
+ * copied into exec->workspace (>= camelot_trees_workspace_bytes).  Asynchronous
+ * on exec->stream.  EINVAL: malformed tree (feature not in {-1,0,1}, child index
+ * not in (k, n_nodes)), empty grid, null pointers. */
+int camelot_tables_from_trees(int n_stages, const camelot_tree *trees, int n_batch, const int32_t *batch,
+                              int n_quota, const int32_t *quota_pct, const camelot_exec *exec, float *d_table);
+
 /* Process-wide number of kernels launched by this library so far. */
 uint64_t camelot_kernel_launches(void);
 

@@ -750,3 +750,21 @@ int oc_sa(const oc_problem *P, int policy, const float *load, uint64_t seed, int
     return 0;
 }
 int oc_sizeof_sa(void) { return (int)sizeof(oc_sa_chain_t); }
+
+/* ---------------------------------------------------------------- NEXT-3
+ * The paper's decision-tree performance model: one
+ * regression tree per microservice and target (duration, throughput,
+ * bandwidth) over the features batch size s and SM quota p.  Node k is a leaf
+ * when feature[k] < 0; otherwise x = (feature[k] == 0 ? s : p) goes left when
+ * x <= threshold[k].  Plain traversal; NaN for a malformed tree. */
+float oc_tree_eval(const int32_t *feature, const int32_t *threshold, const int32_t *left,
+                   const int32_t *right, const float *value, int32_t n_nodes, int32_t s, int32_t p) {
+    int32_t k = 0;
+    for (int32_t step = 0; step <= n_nodes; step++) {
+        if (k < 0 || k >= n_nodes) break;
+        if (feature[k] < 0) return value[k];
+        const int32_t x = feature[k] == 0 ? s : p;
+        k = x <= threshold[k] ? left[k] : right[k];
+    }
+    return NAN;
+}

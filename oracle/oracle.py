@@ -295,3 +295,27 @@ def sa(prob, policy: str = "max_load", load=None, seed: int = 1, chain_lo: int =
         raise ValueError(f"oracle sa rc={rc}")
     return [(None if r.best_index == NONE else int(r.best_index), int(r.best_key), int(r.accepted),
              int(r.final_index)) for r in out]
+
+
+# ---------------------------------------------------------------------- NEXT-3
+def tree_eval(tree, s: int, p: int) -> float:
+    """oc_tree_eval: one decision-tree prediction at batch s, quota p."""
+    f = lib().oc_tree_eval
+    f.restype = C.c_float
+    a = [np.ascontiguousarray(v) for v in (tree.feature, tree.threshold, tree.left, tree.right)]
+    v = np.ascontiguousarray(tree.value, np.float32)
+    ip = lambda x: x.ctypes.data_as(C.POINTER(C.c_int32))
+    return float(f(ip(a[0]), ip(a[1]), ip(a[2]), ip(a[3]), v.ctypes.data_as(C.POINTER(C.c_float)),
+                   C.c_int32(tree.n_nodes), C.c_int32(int(s)), C.c_int32(int(p))))
+
+
+def tree_tables(trees, batch, quota) -> np.ndarray:
+    """The predictor table [n][nS][nQ][4] = (dur, thr, bw, 0) from 3 trees per stage
+    (component order), evaluated point by point."""
+    n = len(trees) // 3
+    tab = np.zeros((n, len(batch), len(quota), 4), np.float32)
+    for t, tree in enumerate(trees):
+        for b, s in enumerate(batch):
+            for q, p in enumerate(quota):
+                tab[t // 3, b, q, t % 3] = tree_eval(tree, s, p)
+    return tab

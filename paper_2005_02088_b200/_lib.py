@@ -117,10 +117,16 @@ class Plan(C.Structure):
                 ("comm_ms", C.c_float * MAX_STAGES)]
 
 
+class Tree(C.Structure):
+    _fields_ = [("n_nodes", C.c_int32), ("feature", C.POINTER(C.c_int32)), ("threshold", C.POINTER(C.c_int32)),
+                ("left", C.POINTER(C.c_int32)), ("right", C.POINTER(C.c_int32)), ("value", C.POINTER(C.c_float))]
+
+
 EXPORTS = ["camelot_last_error", "camelot_version", "camelot_workspace_bytes", "camelot_upload",
            "camelot_plan_max_load", "camelot_plan_min_resource", "camelot_predict",
            "camelot_score_range", "camelot_search_local", "camelot_finalize", "camelot_last_stats",
-           "camelot_kernel_launches", "camelot_sa", "camelot_trace"]
+           "camelot_kernel_launches", "camelot_sa", "camelot_trace",
+           "camelot_trees_workspace_bytes", "camelot_tables_from_trees"]
 
 _lib = None
 
@@ -155,6 +161,10 @@ def lib():
         L.camelot_finalize.argtypes = [P, Cl, C.c_int, fp, C.c_int, C.c_void_p, E, Pl]
         L.camelot_last_stats.argtypes = [E, C.POINTER(C.c_uint64)]
         L.camelot_trace.argtypes = [E, C.POINTER(C.c_uint64), C.c_int]
+        L.camelot_trees_workspace_bytes.restype = C.c_size_t
+        L.camelot_trees_workspace_bytes.argtypes = [C.c_int, C.POINTER(Tree), C.c_int, C.c_int]
+        L.camelot_tables_from_trees.argtypes = [C.c_int, C.POINTER(Tree), C.c_int, C.POINTER(C.c_int32), C.c_int,
+                                                C.POINTER(C.c_int32), E, C.c_void_p]
         L.camelot_kernel_launches.restype = C.c_uint64
         L.camelot_sa.argtypes = [P, Cl, C.c_int, fp, C.c_uint64, C.c_int, C.c_int, C.c_float, C.c_float, E, Pl,
                                  C.c_void_p, C.c_void_p]

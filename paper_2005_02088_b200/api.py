@@ -267,6 +267,35 @@ class Session:
 
 
 # ---------------------------------------------------------------------- functional API
+def tables_from_trees(trees, batch, quota_pct, device: Optional[int] = None) -> torch.Tensor:
+    """NEXT-3: the predictor table [n][nS][nQ][4] of a problem built ON THE DEVICE
+    from its decision-tree models (3 per stage: duration, throughput, bandwidth;
+    gen.dt.Tree-like objects) evaluated at every (batch, quota) grid point."""
+    L.lib()
+    dev = torch.cuda.current_device() if device is None else device
+    keep = []
+    arr = (L.Tree * len(trees))()
+    for t, tr in enumerate(trees):
+        f, th, le, ri = (np.ascontiguousarray(a, np.int32) for a in (tr.feature, tr.threshold, tr.left, tr.right))
+        v = np.ascontiguousarray(tr.value, np.float32)
+        keep += [f, th, le, ri, v]
+        ip = lambda a: a.ctypes.data_as(C.POINTER(C.c_int32))
+        arr[t] = L.Tree(int(f.shape[0]), ip(f), ip(th), ip(le), ip(ri), v.ctypes.data_as(C.POINTER(C.c_float)))
+    S = np.ascontiguousarray(batch, np.int32)
+    Q = np.ascontiguousarray(quota_pct, np.int32)
+    nb = L.lib().camelot_trees_workspace_bytes(len(trees), arr, len(S), len(Q))
+    if nb == 0:
+        raise L.CamelotError(L.EINVAL, L.lib().camelot_last_error().decode())
+    ws = torch.empty(nb, dtype=torch.uint8, device=f"cuda:{dev}")
+    out = torch.empty((len(trees) // 3, len(S), len(Q), 4), dtype=torch.float32, device=f"cuda:{dev}")
+    ex = L.Exec(device=dev, stream=torch.cuda.current_stream(dev).cuda_stream, rank=0, world=1, index_lo=0,
+                index_hi=0, workspace=ws.data_ptr(), workspace_bytes=nb, exec_flags=0)
+    L.check(L.lib().camelot_tables_from_trees(len(trees) // 3, arr, len(S), S.ctypes.data_as(C.POINTER(C.c_int32)),
+                                              len(Q), Q.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(ex),
+                                              out.data_ptr()), False)
+    return out
+
+
 def plan_max_load(problem, **kw) -> PlanResult:
     return Session(problem, device=kw.pop("device", None)).plan_max_load(**kw)
 

@@ -1105,6 +1105,78 @@ int camelot_last_stats(const camelot_exec *ex, uint64_t *out8) {
     return CAMELOT_OK;
 }
 
+static int check_trees(int n_trees, const camelot_tree *trees, size_t &nodes) {
+    nodes = 0;
+    if (!trees || n_trees < 1) return fail(CAMELOT_EINVAL, "no trees");
+    for (int t = 0; t < n_trees; ++t) {
+        const camelot_tree &T = trees[t];
+        if (T.n_nodes < 1 || !T.feature || !T.threshold || !T.left || !T.right || !T.value)
+            return fail(CAMELOT_EINVAL, "tree %d: empty or null arrays", t);
+        for (int k = 0; k < T.n_nodes; ++k) {
+            const int f = T.feature[k];
+            if (f < -1 || f > 1) return fail(CAMELOT_EINVAL, "tree %d node %d: feature must be -1, 0 or 1", t, k);
+            if (f >= 0 && (T.left[k] <= k || T.left[k] >= T.n_nodes || T.right[k] <= k || T.right[k] >= T.n_nodes))
+                return fail(CAMELOT_EINVAL, "tree %d node %d: children must lie in (k, n_nodes)", t, k);
+            if (f < 0 && !std::isfinite(T.value[k])) return fail(CAMELOT_EINVAL, "tree %d node %d: non-finite leaf", t, k);
+        }
+        nodes += (size_t)T.n_nodes;
+    }
+    return CAMELOT_OK;
+}
+
+size_t camelot_trees_workspace_bytes(int n_trees, const camelot_tree *trees, int n_batch, int n_quota) {
+    size_t nodes = 0;
+    if (check_trees(n_trees, trees, nodes) || n_batch < 1 || n_quota < 1) return 0;
+    return al(nodes * sizeof(int4)) + al(nodes * sizeof(float)) + al((n_trees + 1) * sizeof(int)) +
+           al(n_batch * sizeof(int)) + al(n_quota * sizeof(int));
+}
+
+int camelot_tables_from_trees(int n_stages, const camelot_tree *trees, int n_batch, const int32_t *batch,
+                              int n_quota, const int32_t *quota_pct, const camelot_exec *ex, float *d_table) {
+    t_call_launches = 0;
+    if (n_stages < 1 || n_stages > CAMELOT_MAX_STAGES) return fail(CAMELOT_EINVAL, "n_stages must be in 1..8");
+    if (!batch || !quota_pct || !d_table || n_batch < 1 || n_quota < 1) return fail(CAMELOT_EINVAL, "empty grid or null");
+    const int n_trees = 3 * n_stages;
+    size_t nodes = 0;
+    int rc = check_trees(n_trees, trees, nodes);
+    if (rc) return rc;
+    rc = device_ok(ex);
+    if (rc) return rc;
+    const size_t need = camelot_trees_workspace_bytes(n_trees, trees, n_batch, n_quota);
+    if (ex->workspace_bytes < need) return fail(CAMELOT_ENOMEM, "workspace too small: %zu < %zu bytes", ex->workspace_bytes, need);
+    std::vector<int4> hn(nodes);
+    std::vector<float> hv(nodes);
+    std::vector<int> hoff(n_trees + 1);
+    size_t at = 0;
+    for (int t = 0; t < n_trees; ++t) {
+        hoff[t] = (int)at;
+        for (int k = 0; k < trees[t].n_nodes; ++k, ++at) {
+            hn[at] = make_int4(trees[t].feature[k], trees[t].threshold[k], trees[t].left[k], trees[t].right[k]);
+            hv[at] = trees[t].value[k];
+        }
+    }
+    hoff[n_trees] = (int)at;
+    char *ws = static_cast<char *>(ex->workspace);
+    cudaStream_t st = static_cast<cudaStream_t>(ex->stream);
+    int4 *dn = reinterpret_cast<int4 *>(ws);
+    float *dv = reinterpret_cast<float *>(ws + al(nodes * sizeof(int4)));
+    int *doff = reinterpret_cast<int *>(ws + al(nodes * sizeof(int4)) + al(nodes * sizeof(float)));
+    int *dS = reinterpret_cast<int *>(reinterpret_cast<char *>(doff) + al((n_trees + 1) * sizeof(int)));
+    int *dQ = reinterpret_cast<int *>(reinterpret_cast<char *>(dS) + al(n_batch * sizeof(int)));
+    CU(cudaMemcpyAsync(dn, hn.data(), nodes * sizeof(int4), cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(dv, hv.data(), nodes * sizeof(float), cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(doff, hoff.data(), (n_trees + 1) * sizeof(int), cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(dS, batch, n_batch * sizeof(int), cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(dQ, quota_pct, n_quota * sizeof(int), cudaMemcpyHostToDevice, st));
+    const long long total = (long long)n_trees * n_batch * n_quota;
+    const int blocks = (int)std::min<long long>((total + 255) / 256, 4096);
+    tree_table_kernel<<<blocks, 256, 0, st>>>(n_trees, dn, dv, doff, n_batch, dS, n_quota, dQ, d_table);
+    COUNT_LAUNCH();
+    CU(cudaGetLastError());
+    CU(cudaStreamSynchronize(st));   // the host staging vectors die on return
+    return CAMELOT_OK;
+}
+
 int camelot_trace(const camelot_exec *ex, uint64_t *out, int cap) {
     if (!ex || !out || cap < 0 || !ex->workspace) return fail(CAMELOT_EINVAL, "null argument");
     DevHeader h;

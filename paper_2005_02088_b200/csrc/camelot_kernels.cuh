@@ -854,3 +854,35 @@ __global__ void __launch_bounds__(256) sa_kernel(const DevProb P, const SAArgs A
 }
 
 }  // namespace cam
+
+// ============================================================================
+// NEXT-3: decision-tree performance models evaluated on
+// the device into the predictor table: one thread per (tree, batch, quota).
+namespace cam {
+
+__global__ void tree_table_kernel(int n_trees, const int4 *nodes, const float *values, const int *off,
+                                  int nS, const int *batch, int nQ, const int *quota, float *table) {
+    const long long total = (long long)n_trees * nS * nQ;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int q = (int)(t % nQ), b = (int)((t / nQ) % nS), tr = (int)(t / ((long long)nQ * nS));
+        const int s = batch[b], p = quota[q];
+        const int base = off[tr], m = off[tr + 1] - base;
+        int k = 0;
+        float v = __int_as_float(0x7fc00000);   // NaN: malformed (validated on the host)
+        for (int step = 0; step <= m; ++step) {
+            const int4 nd = nodes[base + k];
+            if (nd.x < 0) {
+                v = values[base + k];
+                break;
+            }
+            k = ((nd.x == 0 ? s : p) <= nd.y) ? nd.z : nd.w;
+        }
+        const int i = tr / 3, c = tr % 3;
+        float *cell = table + (((size_t)i * nS + b) * nQ + q) * 4;
+        cell[c] = v;
+        if (c == 0) cell[3] = 0.0f;
+    }
+}
+
+}  // namespace cam
