@@ -299,6 +299,25 @@ size_t camelot_trees_workspace_bytes(int n_trees, const camelot_tree *trees, int
 int camelot_tables_from_trees(int n_stages, const camelot_tree *trees, int n_batch, const int32_t *batch,
                               int n_quota, const int32_t *quota_pct, const camelot_exec *exec, float *d_table);
 
+/* NEXT-4: tail-latency simulation of ONE plan (reading R32; PAPER.md L527,
+ * L514, L834).  Per application: Poisson arrivals at load_qps[a] from a
+ * counter-based stream (u = ((h >> 11) + 0.5) 2^-53, h = splitmix64(splitmix64(
+ * seed ^ sim * 0xD1B54A32D192ED03) + (a << 40 | q)), gap = -log(u) 1000/load ms),
+ * batches of s_a consecutive queries released at their last arrival, stage i
+ * serving batch b on replica b mod N_i FIFO for its contended duration L_i,
+ * hand-overs under CAMELOT_F_COMM; latency = completion at the app's last stage
+ * - arrival.  n_sims independent simulations (sim = 0..n_sims-1), each
+ * discarding `warmup` queries and measuring n_queries: host out p99_ms and
+ * mean_ms [n_sims][A] (the ceil(0.99 M)-th smallest latency and the mean; -1
+ * when the plan cannot be placed).  The workspace must hold
+ * camelot_simulate_workspace_bytes().  Synchronous. */
+size_t camelot_simulate_workspace_bytes(const camelot_problem *p, const camelot_cluster *c, int64_t n_queries,
+                                        int n_sims);
+int camelot_simulate(const camelot_problem *p, const camelot_cluster *c, const int32_t *batch,
+                     const int32_t *replicas, const int32_t *quota_pct, const float *load_qps, int64_t n_queries,
+                     int64_t warmup, uint64_t seed, int n_sims, const camelot_exec *exec, double *p99_ms,
+                     double *mean_ms);
+
 /* Process-wide number of kernels launched by this library so far. */
 uint64_t camelot_kernel_launches(void);
 

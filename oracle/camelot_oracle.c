@@ -768,3 +768,86 @@ float oc_tree_eval(const int32_t *feature, const int32_t *threshold, const int32
     }
     return NAN;
 }
+
+/* ---------------------------------------------------------------- NEXT-4
+ * Tail-latency simulation of one plan (reading R32; queries are
+ * batched at the entry of an application, then flow through its microservices;
+ * L514 / L834: the 99%-ile latency is the QoS metric).  Per application a:
+ *   - Poisson arrivals at load lam[a] QPS: gap_q = -log(u_q) * 1000 / lam[a] ms,
+ *     u_q = ((h >> 11) + 0.5) * 2^-53, h = sm64(sm64(seed ^ sim * 0xD1B54A32D192ED03)
+ *     + (a << 40 | q)) (counter-based: the same stream anywhere);
+ *   - every s_a consecutive queries form a batch, released at its last arrival;
+ *   - stage i of the app serves batch b on replica b mod N_i, FIFO, for the
+ *     plan's contended duration L_i ms; then the hand-over comm_i (COMM) ms;
+ *   - latency of a query = completion of its batch at the last stage - arrival.
+ * The first `warmup` queries are discarded; p99 = the ceil(0.99 M)-th smallest
+ * of the M = n_queries measured latencies; mean = their sum / M (double,
+ * in query order).  Times are doubles. */
+static int cmp_double(const void *a, const void *b) {
+    const double x = *(const double *)a, y = *(const double *)b;
+    return (x > y) - (x < y);
+}
+
+int oc_simulate(const oc_problem *P, const int32_t *beta, const int32_t *rho, const int32_t *theta,
+                const float *lam, int64_t n_queries, int64_t warmup, uint64_t seed, uint64_t sim,
+                double *p99, double *mean) {
+    oc_score_t sc;
+    oc_score(P, beta, rho, theta, NULL, 0, &sc);
+    if (sc.place_viol) return -1;
+    if (n_queries < 1 || warmup < 0) return -2;
+    double *lat = (double *)malloc(sizeof(double) * (size_t)n_queries);
+    if (!lat) return -3;
+    for (int a = 0; a < P->A; a++) {
+        const int32_t s = P->S[beta[a]];
+        int first = -1, last = -1;
+        for (int i = 0; i < P->n; i++)
+            if (P->app[i] == a) {
+                if (first < 0) first = i;
+                last = i;
+            }
+        double freet[OC_MAX_STAGES][OC_MAX_REPL];
+        for (int i = 0; i < OC_MAX_STAGES; i++)
+            for (int r = 0; r < OC_MAX_REPL; r++) freet[i][r] = 0.0;
+        const double scale = 1000.0 / (double)lam[a];
+        const uint64_t base = sm64(seed ^ (sim * 0xD1B54A32D192ED03ull));
+        const int64_t total = warmup + n_queries;
+        const int64_t nbatch = (total + s - 1) / s;
+        double t = 0.0, sum = 0.0;
+        double arr[OC_MAX_REPL * 8 + 128];   /* arrivals of the current batch (s <= 1024) */
+        double *arrv = s <= (int32_t)(sizeof(arr) / sizeof(arr[0])) ? arr : (double *)malloc(sizeof(double) * s);
+        int64_t m = 0;
+        for (int64_t b = 0; b < nbatch; b++) {
+            for (int32_t j = 0; j < s; j++) {
+                const uint64_t q = (uint64_t)(b * s + j);
+                const uint64_t h = sm64(base + (((uint64_t)a << 40) | q));
+                const double u = ((double)(h >> 11) + 0.5) * 0x1.0p-53;
+                t = t + (-log(u)) * scale;
+                arrv[j] = t;
+            }
+            double ready = arrv[s - 1];
+            for (int i = first; i <= last; i++) {
+                const int r = (int)(b % (rho[i] + 1));
+                const double start = ready > freet[i][r] ? ready : freet[i][r];
+                const double fin = start + (double)sc.L[i];
+                freet[i][r] = fin;
+                ready = fin;
+                if (i < last && (P->flags & OC_COMM)) ready = ready + (double)sc.comm[i];
+            }
+            for (int32_t j = 0; j < s; j++) {
+                const int64_t q = b * s + j;
+                if (q < warmup || q >= total) continue;
+                const double l = ready - arrv[j];
+                lat[m++] = l;
+                sum = sum + l;
+            }
+        }
+        if (arrv != arr) free(arrv);
+        qsort(lat, (size_t)m, sizeof(double), cmp_double);
+        int64_t k = (int64_t)ceil(0.99 * (double)m) - 1;
+        if (k < 0) k = 0;
+        p99[a] = lat[k];
+        mean[a] = sum / (double)m;
+    }
+    free(lat);
+    return 0;
+}

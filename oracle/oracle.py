@@ -319,3 +319,26 @@ def tree_tables(trees, batch, quota) -> np.ndarray:
             for q, p in enumerate(quota):
                 tab[t // 3, b, q, t % 3] = tree_eval(tree, s, p)
     return tab
+
+
+# ---------------------------------------------------------------------- NEXT-4
+def simulate(prob, x: int, loads, n_queries: int = 100000, warmup: int = 10000, seed: int = 1, sim: int = 0,
+             flags=None):
+    """oc_simulate: (p99[A], mean[A]) latency (ms) of candidate x at loads[A] QPS."""
+    h = Handle(prob, flags)
+    beta, rho, theta = decode(prob, x)
+    b = (C.c_int32 * MAX_APPS)(*beta)
+    r = (C.c_int32 * MAX_STAGES)(*rho)
+    t = (C.c_int32 * MAX_STAGES)(*theta)
+    lam = (C.c_float * MAX_APPS)(*[float(v) for v in loads])
+    p99 = (C.c_double * MAX_APPS)()
+    mean = (C.c_double * MAX_APPS)()
+    f = lib().oc_simulate
+    f.argtypes = [C.POINTER(OcProblem), C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                  C.POINTER(C.c_float), C.c_int64, C.c_int64, C.c_uint64, C.c_uint64,
+                  C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    rc = f(h.ref, b, r, t, lam, n_queries, warmup, seed, sim, p99, mean)
+    if rc != 0:
+        raise ValueError(f"oc_simulate rc={rc}")
+    A = prob.n_apps
+    return list(p99[:A]), list(mean[:A])

@@ -126,7 +126,8 @@ EXPORTS = ["camelot_last_error", "camelot_version", "camelot_workspace_bytes", "
            "camelot_plan_max_load", "camelot_plan_min_resource", "camelot_predict",
            "camelot_score_range", "camelot_search_local", "camelot_finalize", "camelot_last_stats",
            "camelot_kernel_launches", "camelot_sa", "camelot_trace",
-           "camelot_trees_workspace_bytes", "camelot_tables_from_trees"]
+           "camelot_trees_workspace_bytes", "camelot_tables_from_trees", "camelot_simulate_workspace_bytes",
+           "camelot_simulate"]
 
 _lib = None
 
@@ -161,6 +162,10 @@ def lib():
         L.camelot_finalize.argtypes = [P, Cl, C.c_int, fp, C.c_int, C.c_void_p, E, Pl]
         L.camelot_last_stats.argtypes = [E, C.POINTER(C.c_uint64)]
         L.camelot_trace.argtypes = [E, C.POINTER(C.c_uint64), C.c_int]
+        L.camelot_simulate_workspace_bytes.restype = C.c_size_t
+        L.camelot_simulate_workspace_bytes.argtypes = [P, Cl, C.c_int64, C.c_int]
+        L.camelot_simulate.argtypes = [P, Cl, ip, ip, ip, fp, C.c_int64, C.c_int64, C.c_uint64, C.c_int, E,
+                                       C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.camelot_trees_workspace_bytes.restype = C.c_size_t
         L.camelot_trees_workspace_bytes.argtypes = [C.c_int, C.POINTER(Tree), C.c_int, C.c_int]
         L.camelot_tables_from_trees.argtypes = [C.c_int, C.POINTER(Tree), C.c_int, C.POINTER(C.c_int32), C.c_int,

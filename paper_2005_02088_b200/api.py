@@ -253,6 +253,28 @@ class Session:
         return dict(n_scored=out[0], n_nodes=out[1], n_feasible=out[2], t_ns=out[3], items=out[4],
                     launches=out[5], cum_scored=out[6], cum_nodes=out[7])
 
+    def simulate(self, batch, replicas, quota_pct, loads, n_queries: int = 100000, warmup: int = 10000,
+                 seed: int = 1, n_sims: int = 1):
+        """NEXT-4: simulated (p99, mean) latency in ms of an explicit plan at loads[A]
+        QPS, for n_sims independent streams: two lists [n_sims][A]."""
+        A = self.A
+        nb = L.lib().camelot_simulate_workspace_bytes(C.byref(self.cprob), C.byref(self.ccl), int(n_queries),
+                                                      int(n_sims))
+        if nb == 0:
+            raise L.CamelotError(L.EINVAL, L.lib().camelot_last_error().decode())
+        ws = torch.empty(nb, dtype=torch.uint8, device=f"cuda:{self.device}")
+        ex = self.exec()
+        ex.workspace, ex.workspace_bytes = ws.data_ptr(), nb
+        ip = lambda v: (C.c_int32 * len(v))(*[int(a) for a in v])
+        lam = (C.c_float * A)(*[float(v) for v in loads])
+        p99 = (C.c_double * (A * n_sims))()
+        mean = (C.c_double * (A * n_sims))()
+        L.check(L.lib().camelot_simulate(C.byref(self.cprob), C.byref(self.ccl), ip(batch), ip(replicas),
+                                         ip(quota_pct), lam, int(n_queries), int(warmup), int(seed), int(n_sims),
+                                         C.byref(ex), p99, mean), False)
+        return ([list(p99[k * A:(k + 1) * A]) for k in range(n_sims)],
+                [list(mean[k * A:(k + 1) * A]) for k in range(n_sims)])
+
     def trace(self):
         """Phase timestamps of the last search: [(tag, ns since the first mark)]."""
         out = (C.c_uint64 * 256)()

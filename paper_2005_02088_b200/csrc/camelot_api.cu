@@ -1004,6 +1004,73 @@ int camelot_predict(const camelot_problem *p, const camelot_cluster *c, const in
     return out->status;
 }
 
+size_t camelot_simulate_workspace_bytes(const camelot_problem *p, const camelot_cluster *c, int64_t n_queries,
+                                        int n_sims) {
+    Dims d;
+    if (check_problem(p, c, d)) return 0;
+    if (n_queries < 1 || n_sims < 1 || n_sims > 65535) {
+        fail(CAMELOT_EINVAL, "n_queries >= 1 and n_sims in 1..65535");
+        return 0;
+    }
+    return make_layout(d, 1).total + al((size_t)n_sims * (size_t)n_queries * sizeof(double)) +
+           al((size_t)n_sims * CAMELOT_MAX_APPS * 2 * sizeof(double));
+}
+
+int camelot_simulate(const camelot_problem *p, const camelot_cluster *c, const int32_t *batch,
+                     const int32_t *replicas, const int32_t *quota_pct, const float *load_qps, int64_t n_queries,
+                     int64_t warmup, uint64_t seed, int n_sims, const camelot_exec *ex, double *p99_ms,
+                     double *mean_ms) {
+    t_call_launches = 0;
+    if (!batch || !replicas || !quota_pct || !load_qps || !p99_ms || !mean_ms) return fail(CAMELOT_EINVAL, "null argument");
+    if (warmup < 0) return fail(CAMELOT_EINVAL, "warmup < 0");
+    const size_t need = camelot_simulate_workspace_bytes(p, c, n_queries, n_sims);
+    if (!need) return CAMELOT_EINVAL;
+    if (!ex || ex->workspace_bytes < need) return fail(CAMELOT_ENOMEM, "workspace too small for the simulation (%zu bytes)", need);
+    int rc = check_loads(p, load_qps, 1);
+    if (rc) return rc;
+    Ctx X;
+    rc = setup(p, c, ex, 1, X, true);
+    if (rc) return rc;
+    unsigned long long x = 0;
+    for (int a = 0; a < X.d.A; ++a) {
+        int b = -1;
+        for (int k = 0; k < X.d.nS; ++k)
+            if (p->batch[k] == batch[a]) b = k;
+        if (b < 0) return fail(CAMELOT_EINVAL, "batch %d of app %d is not on the batch grid", batch[a], a);
+        x = x * X.d.nS + b;
+    }
+    for (int i = 0; i < X.d.n; ++i) {
+        if (replicas[i] < 1 || replicas[i] > X.d.Rmax) return fail(CAMELOT_EINVAL, "replicas[%d] not in 1..Rmax", i);
+        int t = -1;
+        for (int k = 0; k < X.d.nQ; ++k)
+            if (p->quota_pct[k] == quota_pct[i]) t = k;
+        if (t < 0) return fail(CAMELOT_EINVAL, "quota %d of stage %d is not on the quota grid", quota_pct[i], i);
+        x = x * X.d.Rmax + (replicas[i] - 1);
+        x = x * X.d.nQ + t;
+    }
+    SimArgs A;
+    memset(&A, 0, sizeof(A));
+    A.x = x;
+    for (int a = 0; a < X.d.A; ++a) A.lam[a] = load_qps[a];
+    A.n_queries = n_queries;
+    A.warmup = warmup;
+    A.seed = seed;
+    A.lat = reinterpret_cast<double *>(X.ws + X.L.total);
+    A.out = reinterpret_cast<double *>(X.ws + X.L.total + al((size_t)n_sims * (size_t)n_queries * sizeof(double)));
+    simulate_kernel<<<n_sims, 256, 0, X.st>>>(X.P, A);
+    COUNT_LAUNCH();
+    CU(cudaGetLastError());
+    std::vector<double> h((size_t)n_sims * X.d.A * 2);
+    CU(cudaMemcpyAsync(h.data(), A.out, h.size() * sizeof(double), cudaMemcpyDeviceToHost, X.st));
+    CU(cudaStreamSynchronize(X.st));
+    for (int sidx = 0; sidx < n_sims; ++sidx)
+        for (int a = 0; a < X.d.A; ++a) {
+            p99_ms[sidx * X.d.A + a] = h[((size_t)sidx * X.d.A + a) * 2];
+            mean_ms[sidx * X.d.A + a] = h[((size_t)sidx * X.d.A + a) * 2 + 1];
+        }
+    return CAMELOT_OK;
+}
+
 int camelot_score_range(const camelot_problem *p, const camelot_cluster *c, uint64_t lo, uint64_t hi,
                         const camelot_exec *ex, uint8_t *d_verdict, float *d_T, int32_t *d_u, int32_t *d_U) {
     t_call_launches = 0;

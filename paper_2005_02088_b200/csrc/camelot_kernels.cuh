@@ -886,3 +886,137 @@ __global__ void tree_table_kernel(int n_trees, const int4 *nodes, const float *v
 }
 
 }  // namespace cam
+
+// ============================================================================
+// NEXT-4: tail-latency simulation of one plan (reading R32; PAPER.md L527
+// batching at the entry, L514 / L834 the 99%-ile QoS).  One CTA per
+// simulation: thread 0 runs the queueing recursion of each application
+// (Poisson arrivals from a counter-based stream, batches of s_a queries,
+// round-robin replicas, FIFO, contended durations, hand-overs) and writes the
+// measured latencies; the CTA then selects the exact ceil(0.99 M)-th smallest
+// by an 8-pass byte radix select on the (positive, hence ordered) double bit
+// patterns.
+namespace cam {
+
+__device__ __forceinline__ unsigned long long sim_sm64(unsigned long long z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+struct SimArgs {
+    unsigned long long x;                  // candidate (canonical index)
+    float lam[AMAX];                       // load per application (QPS)
+    long long n_queries, warmup;
+    unsigned long long seed;
+    double *lat;                           // [n_sims][n_queries]
+    double *out;                           // [n_sims][A][2] = (p99, mean)
+};
+
+__global__ void __launch_bounds__(256) simulate_kernel(const DevProb P, const SimArgs A) {
+    __shared__ FullScore sc;
+    __shared__ double freet[NMAX][CAMELOT_MAX_REPLICAS];
+    __shared__ unsigned int hist[256];
+    __shared__ unsigned long long sel[2];   // prefix, remaining rank
+    __shared__ double s_sum;
+    __shared__ int s_ok;
+    __shared__ ScoreScratch scr;
+    const unsigned long long sim = blockIdx.x;
+    double *lat = A.lat + sim * (unsigned long long)A.n_queries;
+    int beta[AMAX], rho[NMAX], theta[NMAX];
+    decode_index(P, A.x, beta, rho, theta);
+    if (threadIdx.x == 0) {
+        FullScore f;
+        score_digits(P, beta, rho, theta, f, &scr);
+        sc = f;
+        s_ok = f.place_viol == 0;
+    }
+    __syncthreads();
+    for (int a = 0; a < P.A; ++a) {
+        if (threadIdx.x == 0 && s_ok) {
+            const int s = P.S[beta[a]];
+            const int first = P.first_of_app[a], last = P.last_of_app[a];
+            for (int i = 0; i < NMAX; ++i)
+                for (int r = 0; r < CAMELOT_MAX_REPLICAS; ++r) freet[i][r] = 0.0;
+            const double scale = 1000.0 / (double)A.lam[a];
+            const unsigned long long base = sim_sm64(A.seed ^ (sim * 0xD1B54A32D192ED03ull));
+            const long long total = A.warmup + A.n_queries;
+            const long long nbatch = (total + s - 1) / s;
+            double t = 0.0, sum = 0.0;
+            long long m = 0;
+            for (long long b = 0; b < nbatch; ++b) {
+                const double t0 = t;   // arrivals of this batch are regenerated below (no per-batch buffer)
+                for (int j = 0; j < s; ++j) {
+                    const unsigned long long q = (unsigned long long)(b * s + j);
+                    const unsigned long long h = sim_sm64(base + (((unsigned long long)a << 40) | q));
+                    const double u = ((double)(h >> 11) + 0.5) * 0x1.0p-53;
+                    t = __dadd_rn(t, __dmul_rn(-log(u), scale));
+                }
+                double ready = t;
+                for (int i = first; i <= last; ++i) {
+                    const int r = (int)(b % (long long)(rho[i] + 1));
+                    const double start = ready > freet[i][r] ? ready : freet[i][r];
+                    const double fin = __dadd_rn(start, (double)sc.L[i]);
+                    freet[i][r] = fin;
+                    ready = fin;
+                    if (i < last && (P.flags & F_COMM)) ready = __dadd_rn(ready, (double)sc.comm[i]);
+                }
+                double ta = t0;
+                for (int j = 0; j < s; ++j) {
+                    const long long q = b * s + j;
+                    const unsigned long long h = sim_sm64(base + (((unsigned long long)a << 40) | (unsigned long long)q));
+                    const double u = ((double)(h >> 11) + 0.5) * 0x1.0p-53;
+                    ta = __dadd_rn(ta, __dmul_rn(-log(u), scale));
+                    if (q < A.warmup || q >= total) continue;
+                    const double l = __dsub_rn(ready, ta);
+                    lat[m++] = l;
+                    sum = __dadd_rn(sum, l);
+                }
+            }
+            s_sum = sum;
+            sel[0] = 0;
+            sel[1] = (unsigned long long)max(0ll, (long long)ceil(0.99 * (double)m) - 1);
+        }
+        __syncthreads();
+        if (!s_ok) {
+            if (threadIdx.x == 0) {
+                A.out[(sim * P.A + a) * 2 + 0] = -1.0;
+                A.out[(sim * P.A + a) * 2 + 1] = -1.0;
+            }
+            __syncthreads();
+            continue;
+        }
+        // exact order statistic: byte radix select, most significant byte first
+        const long long M = A.n_queries;
+        for (int byte = 7; byte >= 0; --byte) {
+            for (int t2 = threadIdx.x; t2 < 256; t2 += blockDim.x) hist[t2] = 0u;
+            __syncthreads();
+            const unsigned long long prefix = sel[0];
+            const unsigned long long hmask = byte == 7 ? 0ull : (~0ull << (8 * (byte + 1)));
+            for (long long q = threadIdx.x; q < M; q += blockDim.x) {
+                const unsigned long long key = (unsigned long long)__double_as_longlong(lat[q]);
+                if ((key & hmask) == prefix) atomicAdd(&hist[(key >> (8 * byte)) & 255u], 1u);
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                unsigned long long k = sel[1];
+                int d = 0;
+                while (d < 255 && k >= hist[d]) {
+                    k -= hist[d];
+                    ++d;
+                }
+                sel[0] = prefix | ((unsigned long long)d << (8 * byte));
+                sel[1] = k;
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            A.out[(sim * P.A + a) * 2 + 0] = __longlong_as_double((long long)sel[0]);
+            A.out[(sim * P.A + a) * 2 + 1] = s_sum / (double)M;
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace cam
