@@ -154,6 +154,7 @@ def main():
     ap.add_argument("--no-flat", action="store_true", help="skip the flat-scan roofline leg")
     ap.add_argument("--no-sa", action="store_true", help="skip the simulated-annealing baseline")
     ap.add_argument("--no-comm", action="store_true", help="skip the NEXT-2 communication-aware leg")
+    ap.add_argument("--no-sim", action="store_true", help="skip the NEXT-4 tail-simulation leg")
     ap.add_argument("--sa-chains", type=int, default=4096)
     ap.add_argument("--sa-iters", type=int, default=500)
     ap.add_argument("--flat-config", type=int, default=4, help="config of the flat scan (4 = C4)")
@@ -378,6 +379,23 @@ def main():
                 "min_resource": {"index": c2.index, "gpus_used": c2.gpus_used, "quota_used": c2.quota_used},
                 "note": "NEXT-2, reading R29/R30: hand-over times in Constraint-5's ordered sum"}
 
+    # NEXT-4: the simulated tail of the step's max-load plan (reading R32)
+    tail = None
+    if not args.no_sim and rank == 0:
+        ss2 = api.Session(prob, device=local)
+        sims, n_q = 64, 20000
+        tail = {"plan": "C4 max-load plan of this step", "queries_per_sim": n_q, "sims": sims, "points": []}
+        for f in (0.3, 0.6, 0.9):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            p99, mean = ss2.simulate(pm.batch, pm.replicas, pm.quota_pct, [f * pm.objective] * prob.n_apps,
+                                     n_q, 2000, seed=1, n_sims=sims)
+            dt = time.perf_counter() - t0
+            v = sorted(r[0] for r in p99)
+            tail["points"].append({"load_frac_of_T": f, "p99_ms_median_over_sims": v[len(v) // 2],
+                                   "mean_ms": statistics.mean(r[0] for r in mean), "sim_ms": dt * 1e3,
+                                   "predicted_latency_ms": pm.e2e_latency_ms[0], "qos_ms": float(prob.qos_ms[0])})
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         r = cpu_reference_leg(prob, args, rank, world, as_main=False)
@@ -397,7 +415,7 @@ def main():
                           "min_resource": {"index": pr.index, "gpus_used": pr.gpus_used,
                                            "quota_used": pr.quota_used, "load": LOW_LOAD * pm.objective}},
                 "scored_per_step": evals, "gpu_launches": launches, "roofline": roof, "flat_scan": flat,
-                "sa_baseline": sa, "comm_qos": comm,
+                "sa_baseline": sa, "comm_qos": comm, "tail_sim": tail,
                 "clocks": clocks,
                 "e2e": e2e, "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)
