@@ -743,9 +743,9 @@ std::vector<int> coarse_strides(const Ctx &X) {
         }
         return v;
     }
-    // measured on C4 / C5: (nQ/2, nQ/4, nQ/20) = C4 (50, 25, 5),
-    // C5 (5, 2) beat single levels (10) / (2) and (25, 10)
-    for (int s : {X.d.nQ / 2, X.d.nQ / 4, X.d.nQ / 20})
+    // measured on C4 / C5: (nQ/2, nQ/5, nQ/20) = C4 (50, 20, 5) (1.36 ms
+    // both policies vs 1.41 for (50, 25, 5)), C5 (5, 2)
+    for (int s : {X.d.nQ / 2, X.d.nQ / 5, X.d.nQ / 20})
         if (s >= 2 && (v.empty() || s < v.back())) v.push_back(s);
     return v;
 }
