@@ -192,6 +192,10 @@ typedef struct {
     uint64_t n_scored;        /* candidates fully scored by the search               */
     uint64_t n_covered;       /* candidates covered (scored or excluded by a bound)  */
     float comm_ms[CAMELOT_MAX_STAGES];  /* CAMELOT_F_COMM: hand-over time of edge i -> i+1 (ms) */
+    uint64_t n_evaluated;     /* leaves + inner nodes evaluated by the whole search
+                                 (incumbent cascade + main pass) of this call         */
+    uint64_t search_ns;       /* device time of that search (CUDA events on the stream,
+                                 ns) when searched and finalized on this thread, else 0 */
 } camelot_plan;
 
 /* ------------------------------------------------------------------ entry points */

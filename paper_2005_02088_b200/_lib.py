@@ -114,7 +114,7 @@ class Plan(C.Structure):
                 ("objective", C.c_float), ("quota_used", C.c_int32), ("gpus_used", C.c_int32),
                 ("eq2_gpus", C.c_int32), ("violations", C.c_uint32),
                 ("n_feasible", C.c_uint64), ("n_scored", C.c_uint64), ("n_covered", C.c_uint64),
-                ("comm_ms", C.c_float * MAX_STAGES)]
+                ("comm_ms", C.c_float * MAX_STAGES), ("n_evaluated", C.c_uint64), ("search_ns", C.c_uint64)]
 
 
 class Tree(C.Structure):

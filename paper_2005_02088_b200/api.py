@@ -40,6 +40,8 @@ class PlanResult:
     n_scored: int
     n_covered: int
     comm_ms: List[float] = None   # COMM: hand-over time of edge i -> i+1 (ms)
+    n_evaluated: int = 0          # leaves + inner nodes evaluated (cascade + main pass)
+    search_ns: int = 0            # device time of the search (ns), 0 if unknown
 
     @property
     def feasible(self) -> bool:
@@ -55,7 +57,8 @@ def _plan(p: L.Plan, n: int, A: int) -> PlanResult:
                       list(p.stage_latency_ms[:n]), list(p.stage_throughput_qps[:n]),
                       list(p.kappa[:n]), list(p.e2e_latency_ms[:A]), list(p.throughput_qps[:A]),
                       p.objective, p.quota_used, p.gpus_used, p.eq2_gpus, p.violations,
-                      int(p.n_feasible), int(p.n_scored), int(p.n_covered), list(p.comm_ms[:n]))
+                      int(p.n_feasible), int(p.n_scored), int(p.n_covered), list(p.comm_ms[:n]),
+                      int(p.n_evaluated), int(p.search_ns))
 
 
 class Session:

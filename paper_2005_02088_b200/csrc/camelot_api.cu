@@ -864,9 +864,16 @@ int finalize_impl(const Ctx &X, const camelot_exec *ex, int policy, int nlev, co
     CU(cudaStreamSynchronize(X.st));
     unsigned long long lo, hi;
     range_of(X, ex, lo, hi);
+    uint64_t search_ns = 0;   // the stream is synchronised: the search's events are complete
+    if (t_ev.armed && t_ev.dev == ex->device) {
+        float ms = 0.0f;
+        if (cudaEventElapsedTime(&ms, t_ev.a, t_ev.b) == cudaSuccess) search_ns = (uint64_t)((double)ms * 1e6);
+        else cudaGetLastError();
+    }
     bool any = false;
     for (int k = 0; k < nlev; ++k) {
         out[k].n_covered = hi - lo;
+        out[k].search_ns = search_ns;
         any |= out[k].status == CAMELOT_OK;
     }
     return any ? CAMELOT_OK : CAMELOT_INFEASIBLE;

@@ -357,6 +357,8 @@ __global__ void plan_kernel(const DevProb P, int policy, int nlev, const Slot *w
     memset(&pl, 0, sizeof(pl));
     for (int i = 0; i < CAMELOT_MAX_STAGES * CAMELOT_MAX_REPLICAS; ++i) pl.gpu_of_instance[i] = -1;
     pl.n_scored = hdr->n_scored;
+    pl.n_evaluated = hdr->cum_scored + hdr->cum_nodes;
+    pl.search_ns = 0;
     pl.n_feasible = hdr->n_feasible;
     pl.n_covered = 0;
     const Slot w = winner[k];
