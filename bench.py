@@ -290,7 +290,7 @@ def main():
     k_ns = sum(s1["t_ns"] + s2["t_ns"] for s1, s2 in kt) / args.steps
     achieved = ops_per_eval * evals / (k_ns * 1e-9) / 1e12 if k_ns else None
     peak = n_sm * 4 * 32 * sm_max * 1e6 / 1e12          # lane-instructions/s (issue bound)
-    traffic, traffic_src = ncu_traffic("r01_v6_ncu_search_raw.csv")
+    traffic, traffic_src = ncu_traffic("r01_v10_ncu_search_raw.csv")
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s",
             "frac": (achieved / peak) if achieved else None, "traffic": traffic,
             "traffic_note": f"DRAM bytes read+written per step (sum over the search-level launches of one step) "

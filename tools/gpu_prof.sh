@@ -3,7 +3,7 @@
 # exported to CSV on the box (the .ncu-rep files stay there).
 set -x
 mkdir -p gpurun_out/prof
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/prof/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-flat --no-sa > gpurun_out/prof/launch_bench.log 2>&1; echo ncu1=$?
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/prof/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-flat --no-sa --no-comm --no-sim > gpurun_out/prof/launch_bench.log 2>&1; echo ncu1=$?
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:search_level -c ${NCU_C:-6} -o /tmp/search_full python tools/ncu_one.py 4 > gpurun_out/prof/ncu_full.log 2>&1; echo ncu2=$?
 ncu -i /tmp/search_full.ncu-rep --page raw --csv > gpurun_out/prof/search_raw.csv 2>&1
 ncu -i /tmp/search_full.ncu-rep --page details --csv > gpurun_out/prof/search_details.csv 2>&1
