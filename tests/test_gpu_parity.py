@@ -334,3 +334,18 @@ def test_wide_instantiations(api, oracle, C, n, A, seed):
         check_plan(api, prob, gm, rm, oracle, loads=lam)
         flat = api.Session(prob, flags=prob.flags | G.F_NO_FILTER).plan_max_load()
         assert flat.index == ref.index and flat.n_feasible == ref.n_feasible
+
+
+def test_plan_diagnostics_and_trace(api):
+    """camelot_plan.search_ns / n_evaluated and the camelot_trace phase marks."""
+    prob = G.config_problems(6)[0]
+    s = api.Session(prob)
+    r = s.plan_max_load()
+    st = s.last_stats()
+    assert r.n_evaluated == st["cum_scored"] + st["cum_nodes"] > 0
+    assert r.search_ns > 0 and abs(r.search_ns - st["t_ns"]) <= 1000
+    tr = s.trace()
+    tags = [t for t, _ in tr if t < 64]
+    assert tags.count(0) >= 1 and 16 in tags and 32 in tags      # launch start, pass 0, CTA reduction
+    times = [ns for t, ns in tr if t < 64]
+    assert times == sorted(times)
