@@ -396,21 +396,28 @@ int coop_grid_for(int dev, int &grid) {
 }
 
 template <int CM, int NS, int POL>
-int launch_level(const Ctx &X, int dev, LevelArgs LA) {
+int launch_level(const Ctx &X, int dev, const std::vector<LevelArgs> &levels) {
     int grid = 0;
     int rc = coop_grid_for<CM, NS, POL>(dev, grid);
     if (rc) return rc;
-    LA.F.nslots = grid * LA.S.nlev;
+    LevelSet LS;
+    memset(&LS, 0, sizeof(LS));
+    if (levels.empty() || levels.size() > (size_t)MAX_LEVELS) return fail(CAMELOT_EINVAL, "bad level count");
+    LS.count = (int)levels.size();
+    for (int l = 0; l < LS.count; ++l) {
+        LS.L[l] = levels[l];
+        LS.L[l].F.nslots = grid * LS.L[l].S.nlev;
+    }
     const size_t sm = level_smem<CM>();
-    void *args[] = {(void *)&X.P, (void *)&LA};
+    void *args[] = {(void *)&X.P, (void *)&LS};
     CU(cudaLaunchCooperativeKernel((const void *)search_level_kernel<CM, NS, POL>, dim3(grid), dim3(SEARCH_THREADS),
                                    args, sm, X.st));
     COUNT_LAUNCH();
     return CAMELOT_OK;
 }
 
-int launch_level_any(const Ctx &X, int policy, int dev, const LevelArgs &LA) {
-    CAM_DISPATCH(launch_level, X, dev, LA);
+int launch_level_any(const Ctx &X, int policy, int dev, const std::vector<LevelArgs> &levels) {
+    CAM_DISPATCH(launch_level, X, dev, levels);
 }
 
 int launch_search_any(const Ctx &X, int policy, const SearchArgs &S, int grid) {
@@ -599,7 +606,7 @@ int sweep_pass(const Ctx &X, int dev, int policy, int nlev, const Slot *inc, Slo
 
 int search_pass(const Ctx &X, int dev, int policy, int nlev, bool prune, int stride, const Slot *inc,
                 Slot *result, long long *keys, int rank, int world, unsigned long long lo, unsigned long long hi,
-                bool timed, Slot *inc_out = nullptr) {
+                bool timed, Slot *inc_out = nullptr, std::vector<LevelArgs> *defer = nullptr) {
     char *ws = X.ws;
     if (X.naive)
         return flat_pass(X, dev, policy, nlev, nlev, 0, reinterpret_cast<const float *>(ws + X.L.lam), inc, result,
@@ -668,7 +675,11 @@ int search_pass(const Ctx &X, int dev, int policy, int nlev, bool prune, int str
         LA.buf0 = ws + X.L.front0;
         LA.buf1 = ws + X.L.front1;
         LA.fcap = X.L.fcap;
-        return launch_level_any(X, policy, dev, LA);
+        if (defer) {   // chained into one cooperative launch by the caller
+            defer->push_back(LA);
+            return CAMELOT_OK;
+        }
+        return launch_level_any(X, policy, dev, std::vector<LevelArgs>{LA});
     }
     return run_passes(X, dev, policy, S, timed, false);
 }
@@ -787,6 +798,7 @@ int local_search(const Ctx &X, const camelot_exec *ex, int policy, int nlev, lon
         t_ev.dev = dev;
     }
     CU(cudaEventRecord(t_ev.a, X.st));
+    std::vector<int> pending_strides;
     if (use_coarse(X, prune)) {
         // incumbent: exact optimum of coarse quota sub-grids, coarsest first (each
         // pass seeds the next); replicated on every rank.  The coarse levels small
@@ -812,14 +824,25 @@ int local_search(const Ctx &X, const camelot_exec *ex, int policy, int nlev, lon
                 strides.swap(rest);
             }
         }
-        for (int stride : strides) {
-            rc = search_pass(X, dev, policy, nlev, true, stride, inc, result,
-                             reinterpret_cast<long long *>(ws + X.L.keys), 0, 1, lo, hi, false, inc);
-            if (rc) return rc;
-        }
+        pending_strides = strides;
     }
-    rc = search_pass(X, dev, policy, nlev, prune, 1, inc, result, keys, ex->rank, ex->world, lo, hi, false);
+    // the pruned levels (cascade, then the main pass) go into ONE cooperative launch
+    std::vector<LevelArgs> levels;
+    const bool chain = use_coop() && !X.naive && prune;
+    std::vector<int> strides2;
+    if (use_coarse(X, prune)) strides2 = pending_strides;
+    for (int stride : strides2) {
+        rc = search_pass(X, dev, policy, nlev, true, stride, inc, result, reinterpret_cast<long long *>(ws + X.L.keys),
+                         0, 1, lo, hi, false, inc, chain ? &levels : nullptr);
+        if (rc) return rc;
+    }
+    rc = search_pass(X, dev, policy, nlev, prune, 1, inc, result, keys, ex->rank, ex->world, lo, hi, false, nullptr,
+                     chain ? &levels : nullptr);
     if (rc) return rc;
+    if (!levels.empty()) {
+        rc = launch_level_any(X, policy, dev, levels);
+        if (rc) return rc;
+    }
     CU(cudaEventRecord(t_ev.b, X.st));
     t_ev.armed = true;
     CU(cudaMemcpyAsync(ws + X.L.hdr2, ws + X.L.hdr, sizeof(DevHeader), cudaMemcpyDeviceToDevice, X.st));

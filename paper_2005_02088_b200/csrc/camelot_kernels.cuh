@@ -594,12 +594,11 @@ struct LevelArgs {
     unsigned long long fcap;
 };
 
+// One search level (incumbent cascade level or main pass) executed by the whole
+// cooperative grid; levels are chained inside one launch (search_level_kernel).
 template <int CM, int NS, int POLICY>
-__global__ void __launch_bounds__(SEARCH_THREADS, SEARCH_MINB)
-search_level_kernel(const DevProb P, const LevelArgs LA) {
-    namespace cg = cooperative_groups;
-    cg::grid_group grid = cg::this_grid();
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+__device__ __forceinline__ void level_body(const DevProb &P, const LevelArgs &LA, unsigned char *smem_raw,
+                                           cooperative_groups::grid_group &grid) {
     SearchArgs S = LA.S;
     DevHeader *hdr = S.hdr;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -708,6 +707,26 @@ search_level_kernel(const DevProb P, const LevelArgs LA) {
     }
 }
 
+
+// All pruned levels of one search in ONE cooperative launch: level l+1 reads the
+// incumbent level l's reduction (block 0) wrote before level l+1's first grid
+// barrier, so no extra barrier or launch is needed between levels.
+constexpr int MAX_LEVELS = 4;
+struct LevelSet {
+    int count;
+    LevelArgs L[MAX_LEVELS];
+};
+
+template <int CM, int NS, int POLICY>
+__global__ void __launch_bounds__(SEARCH_THREADS, SEARCH_MINB)
+search_level_kernel(const DevProb P, const LevelSet LS) {
+    cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    for (int l = 0; l < LS.count; ++l) {
+        level_body<CM, NS, POLICY>(P, LS.L[l], smem_raw, grid);
+        __syncthreads();   // block 0's reduction used shared memory
+    }
+}
 }  // namespace cam
 
 // ============================================================================
