@@ -1050,12 +1050,15 @@ __device__ __forceinline__ void init_warp_best(const SearchArgs &S, WarpBest *wb
 template <int CM, int NS, int POLICY>
 __device__ __forceinline__ void thread_chunk(const DevProb &P, const SearchArgs &S, const Frontier<CM> &in,
                                           const Frontier<CM> &outf, unsigned long long e0, unsigned live, int j,
-                                          WarpBest *wb, int lane, Counters &cn) {
+                                          WarpBest *wb, int lane, Counters &cn, int G) {
+    // G lanes per parent (G > 1 only for leaf passes): lane l takes parent e0 + l / G
+    // and its children sub, sub + G, ... (sub = l % G)
     const int n = P.n, nlev = S.nlev;
     const bool leaf = j == n - 1;
     const unsigned long long span = P.opow[n - 1 - j];
     unsigned long long bk = wb->key[0], bx = wb->x[0];   // lane-local best (leaf passes: one level)
-    const bool mine = (live >> lane) & 1u;
+    const int pl = lane / G, sub = lane % G;
+    const bool mine = (live >> pl) & 1u;
 #ifdef CAMELOT_FTRACE
     const bool tme = lane == 0;
     unsigned long long tt[4] = {0, 0, 0, 0};
@@ -1063,7 +1066,7 @@ __device__ __forceinline__ void thread_chunk(const DevProb &P, const SearchArgs 
 #endif
     {
         // dead lanes view node e0 (valid memory) and have no children
-        const NodeSoA<CM> nd(in, e0 + (mine ? lane : 0));
+        const NodeSoA<CM> nd(in, e0 + (mine ? pl : 0));
         PCtx<CM, NS> c;
         load_ctx<CM, NS>(P, S, nd, j, c);
         const int bj = nd.b[P.app[j]];
@@ -1084,9 +1087,11 @@ __device__ __forceinline__ void thread_chunk(const DevProb &P, const SearchArgs 
         if (tme) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt[1]));
 #endif
         unsigned smask = 0u;   // surviving children of this lane's parent (inner passes)
-        const int cntw = __reduce_max_sync(0xffffffffu, cnt);
-        for (int k = 0; k < cntw; ++k) {
-            const bool valid = k < cnt;
+        const int my_iters = cnt > sub ? (cnt - sub + G - 1) / G : 0;
+        const int cntw = __reduce_max_sync(0xffffffffu, my_iters);
+        for (int t = 0; t < cntw; ++t) {
+            const int k = sub + t * G;
+            const bool valid = t < my_iters;
             OptRec r;
             {
                 const uint4 *src = reinterpret_cast<const uint4 *>(list + (valid ? k : 0));
@@ -1298,10 +1303,13 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
     // thread-per-parent mode: leaf passes with one level, or inner passes whose children
     // all fit in the output frontier (no inline descent possible in this mode)
     // (measured: leaf passes with more than 32 options per parent are faster in the warp mode)
-    const bool tmode = S.prune && have_in && split == 1 && count >= 2ull * nwarps && maxc <= 32 && !getenv_tmode_off() &&
-                       ((S.flevel < 0 && jtop == n - 1 && nlev == 1) ||
-                        (S.flevel == jtop + 1 && count * (unsigned long long)maxc <= S.out_cap));
-    const unsigned grab = tmode ? 32u : screen ? 8u : (unsigned)S.grab;
+    // leaf passes with more than 32 options per parent use G = 2 or 4 lanes per parent
+    const bool leafp = S.flevel < 0 && jtop == n - 1 && nlev == 1;
+    const int G = (!leafp || maxc <= 32) ? 1 : maxc <= 64 ? 2 : 4;
+    const bool tmode = S.prune && have_in && split == 1 && count >= 2ull * nwarps && !getenv_tmode_off() &&
+                       ((leafp && maxc <= 128) ||
+                        (S.flevel == jtop + 1 && maxc <= 32 && count * (unsigned long long)maxc <= S.out_cap));
+    const unsigned grab = tmode ? 32u / (unsigned)G : screen ? 8u : (unsigned)S.grab;
     const unsigned long long nw = nwarps * grab;
     unsigned long long e0 = ((unsigned long long)blockIdx.x * SEARCH_WARPS + (threadIdx.x >> 5)) * grab;
     bool first = true;
@@ -1356,7 +1364,7 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
             live = __ballot_sync(0xffffffffu, lv);
         }
         if (tmode) {
-            thread_chunk<CM, NS, POLICY>(P, S, in, outf, e0, live, jtop, wb, lane, cn);
+            thread_chunk<CM, NS, POLICY>(P, S, in, outf, e0, live, jtop, wb, lane, cn, G);
             continue;
         }
         for (unsigned long long it = e0; it < e1; ++it) {
