@@ -1305,11 +1305,11 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
     // (measured: leaf passes with more than 32 options per parent are faster in the warp mode)
     // leaf passes with more than 32 options per parent use G = 2 or 4 lanes per parent
     const bool leafp = S.flevel < 0 && jtop == n - 1 && nlev == 1;
-    // lanes per parent: enough parent groups to occupy the warps (measured: a pass with
+    // lanes per parent (1..8): enough parent groups to occupy the warps (measured: a pass with
     // 7.5k parents kept only 234 of 1184 warps busy at one lane per parent), and for
     // leaf passes at most 32 children per lane
     int G = 1;
-    while (G < 4 && count * (unsigned long long)(2 * G) <= 32ull * nwarps) G *= 2;
+    while (G < 8 && count * (unsigned long long)(2 * G) <= 32ull * nwarps) G *= 2;
     if (leafp) G = max(G, maxc <= 32 ? 1 : maxc <= 64 ? 2 : 4);
     const bool tmode = S.prune && have_in && split == 1 && count >= 2ull * nwarps && !getenv_tmode_off() &&
                        ((leafp && maxc <= 128) ||
