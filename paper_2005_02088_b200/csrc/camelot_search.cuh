@@ -1478,9 +1478,11 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
                 const int opt = base + lane;
                 const bool valid = opt < endj;
                 OptRec r;
+                uint4 cold = make_uint4(0u, 0u, 0u, 0u);   // p, W, A*s, MEM (emission only)
                 {
                     const uint4 *src = reinterpret_cast<const uint4 *>(list + (valid ? opt : base));
                     const uint4 a = __ldg(src), b = __ldg(src + 1);
+                    if (!leaf) cold = __ldg(src + 2);
                     r.code = a.x;
                     r.NP = a.y;
                     r.N = a.z;
@@ -1565,10 +1567,7 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
                     fbase = __shfl_sync(0xffffffffu, fbase, 0);
                     const unsigned long long slot = fbase + __popc(m & ((1u << lane) - 1u));
                     const bool fits = sv && slot < S.out_cap;
-                    if (fits) {
-                        const OptRec &full = list[opt];
-                        emit_child<CM, NS>(P, nd, c, j, r, full.p, full.W, full.As, opt, outf, slot);
-                    }
+                    if (fits) emit_child<CM, NS>(P, nd, c, j, r, cold.x, cold.y, cold.z, opt, outf, slot);
                     PTM(5);
                     m = __ballot_sync(0xffffffffu, sv && !fits);   // frontier full: descend inline
                 }
