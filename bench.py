@@ -34,14 +34,17 @@ WORKLOAD = "C4: 5-stage p1-c2-m2-c3-m1 pipeline, 8 modeled V100 (BW 897 GB/s), 1
 LOW_LOAD = 0.3   # low load = 30% of the peak
 
 
-def ncu_traffic(name):
-    """dram__bytes_read.sum + dram__bytes_write.sum summed over the launches of a
-    committed ncu --page raw --csv capture under profiles/ (None if absent)."""
+def ncu_traffic(name, launches_per_step=None):
+    """dram__bytes_read.sum + dram__bytes_write.sum summed over the first
+    `launches_per_step` launches (one step) of a committed ncu --page raw --csv
+    capture under profiles/ (all launches if None; None if the file is absent)."""
     import csv
     path = os.path.join(ROOT, "profiles", name)
     try:
         rows = list(csv.reader(open(path)))
         hdr, units, data = rows[0], rows[1], rows[2:]
+        if launches_per_step:
+            data = data[:launches_per_step]
         tot = 0.0
         for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
             i = hdr.index(key)
@@ -290,7 +293,7 @@ def main():
     k_ns = sum(s1["t_ns"] + s2["t_ns"] for s1, s2 in kt) / args.steps
     achieved = ops_per_eval * evals / (k_ns * 1e-9) / 1e12 if k_ns else None
     peak = n_sm * 4 * 32 * sm_max * 1e6 / 1e12          # lane-instructions/s (issue bound)
-    traffic, traffic_src = ncu_traffic("r01_v10_ncu_search_raw.csv")
+    traffic, traffic_src = ncu_traffic("r01_v13_ncu_search_raw.csv", 2)   # one launch per policy
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s",
             "frac": (achieved / peak) if achieved else None, "traffic": traffic,
             "traffic_note": f"DRAM bytes read+written per step (sum over the search-level launches of one step) "
