@@ -198,8 +198,7 @@ typedef struct {
     int32_t rq[OC_MAX_GPUS];     /* remaining quota (%) */
     int32_t cnt[OC_MAX_GPUS];    /* instances hosted */
     int64_t rm[OC_MAX_GPUS];     /* remaining memory (MiB) */
-    float dem[OC_MAX_GPUS];
-    float comm[OC_MAX_STAGES];             /* COMM: hand-over time of edge i -> i+1 (0: none) */      /* accumulated bandwidth demand (GB/s) */
+    float dem[OC_MAX_GPUS];      /* accumulated bandwidth demand (GB/s) */
     int32_t host[OC_MAX_STAGES][OC_MAX_GPUS];
 } oc_state;
 

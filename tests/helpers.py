@@ -68,3 +68,17 @@ def contention_problem(qos, flags=0):
         [[[8, 16, 20]], [[32, 64, 64]]])
     return G.custom_problem("pk", tab, [25, 50, 75], [1], [qos], cluster(C=1, BW=128.0),
                             bw_sensitivity=[0.0, 1.0], flags=flags_of(flags))
+
+
+def kappa_split_problem(bwA):
+    """tests/golden/kappa_split.json: stage A (1 x 50%) then stage B (3 x 50%) on 2 GPUs."""
+    tab = table_from([[[10.0]], [[20.0]]], [[[200.0]], [[50.0]]], [[[bwA]], [[32.0]]])
+    return G.custom_problem("ksplit", tab, [50], [1], [1e9], cluster(C=2, BW=128.0), max_replicas=3,
+                            bw_sensitivity=[0.0, 1.0])
+
+
+def min_resource_priority_problem():
+    """tests/golden/min_resource_priority.json: thr = p per replica, I = 2, two GPUs."""
+    Q = [15, 40, 60]
+    tab = table_from([[[1000.0 / q for q in Q]]] * 2, [[[float(q) for q in Q]]] * 2, [[[0.0] * 3]] * 2)
+    return G.custom_problem("uU", tab, Q, [1], [1e9], cluster(C=2, I=2), max_replicas=2)
