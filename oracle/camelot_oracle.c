@@ -629,6 +629,273 @@ int oc_search(const oc_problem *P, int policy, const float *loads, int L, uint64
     return 0;
 }
 
+/* ---------------------------------------------------------------- O7: filtered oracle
+ * SURVEY.md §8(c) O7 / §8(a) A6.  The same answer as oc_search over the whole
+ * space, for spaces too large to scan (full C4), given an INCUMBENT: the
+ * objective of a known feasible candidate of the space (max-load: T_inc;
+ * min-resource, one load level: (u_inc, U_inc)).  Plain steps:
+ *   1. per batch combination and stage i, the option list (rho_i, theta_i) in
+ *      canonical order keeps only options that pass every NECESSARY condition of
+ *      "feasible and at least as good as the incumbent" (non-strict, so ties
+ *      survive), iterated to a fixpoint:
+ *        - throughput: T <= T_i <= fl(N_i thr_i) (kappa >= 1, Eq. 1, R12), so
+ *          max-load drops fl(N thr) < T_inc and min-resource drops fl(N thr) <
+ *          lambda_app (load floor R10);
+ *        - QoS (Constraint-5, L834, R1): L_j >= dur_j (kappa >= 1) and the ordered
+ *          binary32 sum of non-negative terms is monotone in every term (and only
+ *          grows when hand-over terms are inserted), so the ordered sum with this
+ *          option's dur at stage i and the smallest surviving dur at the app's
+ *          other stages must be <= QoS_a;
+ *        - quota (Constraint-2, L831): every GPU holds at most R, so
+ *          N p + sum_{j != i} min_j(N p) <= C R;
+ *        - min-resource incumbent (L842, R11): U = sum N p exactly and every used
+ *          GPU holds at most R, so u >= ceil(U / R) (u = 0 under PAPER_GLOBAL);
+ *          with U_lb = N p + sum_{j != i} min_j(N p) and u_lb = ceil(U_lb / R) the
+ *          option is dropped iff u_lb > u_inc, or u_lb >= u_inc and U_lb > U_inc;
+ *   2. nested loops over the surviving options in canonical order (batch, then
+ *      stage 1 .. n), where a prefix whose partial sum N p plus the unplaced
+ *      stages' minima already fails the quota or the min-resource test above is
+ *      skipped (the same necessary conditions on the partial sum);
+ *   3. every remaining candidate is scored by the unchanged oc_score and kept on
+ *      STRICT improvement, exactly as oc_search does.
+ * Scanning in canonical order with strict improvement returns the smallest
+ * index among ties, as oc_search.  The incumbent only ever removes candidates
+ * strictly worse than itself, hence strictly worse than the optimum.
+ * n_scanned counts the candidates scored; n_feasible those feasible among them. */
+typedef struct {
+    int32_t cnt[OC_MAX_STAGES];
+    int32_t code[OC_MAX_STAGES][OC_MAX_REPL * 128];   /* rho * nQ + theta, ascending */
+} oc_optlist;
+
+static int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+/* step 1 for one batch combination; returns 0 if some stage has no option left */
+static int o7_filter(const oc_problem *P, int policy, const float *lam, const int32_t *beta, float T_inc,
+                     int32_t u_inc, int32_t U_inc, oc_optlist *ol) {
+    const int n = P->n, O = P->Rmax * P->nQ;
+    uint8_t alive[OC_MAX_STAGES][OC_MAX_REPL * 128];
+    for (int i = 0; i < n; i++)
+        for (int k = 0; k < O; k++) alive[i][k] = 1;
+    for (int iter = 0;; iter++) {
+        float mindur[OC_MAX_STAGES];
+        int32_t minnp[OC_MAX_STAGES];
+        for (int i = 0; i < n; i++) {
+            mindur[i] = INFINITY;
+            minnp[i] = INT32_MAX;
+            for (int k = 0; k < O; k++) {
+                if (!alive[i][k]) continue;
+                const int N = k / P->nQ + 1, th = k % P->nQ;
+                const float d = entry(P, i, beta[P->app[i]], th)[0];
+                if (d < mindur[i]) mindur[i] = d;
+                if (N * P->Q[th] < minnp[i]) minnp[i] = N * P->Q[th];
+            }
+            if (minnp[i] == INT32_MAX) return 0;
+        }
+        int changed = 0;
+        for (int i = 0; i < n; i++) {
+            const int a = P->app[i];
+            for (int k = 0; k < O; k++) {
+                if (!alive[i][k]) continue;
+                const int N = k / P->nQ + 1, th = k % P->nQ;
+                const float *e = entry(P, i, beta[a], th);
+                int drop = 0;
+                const float nt = (float)N * e[1];
+                if (policy == 0 && nt < T_inc) drop = 1;
+                if (policy != 0 && nt < lam[a]) drop = 1;
+                /* QoS: ordered sum over the app's stages */
+                int first = 1;
+                float ls = 0.0f;
+                for (int j = 0; j < n; j++) {
+                    if (P->app[j] != a) continue;
+                    const float t = j == i ? e[0] : mindur[j];
+                    ls = first ? t : ls + t;
+                    first = 0;
+                }
+                if (ls > P->qos[a]) drop = 1;
+                /* quota and the min-resource incumbent */
+                int32_t Ulb = N * P->Q[th];
+                for (int j = 0; j < n; j++)
+                    if (j != i) Ulb += minnp[j];
+                if (Ulb > P->C * P->R) drop = 1;
+                if (policy != 0) {
+                    const int32_t ulb = (P->flags & OC_PAPER_GLOBAL) ? 0 : ceil_div(Ulb, P->R);
+                    if (ulb > u_inc || (ulb >= u_inc && Ulb > U_inc)) drop = 1;
+                }
+                if (drop) {
+                    alive[i][k] = 0;
+                    changed = 1;
+                }
+            }
+        }
+        if (!changed) break;
+    }
+    for (int i = 0; i < n; i++) {
+        ol->cnt[i] = 0;
+        for (int k = 0; k < O; k++)
+            if (alive[i][k]) ol->code[i][ol->cnt[i]++] = k;
+        if (ol->cnt[i] == 0) return 0;
+    }
+    return 1;
+}
+
+/* steps 2-3: the candidates below a fixed batch combination and stage-1 option */
+static int o7_prefix_ok(const oc_problem *P, int policy, int32_t Ulb, int32_t u_inc, int32_t U_inc) {
+    if (Ulb > P->C * P->R) return 0;
+    if (policy != 0) {
+        const int32_t ulb = (P->flags & OC_PAPER_GLOBAL) ? 0 : ceil_div(Ulb, P->R);
+        if (ulb > u_inc || (ulb >= u_inc && Ulb > U_inc)) return 0;
+    }
+    return 1;
+}
+
+static void o7_leaf(const oc_problem *P, int policy, const float *lam, const int32_t *beta, const int32_t *rho,
+                    const int32_t *theta, oc_best_t *best) {
+    oc_score_t sc;
+    oc_score(P, beta, rho, theta, lam, policy == 0 ? 0 : 1, &sc);
+    best->n_scanned++;
+    const uint32_t v = policy == 0 ? sc.verdict : sc.level_verdict[0];
+    if (v) {
+        hist_add(best->hist, v);
+        return;
+    }
+    best->n_feasible++;
+    int better;
+    if (policy == 0)
+        better = best->index == UINT64_MAX || sc.T > best->T;
+    else
+        better = best->index == UINT64_MAX || sc.u < best->u || (sc.u == best->u && sc.U < best->U);
+    if (better) {
+        best->index = oc_encode(P, beta, rho, theta);
+        best->T = sc.T;
+        best->u = sc.u;
+        best->U = sc.U;
+    }
+}
+
+static void o7_scan(const oc_problem *P, int policy, const float *lam, const int32_t *beta,
+                    const oc_optlist *ol, int t0, int32_t u_inc, int32_t U_inc, oc_best_t *best) {
+    const int n = P->n;
+    int32_t minnp_after[OC_MAX_STAGES + 1];   /* sum of the minimum N p of the stages after i */
+    minnp_after[n] = 0;
+    for (int i = n - 1; i >= 0; i--) {
+        int32_t m = INT32_MAX;
+        for (int t = 0; t < ol->cnt[i]; t++) {
+            const int k = ol->code[i][t];
+            const int32_t np = (k / P->nQ + 1) * P->Q[k % P->nQ];
+            if (np < m) m = np;
+        }
+        minnp_after[i] = minnp_after[i + 1] + m;
+    }
+    int32_t rho[OC_MAX_STAGES], theta[OC_MAX_STAGES], Upre[OC_MAX_STAGES + 1];
+    int pos[OC_MAX_STAGES];
+    /* stage 1: the one option of this work item */
+    const int k0 = ol->code[0][t0];
+    rho[0] = k0 / P->nQ;
+    theta[0] = k0 % P->nQ;
+    Upre[0] = 0;
+    Upre[1] = (rho[0] + 1) * P->Q[theta[0]];
+    if (!o7_prefix_ok(P, policy, Upre[1] + minnp_after[1], u_inc, U_inc)) return;
+    if (n == 1) {
+        o7_leaf(P, policy, lam, beta, rho, theta, best);
+        return;
+    }
+    /* stages 2..n: nested loops (explicit stack), canonical order */
+    int depth = 1;
+    pos[1] = -1;
+    while (depth >= 1) {
+        if (++pos[depth] >= ol->cnt[depth]) {
+            depth--;
+            continue;
+        }
+        const int k = ol->code[depth][pos[depth]];
+        rho[depth] = k / P->nQ;
+        theta[depth] = k % P->nQ;
+        Upre[depth + 1] = Upre[depth] + (rho[depth] + 1) * P->Q[theta[depth]];
+        if (!o7_prefix_ok(P, policy, Upre[depth + 1] + minnp_after[depth + 1], u_inc, U_inc)) continue;
+        if (depth + 1 < n) {
+            depth++;
+            pos[depth] = -1;
+            continue;
+        }
+        o7_leaf(P, policy, lam, beta, rho, theta, best);
+    }
+}
+
+int oc_search_filtered(const oc_problem *P, int policy, const float *lam, float T_inc, int32_t u_inc,
+                       int32_t U_inc, int threads, oc_best_t *best) {
+    if (oc_validate(P) != 0) return -1;
+    if (P->Rmax * P->nQ > OC_MAX_REPL * 128) return -1;
+    if (policy != 0)
+        for (int a = 0; a < P->A; a++)
+            if (!(lam[a] > 0.0f) || !isfinite(lam[a])) return -1;
+    if (oc_ntot(P) == 0) return -2;
+    int nb = 1;
+    for (int a = 0; a < P->A; a++) nb *= P->nS;
+    oc_optlist *ol = (oc_optlist *)malloc(sizeof(oc_optlist) * (size_t)nb);
+    int *ok = (int *)malloc(sizeof(int) * (size_t)nb);
+    if (!ol || !ok) return -3;
+    /* step 1 per batch combination (beta digits, most significant first) */
+    int nitems = 0;
+    for (int c = 0; c < nb; c++) {
+        int32_t beta[OC_MAX_APPS];
+        int r = c;
+        for (int a = P->A - 1; a >= 0; a--) {
+            beta[a] = r % P->nS;
+            r /= P->nS;
+        }
+        ok[c] = o7_filter(P, policy, lam, beta, T_inc, u_inc, U_inc, &ol[c]);
+        if (ok[c]) nitems += ol[c].cnt[0];
+    }
+    /* work items = (batch combination, stage-1 option), in canonical order */
+    int *item_c = (int *)malloc(sizeof(int) * (size_t)(nitems + 1));
+    int *item_k = (int *)malloc(sizeof(int) * (size_t)(nitems + 1));
+    oc_best_t *part = (oc_best_t *)calloc((size_t)(nitems + 1), sizeof(oc_best_t));
+    if (!item_c || !item_k || !part) return -3;
+    int m = 0;
+    for (int c = 0; c < nb; c++)
+        if (ok[c])
+            for (int t = 0; t < ol[c].cnt[0]; t++) {
+                item_c[m] = c;
+                item_k[m] = t;
+                m++;
+            }
+    if (threads < 1) threads = 1;
+#pragma omp parallel for num_threads(threads) schedule(dynamic, 1)
+    for (int w = 0; w < nitems; w++) {
+        int32_t beta[OC_MAX_APPS];
+        int r = item_c[w];
+        for (int a = P->A - 1; a >= 0; a--) {
+            beta[a] = r % P->nS;
+            r /= P->nS;
+        }
+        memset(&part[w], 0, sizeof(oc_best_t));
+        part[w].index = UINT64_MAX;
+        o7_scan(P, policy, lam, beta, &ol[item_c[w]], item_k[w], u_inc, U_inc, &part[w]);
+    }
+    /* merge in canonical order with strict improvement (== one sequential scan) */
+    oc_best_t acc;
+    memset(&acc, 0, sizeof(acc));
+    acc.index = UINT64_MAX;
+    for (int w = 0; w < nitems; w++) {
+        acc.n_feasible += part[w].n_feasible;
+        acc.n_scanned += part[w].n_scanned;
+        for (int b = 0; b < 7; b++) acc.hist[b] += part[w].hist[b];
+        if (better_than(policy, &part[w], &acc)) {
+            acc.index = part[w].index;
+            acc.T = part[w].T;
+            acc.u = part[w].u;
+            acc.U = part[w].U;
+        }
+    }
+    *best = acc;
+    free(ol);
+    free(ok);
+    free(item_c);
+    free(item_k);
+    free(part);
+    return 0;
+}
+
 int oc_eq2_y(const oc_problem *P, const int32_t *beta, const float *lam) { return eq2_y(P, beta, lam); }
 
 int oc_sizeof_score(void) { return (int)sizeof(oc_score_t); }

@@ -342,3 +342,29 @@ def simulate(prob, x: int, loads, n_queries: int = 100000, warmup: int = 10000, 
         raise ValueError(f"oc_simulate rc={rc}")
     A = prob.n_apps
     return list(p99[:A]), list(mean[:A])
+
+
+# ---------------------------------------------------------------------- O7
+def search_filtered(prob, policy: str = "max_load", load=None, T_inc: float = 0.0, u_inc: int = 0,
+                    U_inc: int = 0, threads: int = 1, flags=None) -> Best:
+    """O7: the exhaustive scan restricted to the candidates that
+    survive the separable necessary-condition filters against an incumbent (a
+    known feasible candidate's objective: T_inc for max-load; (u_inc, U_inc) for
+    min-resource at ONE load level `load` [A]).  Same answer as search() over the
+    whole space; n_scanned = candidates scored."""
+    h = Handle(prob, flags)
+    pol = 0 if policy == "max_load" else 1
+    la = (C.c_float * MAX_APPS)()
+    if pol == 1:
+        vals = [float(v) for v in np.asarray(load, np.float32).reshape(-1)]
+        for a, v in enumerate(vals):
+            la[a] = v
+    out = OcBest()
+    f = lib().oc_search_filtered
+    f.argtypes = [C.POINTER(OcProblem), C.c_int, C.POINTER(C.c_float), C.c_float, C.c_int32, C.c_int32,
+                  C.c_int, C.POINTER(OcBest)]
+    rc = f(h.ref, pol, la, float(np.float32(T_inc)), int(u_inc), int(U_inc), int(threads), C.byref(out))
+    if rc != 0:
+        raise ValueError(f"oc_search_filtered rc={rc}")
+    return Best(None if out.index == NONE else int(out.index), out.T, out.u, out.U,
+                int(out.n_feasible), int(out.n_scanned), list(out.hist))
