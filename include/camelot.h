@@ -186,8 +186,11 @@ typedef struct {
     int32_t gpus_used;        /* u                                                   */
     int32_t eq2_gpus;         /* y (Eq. 2, R9) at this load level; 0 for max-load    */
     uint32_t violations;      /* first failing check of this plan (0 = feasible);
-                                 for INFEASIBLE results: OR of first-failing checks
-                                 seen (exact in CAMELOT_F_NO_FILTER mode)            */
+                                 for INFEASIBLE results: OR of the first-failing checks
+                                 of the scanned candidates (placement bits = the
+                                 dimensions where fits(g, 1) fails after pass 2,
+                                 DESIGN.md 3.2); exact in CAMELOT_F_NO_FILTER mode, a
+                                 subset when bounds skip candidates                  */
     uint64_t n_feasible;      /* feasible candidates seen (exact in NO_FILTER mode)  */
     uint64_t n_scored;        /* candidates fully scored by the search               */
     uint64_t n_covered;       /* candidates covered (scored or excluded by a bound)  */
@@ -232,6 +235,13 @@ int camelot_predict(const camelot_problem *p, const camelot_cluster *c,
                     const float *load_qps, int n_loads,
                     const camelot_exec *exec, camelot_plan *out);
 
+/* Score ONE candidate given by its canonical index (0 <= index < Ntot, else
+ * CAMELOT_EINVAL): the device decodes the mixed-radix digits (beta_a, rho_i,
+ * theta_i; CANONICAL INDEX above) and scores the plan as
+ * camelot_predict does.  load_qps [1][A] may be NULL (n_loads = 0). */
+int camelot_predict_index(const camelot_problem *p, const camelot_cluster *c, uint64_t index,
+                          const float *load_qps, int n_loads, const camelot_exec *exec, camelot_plan *out);
+
 /* Score every candidate of [lo, hi) (hi - lo <= 2^31) on the device.
  * Device outputs (any may be NULL): d_verdict u8 [hi-lo] first failing check
  * (max-load), d_T f32 [hi-lo], d_u i32, d_U i32.  Asynchronous. */
@@ -248,7 +258,13 @@ int camelot_score_range(const camelot_problem *p, const camelot_cluster *c,
  *     torch.distributed.all_reduce(keys, op=MIN)
  * every rank calls camelot_finalize with the reduced DEVICE keys; it recovers
  * the exact winning index (re-scanning the winning chunk when Ntot > 2^32),
- * scores it and writes the plans to host out[n_keys]. */
+ * scores it and writes the plans to host out[n_keys].
+ * Pairing contract: camelot_finalize reads what the LAST camelot_search_local
+ * left in the same workspace (local best, filtered option lists, loads), so it
+ * must be called with the same problem, policy, n_loads, load_qps, index range,
+ * rank and world, and no other call that rewrites the workspace in between
+ * (any entry point other than camelot_finalize / camelot_last_stats /
+ * camelot_trace does); otherwise it returns CAMELOT_EINVAL. */
 int camelot_search_local(const camelot_problem *p, const camelot_cluster *c, int policy,
                          const float *load_qps, int n_loads, const camelot_exec *exec,
                          int64_t *d_keys);

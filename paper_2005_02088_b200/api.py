@@ -167,21 +167,18 @@ class Session:
         return _plan(out, self.n, self.A)
 
     def predict_index(self, x: int, loads=None) -> PlanResult:
-        """camelot_predict of the candidate with canonical index x (digits decoded here)."""
-        p = self.problem
-        nQ, nS, R = len(p.quota_pct), len(p.batch), int(p.max_replicas)
-        theta, rho = [0] * self.n, [0] * self.n
-        for i in range(self.n - 1, -1, -1):
-            theta[i] = x % nQ
-            x //= nQ
-            rho[i] = x % R
-            x //= R
-        beta = [0] * self.A
-        for a in range(self.A - 1, -1, -1):
-            beta[a] = x % nS
-            x //= nS
-        return self.predict([int(p.batch[b]) for b in beta], [r + 1 for r in rho],
-                            [int(p.quota_pct[t]) for t in theta], loads)
+        """camelot_predict_index: score the candidate with canonical index x (the
+        library decodes the digits on the device)."""
+        out = L.Plan()
+        if loads is not None:
+            arr, _ = self._loads(loads)
+            lp, nl = arr.ctypes.data_as(C.POINTER(C.c_float)), 1
+        else:
+            lp, nl = None, 0
+        ex = self.exec()
+        L.check(L.lib().camelot_predict_index(C.byref(self.cprob), C.byref(self.ccl), int(x), lp, nl,
+                                              C.byref(ex), C.byref(out)))
+        return _plan(out, self.n, self.A)
 
     def score_range(self, lo: int, hi: int):
         """Device vectors (verdict u8, T f32, u i32, U i32) of every candidate in [lo, hi)."""

@@ -13,6 +13,7 @@
 #include <atomic>
 #include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/camelot.h"
@@ -38,6 +39,18 @@ struct EvPair {
     bool armed = false;
 };
 thread_local EvPair t_ev;
+
+// What the last camelot_search_local left in a workspace: camelot_finalize reads
+// that state (local best, filter records, loads, Eq. 2 estimates), so it must be
+// called with the same policy, levels, range, shard and problem size (camelot.h).
+struct SearchRecord {
+    int policy = -1, nlev = 0, rank = 0, world = 1;
+    unsigned long long lo = 0, hi = 0, ntot = 0;
+    uint32_t flags = 0;
+    std::vector<float> loads;
+};
+std::mutex g_rec_mu;
+std::unordered_map<const void *, SearchRecord> g_rec;
 
 int fail(int code, const char *fmt, ...) {
     char buf[512];
@@ -335,6 +348,10 @@ int setup(const camelot_problem *p, const camelot_cluster *c, const camelot_exec
         return fail(CAMELOT_ENOMEM, "workspace too small: %zu < %zu bytes", ex->workspace_bytes, X.L.total);
     X.ws = static_cast<char *>(ex->workspace);
     X.st = static_cast<cudaStream_t>(ex->stream);
+    if (upload) {   // this call rewrites the workspace: a pending finalize would read stale state
+        std::lock_guard<std::mutex> g(g_rec_mu);
+        g_rec.erase(ex->workspace);
+    }
     X.P = make_devprob(p, c, X.d, X.ws, X.L);
     X.d0 = choose_d0(X.d);
     X.cm16 = X.d.C > 8;
@@ -948,7 +965,20 @@ int camelot_search_local(const camelot_problem *p, const camelot_cluster *c, int
     if (rc) return rc;
     rc = upload_loads(X, load_qps, policy == 1 ? n_loads : 0);
     if (rc) return rc;
-    return local_search(X, ex, policy, nlev, reinterpret_cast<long long *>(d_keys));
+    rc = local_search(X, ex, policy, nlev, reinterpret_cast<long long *>(d_keys));
+    if (rc) return rc;
+    SearchRecord r;
+    r.policy = policy;
+    r.nlev = nlev;
+    r.rank = ex->rank;
+    r.world = ex->world;
+    range_of(X, ex, r.lo, r.hi);
+    r.ntot = X.d.ntot;
+    r.flags = p->flags;
+    if (policy == 1) r.loads.assign(load_qps, load_qps + (size_t)n_loads * p->n_apps);
+    std::lock_guard<std::mutex> g(g_rec_mu);
+    g_rec[ex->workspace] = std::move(r);
+    return CAMELOT_OK;
 }
 
 int camelot_finalize(const camelot_problem *p, const camelot_cluster *c, int policy, const float *load_qps,
@@ -957,9 +987,29 @@ int camelot_finalize(const camelot_problem *p, const camelot_cluster *c, int pol
     if (policy != 0 && policy != 1) return fail(CAMELOT_EINVAL, "bad policy");
     if (!out || !d_keys) return fail(CAMELOT_EINVAL, "null out or keys");
     const int nlev = policy == 0 ? 1 : n_loads;
+    if (policy == 1) {
+        int rc = p ? check_loads(p, load_qps, n_loads) : fail(CAMELOT_EINVAL, "null problem");
+        if (rc) return rc;
+    }
     Ctx X;
     int rc = setup(p, c, ex, nlev, X, false);
     if (rc) return rc;
+    {
+        // the pairing contract with camelot_search_local (camelot.h)
+        unsigned long long lo, hi;
+        range_of(X, ex, lo, hi);
+        std::lock_guard<std::mutex> g(g_rec_mu);
+        auto it = g_rec.find(ex->workspace);
+        if (it == g_rec.end()) return fail(CAMELOT_EINVAL, "finalize: no camelot_search_local on this workspace");
+        const SearchRecord &r = it->second;
+        if (r.policy != policy || r.nlev != nlev || r.rank != ex->rank || r.world != ex->world || r.lo != lo ||
+            r.hi != hi || r.ntot != X.d.ntot || r.flags != p->flags)
+            return fail(CAMELOT_EINVAL, "finalize: policy/levels/range/shard differ from the last camelot_search_local "
+                                        "on this workspace");
+        if (policy == 1 && (r.loads.size() != (size_t)n_loads * p->n_apps ||
+                            memcmp(r.loads.data(), load_qps, r.loads.size() * sizeof(float)) != 0))
+            return fail(CAMELOT_EINVAL, "finalize: load_qps differ from the last camelot_search_local");
+    }
     return finalize_impl(X, ex, policy, nlev, reinterpret_cast<const long long *>(d_keys), out);
 }
 
@@ -998,34 +1048,47 @@ int camelot_predict(const camelot_problem *p, const camelot_cluster *c, const in
                     camelot_plan *out) {
     t_call_launches = 0;
     if (!out || !batch || !replicas || !quota_pct) return fail(CAMELOT_EINVAL, "null argument");
+    Dims d;
+    int rc = check_problem(p, c, d);
+    if (rc) return rc;
+    // explicit plan values -> canonical digits (strictly on the grids) -> index
+    unsigned long long x = 0;
+    for (int a = 0; a < d.A; ++a) {
+        int b = -1;
+        for (int k = 0; k < d.nS; ++k)
+            if (p->batch[k] == batch[a]) b = k;
+        if (b < 0) return fail(CAMELOT_EINVAL, "batch %d of app %d is not on the batch grid", batch[a], a);
+        x = x * d.nS + b;
+    }
+    for (int i = 0; i < d.n; ++i) {
+        if (replicas[i] < 1 || replicas[i] > d.Rmax) return fail(CAMELOT_EINVAL, "replicas[%d] not in 1..Rmax", i);
+        int t = -1;
+        for (int k = 0; k < d.nQ; ++k)
+            if (p->quota_pct[k] == quota_pct[i]) t = k;
+        if (t < 0) return fail(CAMELOT_EINVAL, "quota %d of stage %d is not on the quota grid", quota_pct[i], i);
+        x = x * d.Rmax + (replicas[i] - 1);
+        x = x * d.nQ + t;
+    }
+    return camelot_predict_index(p, c, x, load_qps, n_loads, ex, out);
+}
+
+int camelot_predict_index(const camelot_problem *p, const camelot_cluster *c, uint64_t index, const float *load_qps,
+                          int n_loads, const camelot_exec *ex, camelot_plan *out) {
+    t_call_launches = 0;
+    if (!out) return fail(CAMELOT_EINVAL, "null out");
     Ctx X;
     int rc = setup(p, c, ex, 1, X, true);
     if (rc) return rc;
+    if (index >= X.d.ntot) return fail(CAMELOT_EINVAL, "index %llu >= Ntot %llu", (unsigned long long)index, X.d.ntot);
     if (n_loads > 0) {
         rc = check_loads(p, load_qps, 1);
         if (rc) return rc;
         rc = upload_loads(X, load_qps, 1);
         if (rc) return rc;
     }
-    unsigned long long x = 0;
-    for (int a = 0; a < X.d.A; ++a) {
-        int b = -1;
-        for (int k = 0; k < X.d.nS; ++k)
-            if (p->batch[k] == batch[a]) b = k;
-        if (b < 0) return fail(CAMELOT_EINVAL, "batch %d of app %d is not on the batch grid", batch[a], a);
-        x = x * X.d.nS + b;
-    }
-    for (int i = 0; i < X.d.n; ++i) {
-        if (replicas[i] < 1 || replicas[i] > X.d.Rmax) return fail(CAMELOT_EINVAL, "replicas[%d] not in 1..Rmax", i);
-        int t = -1;
-        for (int k = 0; k < X.d.nQ; ++k)
-            if (p->quota_pct[k] == quota_pct[i]) t = k;
-        if (t < 0) return fail(CAMELOT_EINVAL, "quota %d of stage %d is not on the quota grid", quota_pct[i], i);
-        x = x * X.d.Rmax + (replicas[i] - 1);
-        x = x * X.d.nQ + t;
-    }
+    // the device decodes the canonical index (mixed radix, step A2) and scores it
     camelot_plan *dplans = reinterpret_cast<camelot_plan *>(X.ws + X.L.plans);
-    predict_kernel<<<1, 1, 0, X.st>>>(X.P, x, n_loads > 0 ? reinterpret_cast<const float *>(X.ws + X.L.lam) : nullptr,
+    predict_kernel<<<1, 1, 0, X.st>>>(X.P, index, n_loads > 0 ? reinterpret_cast<const float *>(X.ws + X.L.lam) : nullptr,
                                       n_loads > 0 ? 1 : 0, dplans);
     COUNT_LAUNCH();
     CU(cudaGetLastError());

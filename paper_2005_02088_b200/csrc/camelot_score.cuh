@@ -159,8 +159,11 @@ __device__ void score_digits(const DevProb &P, const int *beta, const int *rho, 
                 }
             }
             if (rem > 0) {
+                // first-failing dimensions AFTER pass 2 (DESIGN.md 3.2 step 5): fits(g, 1)
+                // on the updated state, weights charged only where stage i is not yet hosted
                 uint32_t v = 0;
-                for (int g = 0; g < C; ++g) v |= fit_viol(P, rq[g], cnt[g], rm[g], dem[g], 1, p, W, As, bw);
+                for (int g = 0; g < C; ++g)
+                    v |= fit_viol(P, rq[g], cnt[g], rm[g], dem[g], 1, p, hcnt[i][g] ? 0u : W, As, bw);
                 pv = v ? v : V_QUOTA;
             }
         }

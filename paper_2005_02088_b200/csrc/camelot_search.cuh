@@ -208,17 +208,25 @@ __device__ __forceinline__ bool place_stage(const DevProb &P, const Node<CM> &nd
     return rem == 0;
 }
 
-// first-failing placement dimensions of a failed stage (OR over GPUs of fits(g,1) failures)
+// First-failing placement dimensions of a failed stage (DESIGN.md 3.2 step 5):
+// the OR over GPUs of the dimensions in which fits(g, 1) fails AFTER pass 2.  A
+// failed pass 2 leaves every GPU at its capacity c = canHold(g, Rmax) (< the
+// replicas still to place), and on that state fits(g, 1) fails exactly in the
+// integer dimensions where fits(g, c + 1) fails on the parent state (the stage's
+// weights are charged once), and in bandwidth iff fl(fl(dem + fl(c bw)) + bw) > BW.
 template <int CM>
 __device__ __forceinline__ uint32_t place_fail_bits(const DevProb &P, const Node<CM> &nd, const OptRec &r) {
+    const bool cap = !(P.flags & F_NO_BW_CAP);
     uint32_t v = 0;
     for (int q = 0; q < P.C; ++q) {
-        if ((int)r.p > nd.prq[q]) v |= V_QUOTA;
-        int g = nd.pgid[q];
-        (void)g;
-        if (nd.pcnt[q] + 1 > P.I) v |= V_INST;
-        if (r.W + r.As > nd.prm[q]) v |= V_MEM;
-        if (!(P.flags & F_NO_BW_CAP) && __fadd_rn(nd.pdem[q], r.bw) > P.BW) v |= V_BW;
+        int c = min((int)(((uint32_t)nd.prq[q] * r.pmul) >> 16), nd.pkim[q]);   // floor(rq / p), inst + mem
+        if (cap)
+            while (c > 0 && __fadd_rn(nd.pdem[q], __fmul_rn((float)c, r.bw)) > P.BW) --c;
+        const int k = c + 1;
+        if (k * (int)r.p > nd.prq[q]) v |= V_QUOTA;
+        if (nd.pcnt[q] + k > P.I) v |= V_INST;
+        if (r.W + (uint32_t)k * r.As > nd.prm[q]) v |= V_MEM;
+        if (cap && __fadd_rn(__fadd_rn(nd.pdem[q], __fmul_rn((float)c, r.bw)), r.bw) > P.BW) v |= V_BW;
     }
     return v ? v : V_QUOTA;
 }

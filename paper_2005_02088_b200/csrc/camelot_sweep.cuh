@@ -147,14 +147,31 @@ __device__ __forceinline__ float sw_kappa(float dmax, float bw, float gamma, flo
 }
 
 // cold paths of the leaf loop, out of line (instruction-cache footprint)
-static __device__ __noinline__ uint32_t sw_fail_bits(const DevProb &P, int p, float bw, int minrq, int maxcnt, uint32_t need,
-                                              uint32_t minrm, float maxdem, bool cap) {
-    // first-failing dimensions of a failed deployment: OR over GPUs of fits(g, 1) failures
+// First-failing dimensions of a failed deployment of the leaf stage (DESIGN.md 3.2
+// step 5): the OR over GPUs of the dimensions in which fits(g, 1) fails AFTER pass 2.
+// A failed pass 2 leaves every GPU at its capacity c_g (the popcount of its nibble of
+// the thermometer code M, in deployment order; `perm` maps a rank to the GPU id), and
+// on that state fits(g, 1) fails exactly in the integer dimensions where fits(g, c_g+1)
+// fails on the parent state (the leaf stage is new on every GPU, so its weights are
+// charged once), and in bandwidth iff fl(fl(dem + fl(c_g bw)) + bw) > BW.  The same
+// for every failing N: pass 2 fills every GPU to capacity.  The parent state is read
+// from the per-thread shared-memory copies (rq | cnt << 8, rm, dem).
+static __device__ __noinline__ uint32_t sw_fail_bits(const DevProb &P, int p, float bw, uint32_t need1, uint32_t As,
+                                              bool cap, uint32_t M, uint32_t perm, const uint32_t *rqc,
+                                              const uint32_t *rmv, const float *demv, int stride) {
     uint32_t v = 0;
-    if (p > minrq) v |= V_QUOTA;
-    if (maxcnt + 1 > P.I) v |= V_INST;
-    if (need > minrm) v |= V_MEM;
-    if (cap && __fadd_rn(maxdem, bw) > P.BW) v |= V_BW;
+    for (int r = 0; r < P.C; ++r) {
+        const int g = (perm >> (4 * r)) & 0xF;
+        const int c = __popc((M >> (4 * r)) & 0xFu);
+        const uint32_t w = rqc[g * stride];
+        const int rq = (int)(w & 0xFFu), cnt = (int)(w >> 8);
+        const float dem = demv[g * stride];
+        const int k = c + 1;
+        if (k * p > rq) v |= V_QUOTA;
+        if (cnt + k > P.I) v |= V_INST;
+        if (need1 + (uint32_t)c * As > rmv[g * stride]) v |= V_MEM;
+        if (cap && __fadd_rn(__fadd_rn(dem, __fmul_rn((float)c, bw)), bw) > P.BW) v |= V_BW;
+    }
     return v ? v : V_QUOTA;
 }
 
@@ -196,6 +213,7 @@ template <int CM, int NS, int POLICY, bool TWO, bool COMM>
 __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const DevProb P, const SweepArgs A) {
     static_assert(CM <= 8, "thermometer code holds 8 GPUs x 4 bits");
     __shared__ float dem_s[CM][SWEEP_THREADS];
+    __shared__ uint32_t rqc_s[CM][SWEEP_THREADS], rm_s[CM][SWEEP_THREADS];   // cold: failure bits
     __shared__ uint32_t qpm_s[CAMELOT_MAX_QUOTAS];   // p | ceil(2^16/p) << 7
     __shared__ unsigned long long red_k[SWEEP_THREADS / 32], red_x[SWEEP_THREADS / 32];
     __shared__ unsigned long long red_c[SWEEP_THREADS / 32][2];
@@ -321,9 +339,6 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
         int kim[CM], sh[CM];
         float hb[CM];      // bandwidth threshold: fits(k) <=> fl(k bw) <= hb
         uint32_t perm = 0u, E = 0u;
-        int minrq = 0x7fffffff, maxcnt = 0;
-        uint32_t minrm = 0xffffffffu;
-        float maxdem = 0.0f;
 #pragma unroll
         for (int g = 0; g < CM; ++g) {
             int k = 0;
@@ -333,10 +348,6 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
                 if (st.rm[g] < WL) k = 0;
                 else if (AsL > 0u) k = min(k, (int)min((uint32_t)Rmax, (st.rm[g] - WL) / AsL));
                 k = max(k, 0);
-                minrq = min(minrq, st.rq[g]);
-                maxcnt = max(maxcnt, st.cnt[g]);
-                minrm = min(minrm, st.rm[g]);
-                maxdem = fmaxf(maxdem, st.dem[g]);
                 if (st.cnt[g] == 0) E |= 1u << g;
                 hb[g] = cap ? bw_threshold(st.dem[g], P.BW) : __int_as_float(0x7f800000);
             }
@@ -356,6 +367,8 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
             sh[g] = 4 * r;
             perm |= (uint32_t)g << (4 * r);
             dem_s[g][tid] = st.dem[g];
+            rqc_s[g][tid] = (uint32_t)st.rq[g] | ((uint32_t)st.cnt[g] << 8);
+            rm_s[g][tid] = st.rm[g];
         }
         float ptub = __int_as_float(0x7f800000);
 #pragma unroll
@@ -417,7 +430,9 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
             if (nok < Rmax) {   // the failing leaves: first-failing dimensions (OR over GPUs, k = 1)
                 bool any = full;
                 for (int N = nok + 1; N <= Rmax && !any; ++N) any = (unsigned)((N - 1) * nQ + th - clo) < span;
-                if (any) viol |= sw_fail_bits(P, (int)(qp & 127u), bw, minrq, maxcnt, WL + AsL, minrm, maxdem, cap);
+                if (any)
+                    viol |= sw_fail_bits(P, (int)(qp & 127u), bw, WL + AsL, AsL, cap, M, perm, &rqc_s[0][tid],
+                                         &rm_s[0][tid], &dem_s[0][tid], SWEEP_THREADS);
             }
 #pragma unroll 1
             for (int N = 1; N <= nok; ++N) {

@@ -1,0 +1,295 @@
+"""Certification of the headline and of the failure bits (-m gpu), through the C ABI.
+
+* full C4, both policies (8.192e13 candidates each), against the oracle's O7
+  golden (tests/golden/expected_C4-full.json, make_c4_expected.py: oracle only);
+* four 2^32-candidate C4 slices against the plain oracle scan (same file), in the
+  pruned and the exhaustive (NO_FILTER) modes;
+* the sharded search (search_local + MIN + finalize) against the oracle itself;
+* the kappa-over-a-split-stage and GPUs-before-quota goldens on the device;
+* first-failing-check bits after pass 2 on memory-tight problems (score vectors,
+  camelot_predict, and the violations of INFEASIBLE NO_FILTER searches vs the OR
+  of the oracle's histogram);
+* the finalize pairing contract (camelot.h).
+"""
+import json
+import os
+import struct
+
+import numpy as np
+import pytest
+import torch
+
+from gen import problems as G
+from tests import helpers as H
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def api():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2005_02088_b200 import _lib
+    _lib.build()
+    from paper_2005_02088_b200 import api as A
+    return A
+
+
+def fb(x):
+    return struct.unpack("<I", struct.pack("<f", x))[0]
+
+
+def c4_golden():
+    path = os.path.join(GOLD, "expected_C4-full.json")
+    e = json.load(open(path))
+    prob = G.config_problems(4)[0]
+    assert prob.sha256() == e["sha256"]
+    return prob, e
+
+
+# ------------------------------------------------------------------ the headline
+def test_c4_full_golden(api, oracle):
+    """BASELINE config C4, both policies exactly as bench.py runs them, == O7."""
+    prob, e = c4_golden()
+    s = api.Session(prob, n_loads=1)
+    pm = s.plan_max_load()
+    g = e["max_load"]
+    assert pm.index == g["index"] and fb(pm.objective) == fb(g["T"])
+    assert (pm.gpus_used, pm.quota_used) == (g["u"], g["U"])
+    lam = e["min_resource"]["loads"]
+    assert lam[0][0] == 0.3 * pm.objective        # the bench's load level
+    pr = s.plan_min_resource(lam)[0]
+    g = e["min_resource"]
+    assert pr.index == g["index"] and (pr.gpus_used, pr.quota_used) == (g["u"], g["U"])
+    # the winners' full predictions == oracle_predict
+    sc = oracle.score(prob, pm.index)
+    assert [fb(v) for v in pm.stage_latency_ms] == [fb(v) for v in sc.L]
+    assert pm.gpu_of_instance == sc.gpu_of_instance
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_c4_full_sharded_golden(api, world):
+    """The multi-GPU split (search_local per rank, MIN of the keys, finalize on
+    every rank) on full C4 == O7, for several world sizes on one device."""
+    prob, e = c4_golden()
+    from paper_2005_02088_b200 import _lib as L
+    for policy, g in ((L.POLICY_MAX_LOAD, e["max_load"]), (L.POLICY_MIN_RESOURCE, e["min_resource"])):
+        loads = e["min_resource"]["loads"] if policy else None
+        sess = [api.Session(prob, n_loads=1) for _ in range(world)]
+        keys = [sess[r].search_local(policy, loads, rank=r, world=world).clone() for r in range(world)]
+        red = torch.stack(keys).min(dim=0).values
+        for r in range(world):
+            pl = sess[r].finalize(policy, red, loads, rank=r, world=world)[0]
+            assert pl.index == g["index"], (policy, world, r)
+
+
+@pytest.mark.parametrize("k", range(4))
+@pytest.mark.parametrize("mode", ["pruned", "flat"])
+def test_c4_slices_golden(api, k, mode):
+    """2^32-candidate slices of C4 == the plain oracle scan of the same slice."""
+    prob, e = c4_golden()
+    if "slices" not in e or len(e["slices"]) <= k:
+        pytest.skip("slice not generated")
+    sl = e["slices"][k]
+    flags = prob.flags | (G.F_NO_FILTER if mode == "flat" else 0)
+    s = api.Session(prob, n_loads=1, flags=flags)
+    if sl["policy"] == "max_load":
+        got = s.plan_max_load(lo=sl["lo"], hi=sl["hi"])
+        if sl["index"] is not None:
+            assert fb(got.objective) == fb(sl["T"])
+    else:
+        got = s.plan_min_resource(sl["loads"], lo=sl["lo"], hi=sl["hi"])[0]
+        if sl["index"] is not None:
+            assert (got.gpus_used, got.quota_used) == (sl["u"], sl["U"])
+    assert got.index == sl["index"], (sl["name"], mode)
+    if mode == "flat":
+        assert got.n_feasible == sl["n_feasible"]
+
+
+# ------------------------------------------------------------------ sharded == oracle
+@pytest.mark.parametrize("cfg,world,flat", [(2, 2, False), (3, 3, False), (3, 2, True), (4, 2, False),
+                                            (4, 3, True)])
+def test_sharded_equals_oracle(api, oracle, cfg, world, flat):
+    """search_local on every rank + MIN + finalize == oracle.search (C2, C3, a 3M
+    C4 slice whose Ntot > 2^32 exercises the chunk re-scan)."""
+    prob = G.config_problems(cfg)[0]
+    lo, hi = (0, 0) if cfg != 4 else (10 ** 12, 10 ** 12 + 3_000_000)
+    flags = prob.flags | (G.F_NO_FILTER if flat else 0)
+    ref = oracle.search(prob, lo=lo, hi=hi if hi else None, threads=8)[0]
+    lam = [[np.float32(0.3) * np.float32(ref.T)]]
+    refm = oracle.search(prob, "min_resource", loads=lam, lo=lo, hi=hi if hi else None, threads=8)[0]
+    from paper_2005_02088_b200 import _lib as L
+    for policy, r_ in ((L.POLICY_MAX_LOAD, ref), (L.POLICY_MIN_RESOURCE, refm)):
+        loads = lam if policy else None
+        sess = [api.Session(prob, n_loads=1, flags=flags) for _ in range(world)]
+        keys = [sess[r].search_local(policy, loads, rank=r, world=world, lo=lo, hi=hi).clone()
+                for r in range(world)]
+        red = torch.stack(keys).min(dim=0).values
+        for r in range(world):
+            pl = sess[r].finalize(policy, red, loads, rank=r, world=world, lo=lo, hi=hi)[0]
+            assert pl.index == r_.index, (cfg, world, policy, r)
+            if policy == 0:
+                assert fb(pl.objective) == fb(r_.T)
+            else:
+                assert (pl.gpus_used, pl.quota_used) == (r_.u, r_.U)
+
+
+# ------------------------------------------------------------------ goldens on the device
+@pytest.mark.parametrize("case", json.load(open(os.path.join(GOLD, "kappa_split.json")))["cases"],
+                         ids=lambda c: c["name"])
+def test_kappa_split_golden_gpu(api, case):
+    p = H.kappa_split_problem(case["bwA"])
+    s = api.Session(p)
+    g = s.predict([1], [1, 3], [50, 50])
+    assert g.violations == 0 and g.gpus_used == 2
+    assert g.kappa == case["kappa"] and g.stage_latency_ms == case["L"]
+    assert g.stage_throughput_qps == case["Ti"] and g.objective == case["T"]
+    assert g.gpu_of_instance == case["gpus"]
+    best = s.plan_max_load()
+    assert best.index == 2 and best.objective == case["T"] and best.kappa == case["kappa"]
+
+
+def test_min_resource_priority_golden_gpu(api):
+    g = json.load(open(os.path.join(GOLD, "min_resource_priority.json")))
+    p = H.min_resource_priority_problem()
+    for flags in (0, G.F_NO_FILTER):
+        r = api.Session(p, n_loads=1, flags=flags).plan_min_resource([[g["setup"]["load"]]])[0]
+        assert (r.index, r.gpus_used, r.quota_used) == (g["expect"]["index"], g["expect"]["u"], g["expect"]["U"])
+
+
+# ------------------------------------------------------------------ failure bits after pass 2
+def tight(prob, mem_mib, bw=None):
+    cl = G.Cluster(**{**prob.cluster.__dict__, "mem_mib": int(mem_mib),
+                      "bw_gbs": float(bw if bw else prob.cluster.bw_gbs)})
+    return prob.with_(cluster=cl)
+
+
+def tight_problems():
+    out = []
+    for cfg, j, mem, bw in ((2, 0, 8192, None), (2, 5, 6144, None), (2, 13, 8192, 600.0), (3, 0, 8192, None),
+                            (5, 0, 4000, None)):
+        out.append(tight(G.config_problems(cfg)[j], mem, bw))
+    out.append(tight(G.random_small_problem(77, n_stages=4, n_gpus=3, max_replicas=3, quota_step=20,
+                                            batches=(4, 16)), 7000))
+    out.append(H.kappa_split_problem(64.0).with_(cluster=H.cluster(C=2, BW=128.0, FM=10000)))
+    return out
+
+
+@pytest.mark.parametrize("k", range(7))
+def test_fail_bits_score_vectors_memory_tight(api, oracle, k):
+    """score_range / camelot_predict verdict bits == the oracle's (pass-2 state)."""
+    prob = tight_problems()[k]
+    nt = oracle.ntot(prob)
+    rng = np.random.default_rng(k)
+    w = min(nt, 60000)
+    starts = sorted({0, nt - w} | {int(v) for v in rng.integers(0, nt - w + 1, 2)})
+    s = api.Session(prob)
+    seen = 0
+    for lo in starts:
+        v, T, u, U = (t.cpu().numpy() for t in s.score_range(lo, lo + w))
+        rv, rT, ru, rU = oracle.score_range(prob, lo, lo + w)
+        np.testing.assert_array_equal(v, rv)
+        seen |= int(np.bitwise_or.reduce(rv))
+    assert seen & 15, "the problem must produce placement failures"
+    for x in rng.integers(0, nt, 100):
+        g = s.predict_index(int(x))
+        r = oracle.score(prob, int(x))
+        assert g.violations == r.verdict
+
+
+def test_fail_bits_pass2_examples(api, oracle):
+    """The two hand cases of the round-1 review: weights charged once after pass 2
+    (oracle QUOTA only), and a bandwidth failure seen only on the post-pass-2 state."""
+    # C = 2, F = 10000, one stage W = 6000, p = 60, N = 3
+    tab = H.table_from([[[1.0]]], [[[1.0]]], [[[0.0]]])
+    p1 = G.custom_problem("w2", tab, [60], [1], [1e9], H.cluster(C=2, FM=10000), max_replicas=3,
+                          weights_mib=[6000], act_mib_per_item=[0])
+    # C = 1, one replica uses 0.3 BW, N = 4, quota plentiful
+    tab = H.table_from([[[1.0]]], [[[1.0]]], [[[30.0]]])
+    p2 = G.custom_problem("bw2", tab, [10], [1], [1e9], H.cluster(C=1, BW=100.0), max_replicas=4)
+    for p, x, expect in ((p1, 2, oracle.V_QUOTA), (p2, 3, oracle.V_BW)):
+        r = oracle.score(p, x)
+        assert r.verdict == expect
+        assert api.Session(p).predict_index(x).violations == expect
+        for flags in (G.F_NO_FILTER, G.F_NO_FILTER | 0):
+            got = api.Session(p, flags=flags).plan_max_load(lo=x, hi=x + 1)
+            assert got.index is None and got.violations == expect
+
+
+def hist_or(b):
+    return sum(1 << i for i, c in enumerate(b.hist) if c)
+
+
+@pytest.mark.parametrize("k", range(7))
+def test_infeasible_no_filter_violations(api, oracle, k):
+    """INFEASIBLE NO_FILTER searches: violations == OR of the oracle histogram's
+    bits (sweep for C <= 8, tree flat mode for C > 8, naive kernel)."""
+    base = tight_problems()[k]
+    prob = base.with_(qos_ms=np.full(base.n_apps, 1e-3, np.float32))   # nothing meets QoS
+    if oracle.ntot(prob) > 3_000_000:
+        pytest.skip("space too large for the in-test oracle")
+    ref = oracle.search(prob, threads=8)[0]
+    assert ref.index is None
+    s = api.Session(prob, flags=prob.flags | G.F_NO_FILTER)
+    got = s.plan_max_load()
+    assert got.index is None and got.violations == hist_or(ref), (got.violations, ref.hist)
+    lam = [[1.0] * prob.n_apps]
+    refm = oracle.search(prob, "min_resource", loads=lam, threads=8)[0]
+    gm = api.Session(prob, n_loads=1, flags=prob.flags | G.F_NO_FILTER).plan_min_resource(lam)[0]
+    assert gm.index is None and gm.violations == hist_or(refm)
+
+
+def test_infeasible_violations_wide_and_naive(api, oracle):
+    """The tree search's flat mode (C > 8) and the naive kernel report the same bits."""
+    prob = G.random_small_problem(91, n_stages=3, n_gpus=10, max_replicas=3, quota_step=25, batches=(4,),
+                                  qos_rho=0.05)
+    prob = tight(prob, 5000)
+    ref = oracle.search(prob, threads=8)[0]
+    assert ref.index is None
+    got = api.Session(prob, flags=prob.flags | G.F_NO_FILTER).plan_max_load()
+    assert got.violations == hist_or(ref)
+    from paper_2005_02088_b200 import _lib as L
+    import ctypes as C
+    s = api.Session(prob, flags=prob.flags | G.F_NO_FILTER)
+    out = L.Plan()
+    ex = s.exec()
+    ex.exec_flags = 2   # CAMELOT_EXEC_NAIVE
+    L.check(L.lib().camelot_plan_max_load(C.byref(s.cprob), C.byref(s.ccl), C.byref(ex), C.byref(out)))
+    assert out.violations == hist_or(ref)
+
+
+# ------------------------------------------------------------------ ABI contract
+def test_predict_index_abi(api, oracle):
+    prob = G.config_problems(5)[0]
+    s = api.Session(prob)
+    nt = oracle.ntot(prob)
+    for x in (0, nt - 1, 123456789):
+        g = s.predict_index(x)
+        d = oracle.decode(prob, x)
+        assert g.index == x and g.replicas == [r + 1 for r in d[1]]
+        assert g.quota_pct == [int(prob.quota_pct[t]) for t in d[2]]
+    from paper_2005_02088_b200 import _lib as L
+    with pytest.raises(L.CamelotError):
+        s.predict_index(nt)
+
+
+def test_finalize_pairing_contract(api):
+    from paper_2005_02088_b200 import _lib as L
+    prob = G.config_problems(2)[0]
+    s = api.Session(prob, n_loads=2)
+    k = s.search_local(L.POLICY_MAX_LOAD).clone()
+    with pytest.raises(L.CamelotError):
+        s.finalize(L.POLICY_MIN_RESOURCE, k, [[1.0]])           # other policy
+    with pytest.raises(L.CamelotError):
+        s.finalize(L.POLICY_MAX_LOAD, k, lo=0, hi=1000)        # other range
+    ok = s.finalize(L.POLICY_MAX_LOAD, k)[0]
+    assert ok.index is not None
+    km = s.search_local(L.POLICY_MIN_RESOURCE, [[5.0], [9.0]]).clone()
+    with pytest.raises(L.CamelotError):
+        s.finalize(L.POLICY_MIN_RESOURCE, km, [[5.0], [9.5]])  # other loads
+    with pytest.raises(L.CamelotError):
+        s.finalize(L.POLICY_MIN_RESOURCE, km, [[5.0]])         # other level count
+    s.predict_index(0)                                          # rewrites the workspace
+    with pytest.raises(L.CamelotError):
+        s.finalize(L.POLICY_MIN_RESOURCE, km, [[5.0], [9.0]])
