@@ -10,14 +10,19 @@ search of the whole space; value = candidates covered per second
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
-N > 1: launched by torchrun, one rank per GPU; every rank searches its shard
+N > 1: one rank per GPU (bench.py re-launches itself under
+torch.distributed.run when WORLD_SIZE is unset); every rank searches its shard
 (chunk c -> rank c mod N) and ONE all_reduce(MIN) of packed int64 keys per
-policy goes over NCCL.  --impl reference times the CPU oracle (oracle/) on a
-bounded slice of the same workload on the host cores.
+policy goes over NCCL.  With fewer visible GPUs than ranks (e.g. proving the
+launcher on a 1-GPU lease) the ranks share devices and the keys go over gloo
+(--backend gloo; NCCL forbids two ranks on one device).  --impl reference
+times the CPU oracle (oracle/) on a bounded slice of the same workload on the
+host cores.
 """
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -32,6 +37,7 @@ UNIT = "candidates/s"
 WORKLOAD = "C4: 5-stage p1-c2-m2-c3-m1 pipeline, 8 modeled V100 (BW 897 GB/s), 1% quota grid, " \
            "batch 1..128 (pow2), <=4 replicas/stage; max-load then min-resource at 0.3*T*"
 LOW_LOAD = 0.3   # low load = 30% of the peak
+TRAFFIC_CSV = "r01_v13_ncu_search_raw.csv"   # committed ncu --set full capture of the search launches
 
 
 def ncu_traffic(name, launches_per_step=None):
@@ -113,13 +119,39 @@ def dist_env():
     return rank, world, local
 
 
-def cpu_reference_leg(prob, args, rank, world, as_main):
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def maybe_relaunch(args):
+    """--gpus N > 1 without a torchrun environment: re-launch this script with
+    N ranks on this node (the driver's own launch sets WORLD_SIZE itself)."""
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "camelot":
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def cpu_reference_leg(prob, args, as_main):
     """The CPU oracle (plain exhaustive scan, as it stands) on a bounded slice of
-    the workload, on the host cores.  Returns the JSON fields."""
+    the workload: on all host cores, and single-threaded.  Returns the JSON fields."""
     from oracle import oracle as O
     threads = os.cpu_count() or 1
     nt = O.ntot(prob)
-    # size a slice for ~2 s per step (probe the rate first)
     lo = nt // 3
     t0 = time.perf_counter()
     O.search(prob, lo=lo, hi=lo + 200_000, threads=threads)
@@ -132,14 +164,20 @@ def cpu_reference_leg(prob, args, rank, world, as_main):
     for s in range(warm + steps):
         a = lo + s * n
         t0 = time.perf_counter()
-        b_ = O.search(prob, lo=a, hi=a + n, threads=threads)[0]
+        O.search(prob, lo=a, hi=a + n, threads=threads)
         dt = time.perf_counter() - t0
         if s >= warm:
             times.append(dt)
     rate = n * len(times) / sum(times)
-    sample = f"max-load exhaustive scan of {n} consecutive C4 candidates per step from index {lo} " \
-             f"(one policy; full C4 = 2 x {nt:.4g} candidates)"
+    # single thread on a smaller sample of the same slice
+    n1 = int(max(20_000, min(2e8, rate0 / threads * args.cpu1_seconds)))
+    t0 = time.perf_counter()
+    O.search(prob, lo=lo, hi=lo + n1, threads=1)
+    rate1 = n1 / (time.perf_counter() - t0)
+    sample = f"max-load exhaustive scan of {n} consecutive C4 candidates per step from index {lo} on {threads} " \
+             f"threads, and of {n1} candidates on 1 thread (one policy; full C4 = 2 x {nt:.4g} candidates)"
     return dict(value=rate, unit=UNIT, cores=threads, kind="oracle", sample=sample,
+                single_thread_value=rate1, cpu_model=cpu_model(),
                 ms_per_step=1000 * statistics.mean(times), n_per_step=n)
 
 
@@ -150,7 +188,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="camelot", choices=["camelot", "reference"])
     ap.add_argument("--config", type=int, default=4, help="BASELINE config (default 4 = C4)")
+    ap.add_argument("--backend", default=None, choices=["nccl", "gloo"],
+                    help="key all-reduce backend (default: nccl with one GPU per rank, else gloo)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="cpu_baseline sample budget")
+    ap.add_argument("--cpu1-seconds", type=float, default=4.0, help="single-thread oracle sample budget")
     ap.add_argument("--ref-seconds", type=float, default=8.0, help="--impl reference seconds per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -158,12 +199,14 @@ def main():
     ap.add_argument("--no-sa", action="store_true", help="skip the simulated-annealing baseline")
     ap.add_argument("--no-comm", action="store_true", help="skip the NEXT-2 communication-aware leg")
     ap.add_argument("--no-sim", action="store_true", help="skip the NEXT-4 tail-simulation leg")
+    ap.add_argument("--no-hard", action="store_true", help="skip the second C4 instance (C4b)")
     ap.add_argument("--sa-chains", type=int, default=4096)
     ap.add_argument("--sa-iters", type=int, default=500)
     ap.add_argument("--flat-config", type=int, default=4, help="config of the flat scan (4 = C4)")
     ap.add_argument("--flat-slice", type=int, default=1 << 31, help="candidates of the flat-scan slice (0 = all)")
     args = ap.parse_args()
     assert args.warmup >= 3 or args.impl == "reference", "timing rules: >= 3 warm-up steps"
+    maybe_relaunch(args)
 
     from gen import problems as G
     prob = G.config_problems(args.config)[0]
@@ -172,7 +215,7 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        r = cpu_reference_leg(prob, args, rank, world, as_main=True)
+        r = cpu_reference_leg(prob, args, as_main=True)
         line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT,
                 "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "strong",
@@ -180,7 +223,8 @@ def main():
                 "config": {"workload": WORKLOAD, "problem": prob.name, "sha256": prob.sha256(),
                            "l2": "n/a (CPU)"},
                 "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "oracle",
-                                 "sample": r["sample"]},
+                                 "sample": r["sample"], "single_thread_value": r["single_thread_value"],
+                                 "cpu_model": r["cpu_model"]},
                 "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
@@ -190,94 +234,146 @@ def main():
     from paper_2005_02088_b200 import _lib as L
     from paper_2005_02088_b200 import api
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    ndev = torch.cuda.device_count()
+    backend = args.backend or ("nccl" if ndev >= world else "gloo")
+    dev_idx = local % max(1, ndev)
+    torch.cuda.set_device(dev_idx)
+    dev = torch.device("cuda", dev_idx)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     stream = torch.cuda.current_stream(dev)
-    sess = api.Session(prob, device=local, n_loads=1)
+    sess = api.Session(prob, device=dev_idx, n_loads=1)
     sess.upload()
     torch.cuda.synchronize()
-    ntot = 1
-    for _ in range(prob.n_apps):
-        ntot *= len(prob.batch)
-    for _ in range(prob.n_stages):
-        ntot *= prob.max_replicas * len(prob.quota_pct)
+
+    def ntot_of(p):
+        t = 1
+        for _ in range(p.n_apps):
+            t *= len(p.batch)
+        for _ in range(p.n_stages):
+            t *= p.max_replicas * len(p.quota_pct)
+        return t
+
+    ntot = ntot_of(prob)
 
     def all_reduce_min(keys):
+        """THE collective of the path: one all_reduce(MIN) of the packed keys."""
         if world > 1:
-            dist.all_reduce(keys, op=dist.ReduceOp.MIN)
+            if backend == "nccl":
+                dist.all_reduce(keys, op=dist.ReduceOp.MIN)
+            else:   # gloo: host-staged (ranks may share one device)
+                h = keys.cpu()
+                dist.all_reduce(h, op=dist.ReduceOp.MIN)
+                keys.copy_(h)
 
-    def step(resident=True, stats=True):
-        """Both policies, whole hot path: search shard -> allreduce -> finalize."""
-        k1 = sess.search_local(L.POLICY_MAX_LOAD, rank=rank, world=world, resident=resident)
+    def max_over_ranks(v):
+        t = torch.tensor([float(v)], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def step(s_, p_, resident=True, marks=None):
+        """Both policies, whole hot path: search shard -> allreduce -> finalize.
+        marks: optional list collecting CUDA events between the phases."""
+        def mark():
+            if marks is not None:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(stream)
+                marks.append(e)
+        mark()
+        k1 = s_.search_local(L.POLICY_MAX_LOAD, rank=rank, world=world, resident=resident)
+        mark()
         all_reduce_min(k1)
-        pm = sess.finalize(L.POLICY_MAX_LOAD, k1, rank=rank, world=world)[0]
-        st1 = sess.last_stats() if stats else None
-        lam = [[LOW_LOAD * pm.objective] * prob.n_apps]
-        k2 = sess.search_local(L.POLICY_MIN_RESOURCE, lam, rank=rank, world=world, resident=True)
+        mark()
+        pm = s_.finalize(L.POLICY_MAX_LOAD, k1, rank=rank, world=world)[0]
+        mark()
+        lam = [[LOW_LOAD * pm.objective] * p_.n_apps]
+        k2 = s_.search_local(L.POLICY_MIN_RESOURCE, lam, rank=rank, world=world, resident=True)
+        mark()
         all_reduce_min(k2)
-        pr = sess.finalize(L.POLICY_MIN_RESOURCE, k2, lam, rank=rank, world=world)[0]
-        st2 = sess.last_stats() if stats else None
-        return pm, pr, st1, st2
+        mark()
+        pr = s_.finalize(L.POLICY_MIN_RESOURCE, k2, lam, rank=rank, world=world)[0]
+        mark()
+        return pm, pr
 
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
 
     for _ in range(args.warmup):
-        step()
+        step(sess, prob)
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    barrier()
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    kt = []
+    wall = []
     launches0 = L.lib().camelot_kernel_launches()
     plans = []
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev_idx) as clk:
         torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
+        barrier()
         for s in range(args.steps):
             flush.fill_(s & 0xFF)            # L2 flush between timed steps (not timed)
+            t0 = time.perf_counter()
             ev[s][0].record(stream)
-            pm, pr, st1, st2 = step(stats=False)   # no diagnostic syncs inside the timed region
+            pm, pr = step(sess, prob)        # plans land in host memory (finalize synchronises)
             ev[s][1].record(stream)
+            wall.append((time.perf_counter() - t0) * 1e3)
             plans.append((pm, pr))
-            # the search's device time and evaluation count come back in the plans
-            kt.append(({"cum_scored": pm.n_evaluated, "cum_nodes": 0, "t_ns": pm.search_ns},
-                       {"cum_scored": pr.n_evaluated, "cum_nodes": 0, "t_ns": pr.search_ns}))
         torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
+        barrier()
     launches = (L.lib().camelot_kernel_launches() - launches0) / args.steps
     ms = [a.elapsed_time(b) for a, b in ev]
-    ms_step = statistics.mean(ms)
-    t_local = torch.tensor([ms_step], device=dev, dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
-    ms_step = float(t_local.item())
+    ms_step = max_over_ranks(statistics.mean(ms))
+    ms_med, ms_min = max_over_ranks(statistics.median(ms)), max_over_ranks(min(ms))
+    wall_med, wall_min = max_over_ranks(statistics.median(wall)), max_over_ranks(min(wall))
     covered = 2 * ntot
     value = covered / (ms_step / 1000.0)
+    # the search's device time and evaluation count come back in the plans
+    evals = sum(pm.n_evaluated + pr.n_evaluated for pm, pr in plans) / args.steps
+    k_ns = sum(pm.search_ns + pr.search_ns for pm, pr in plans) / args.steps
+
+    # fixed costs per N: one instrumented step, CUDA events between the phases
+    marks = []
+    flush.fill_(0)
+    barrier()
+    step(sess, prob, marks=marks)
+    torch.cuda.synchronize()
+    names = ["search_local_max_load", "allreduce_max_load", "finalize_max_load",
+             "search_local_min_resource", "allreduce_min_resource", "finalize_min_resource"]
+    phases = {nm: max_over_ranks(marks[i].elapsed_time(marks[i + 1])) for i, nm in enumerate(names)}
+    tr = sess.trace()   # the min-resource search of that step: cascade levels vs main pass
+    starts = [ns for t, ns in tr if t == 0]
+    ends = [ns for t, ns in tr if t < 64]
+    if len(starts) >= 1 and ends:
+        phases["min_resource_coop_cascade_levels_ms"] = (starts[-1] - starts[0]) / 1e6
+        phases["min_resource_coop_main_pass_ms"] = (ends[-1] - starts[-1]) / 1e6
+    phases["note"] = ("device time per phase of one step (max over ranks); search_local = incumbent cascade "
+                      "(replicated on every rank) + this rank's shard of the main pass; finalize = resolve + "
+                      "chunk re-scan (Ntot > 2^32, N > 1) + plan scoring + D2H")
 
     # e2e: through the public API with the problem copied from pinned host
     # memory every step (not resident) and the plans read back to the host
     e2e = None
     if not args.no_e2e:
         for _ in range(2):
-            step(resident=False)
+            step(sess, prob, resident=False)
         torch.cuda.synchronize()
+        barrier()
         ee = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
         for s in range(args.steps):
             flush.fill_(s & 0xFF)
             ee[s][0].record(stream)
-            step(resident=False)
+            step(sess, prob, resident=False)
             ee[s][1].record(stream)
         torch.cuda.synchronize()
-        e_ms = statistics.mean(a.elapsed_time(b) for a, b in ee)
-        t_e = torch.tensor([e_ms], device=dev, dtype=torch.float64)
-        if world > 1:
-            dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
-        e_ms = float(t_e.item())
+        barrier()
+        e_ms = max_over_ranks(statistics.mean(a.elapsed_time(b) for a, b in ee))
         h2d = prob.table.nbytes + prob.quota_pct.nbytes + prob.batch.nbytes + 4 * prob.n_apps
         d2h = 2 * C_sizeof_plan()
         e2e = {"value": covered / (e_ms / 1000.0), "unit": UNIT, "ms_per_step": e_ms,
@@ -289,60 +385,105 @@ def main():
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
     clocks = clk.summary()
     ops_per_eval = algorithmic_ops_per_eval(prob)
-    evals = sum(s1["cum_scored"] + s1["cum_nodes"] + s2["cum_scored"] + s2["cum_nodes"] for s1, s2 in kt) / args.steps
-    k_ns = sum(s1["t_ns"] + s2["t_ns"] for s1, s2 in kt) / args.steps
     achieved = ops_per_eval * evals / (k_ns * 1e-9) / 1e12 if k_ns else None
     peak = n_sm * 4 * 32 * sm_max * 1e6 / 1e12          # lane-instructions/s (issue bound)
-    traffic, traffic_src = ncu_traffic("r01_v13_ncu_search_raw.csv", 2)   # one launch per policy
+    traffic, traffic_src = ncu_traffic(TRAFFIC_CSV, 2)   # one launch per policy
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s",
             "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-            "traffic_note": f"DRAM bytes read+written per step (sum over the search-level launches of one step) "
+            "traffic_note": f"DRAM bytes read+written per step (sum over the search launches of one step) "
                             f"from the committed ncu --set full capture {traffic_src}; algorithmic bytes ~0 "
                             f"(64 KB of tables, L2/SMEM resident)" if traffic else None,
-            "kernel": "search_kernel + filter (incumbent cascade and main pass, both policies)",
+            "kernel": "pruned search (incumbent cascade and main pass, both policies)",
             "ops_per_eval": ops_per_eval, "evals_per_step": evals,
             "kernel_ms_per_step": k_ns / 1e6,
             "kernel_share_of_step": (k_ns / 1e6) / ms_step if ms_step else None,
             "peak_note": f"{n_sm} SMs x 4 SMSP x 32 lanes x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)"}
 
     # flat exhaustive scan (NO_FILTER: every candidate placed and scored, no
-    # pruning) of C4r: the sustained hot loop, for the issue-roofline view
+    # pruning), sharded like the main search: chunks dealt round-robin over the
+    # ranks, ONE allreduce-min, finalize.  The sustained hot loop, for the
+    # issue-roofline view and the near-linear scaling leg.
     flat = None
-    if not args.no_flat and rank == 0:
+    if not args.no_flat:
         fp = G.config_problems(args.flat_config)[0]
-        fs = api.Session(fp, device=local, flags=fp.flags | L.F_NO_FILTER)
-        fnt = 1
-        for _ in range(fp.n_apps):
-            fnt *= len(fp.batch)
-        for _ in range(fp.n_stages):
-            fnt *= fp.max_replicas * len(fp.quota_pct)
-        # a slice of the canonical index space (the full C4 flat scan is 8.2e13)
+        fs = api.Session(fp, device=dev_idx, flags=fp.flags | L.F_NO_FILTER)
+        fnt = ntot_of(fp)
         flo = (fnt // 3) - (fnt // 3) % (fp.max_replicas * len(fp.quota_pct))
         fhi = min(fnt, flo + args.flat_slice) if args.flat_slice else fnt
-        fs.plan_max_load(lo=flo, hi=fhi)
-        fts, fev, fsc = [], [], []
+
+        def flat_step():
+            k = fs.search_local(L.POLICY_MAX_LOAD, rank=rank, world=world, lo=flo, hi=fhi)
+            all_reduce_min(k)
+            return k
+
+        for _ in range(2):
+            k = flat_step()
+            fr = fs.finalize(L.POLICY_MAX_LOAD, k, rank=rank, world=world, lo=flo, hi=fhi)[0]
+        torch.cuda.synchronize()
+        fts, fsc, fk = [], [], []
         for _ in range(3):
-            fr = fs.plan_max_load(lo=flo, hi=fhi)
-            st = fs.last_stats()
-            fts.append(st["t_ns"])
-            fev.append(st["cum_scored"] + st["cum_nodes"])
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            k = flat_step()
+            e1.record(stream)
+            st = fs.last_stats()      # this rank's scored leaves and kernel time (synchronises)
+            fts.append(e0.elapsed_time(e1))
+            fk.append(st["t_ns"] / 1e6)
             fsc.append(st["cum_scored"])
-        ft = statistics.median(fts) * 1e-9
-        fnt = fhi - flo
+        fr = fs.finalize(L.POLICY_MAX_LOAD, k, rank=rank, world=world, lo=flo, hi=fhi)[0]
+        ft_local = statistics.median(fts)
+        ft = max_over_ranks(ft_local)
+        scored_local = statistics.median(fsc)
+        scored_all = scored_local
+        if world > 1:
+            t = torch.tensor([scored_local], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
+            dist.all_reduce(t)
+            scored_all = float(t.item())
         fops = algorithmic_ops_per_eval(fp)
-        fach = fops * statistics.median(fev) / ft / 1e12
+        kern = max_over_ranks(statistics.median(fk))
+        fach = fops * scored_all / world / (kern * 1e-3) / 1e12
         flat = {"workload": f"{fp.name} max-load, NO_FILTER exhaustive scan of indices [{flo}, {fhi}) "
-                            f"({fnt:.4g} candidates)",
-                "index": fr.index, "ms": ft * 1e3, "candidates_per_s": fnt / ft,
-                "leaves_scored_per_s": statistics.median(fsc) / ft,
+                            f"({fhi - flo:.4g} candidates), sharded over {world} rank(s)",
+                "index": fr.index, "ms": ft, "candidates_per_s": (fhi - flo) / (ft * 1e-3),
+                "leaves_scored_per_s": scored_all / (ft * 1e-3),
+                "per_rank_leaves_scored_per_s": scored_local / (ft_local * 1e-3),
                 "roofline": {"bound": "alu", "achieved": fach, "peak": peak, "unit": "Tops/s",
-                             "frac": fach / peak, "ops_per_eval": fops}}
+                             "frac": fach / peak, "ops_per_eval": fops,
+                             "note": "per GPU: leaf evaluations x ops_per_eval / sweep kernel time"}}
+
+    # a second C4 instance where pruning is harder (other draws, QoS 0.8x): C4b
+    hard = None
+    if not args.no_hard:
+        hp = G.config_problems(7)[0]
+        hs = api.Session(hp, device=dev_idx, n_loads=1)
+        for _ in range(3):
+            step(hs, hp)
+        torch.cuda.synchronize()
+        hms, hev = [], []
+        for s in range(max(3, min(args.steps, 10))):
+            flush.fill_(s & 0xFF)
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            hm, hr = step(hs, hp)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            hms.append(e0.elapsed_time(e1))
+            hev.append(hm.n_evaluated + hr.n_evaluated)
+        hmed = max_over_ranks(statistics.median(hms))
+        hard = {"problem": hp.name, "sha256": hp.sha256(), "ms_per_step_median": hmed,
+                "ms_per_step_min": max_over_ranks(min(hms)),
+                "candidates_per_s": 2 * ntot_of(hp) / (hmed * 1e-3), "evals_per_step": statistics.median(hev),
+                "max_load": {"index": hm.index, "T": hm.objective},
+                "min_resource": {"index": hr.index, "gpus_used": hr.gpus_used, "quota_used": hr.quota_used}}
 
     # the paper's own solver (simulated annealing, NEXT-1) on the same device:
     # time and quality against the exact plans of this step
+    pm, pr = plans[-1]
     sa = None
     if not args.no_sa and rank == 0:
-        ss = api.Session(prob, device=local, n_loads=1)
+        ss = api.Session(prob, device=dev_idx, n_loads=1)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         r1 = ss.sa(L.POLICY_MAX_LOAD, seed=1, chains=args.sa_chains, iters=args.sa_iters, p0=0.3, cool=0.995)
@@ -365,7 +506,7 @@ def main():
     comm = None
     if not args.no_comm and rank == 0:
         cp = G.with_comm(prob, 4)
-        cs = api.Session(cp, device=local, n_loads=1)
+        cs = api.Session(cp, device=dev_idx, n_loads=1)
         cts = []
         for rep in range(4):
             torch.cuda.synchronize()
@@ -387,7 +528,7 @@ def main():
     # NEXT-4: the simulated tail of the step's max-load plan (reading R32)
     tail = None
     if not args.no_sim and rank == 0:
-        ss2 = api.Session(prob, device=local)
+        ss2 = api.Session(prob, device=dev_idx)
         sims, n_q = 64, 20000
         tail = {"plan": "C4 max-load plan of this step", "queries_per_sim": n_q, "sims": sims, "points": []}
         for f in (0.3, 0.6, 0.9):
@@ -403,24 +544,29 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        r = cpu_reference_leg(prob, args, rank, world, as_main=False)
-        cpu = {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "oracle", "sample": r["sample"]}
+        r = cpu_reference_leg(prob, args, as_main=False)
+        cpu = {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "oracle", "sample": r["sample"],
+               "single_thread_value": r["single_thread_value"], "cpu_model": r["cpu_model"]}
 
-    pm, pr = plans[-1]
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+                "warmup": args.warmup, "ms_per_step": ms_step, "ms_per_step_median": ms_med,
+                "ms_per_step_min": ms_min, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": {"workload": WORKLOAD, "problem": prob.name, "sha256": prob.sha256(),
                            "candidates_per_policy": ntot, "policies": 2, "parallelism": f"shard{world}",
+                           "backend": backend if world > 1 else None, "devices": ndev,
                            "l2": "flushed between timed steps (256 MiB write)"},
                 "time_to_plan_ms": ms_step,
+                "time_to_plan_wall_ms": {"median": wall_med, "min": wall_min,
+                                         "note": "host wall clock from the API entry to both plans in host "
+                                                 "memory (problem resident, process group warm)"},
                 "plans": {"max_load": {"index": pm.index, "T": pm.objective, "replicas": pm.replicas,
                                        "quota_pct": pm.quota_pct, "batch": pm.batch},
                           "min_resource": {"index": pr.index, "gpus_used": pr.gpus_used,
                                            "quota_used": pr.quota_used, "load": LOW_LOAD * pm.objective}},
-                "scored_per_step": evals, "gpu_launches": launches, "roofline": roof, "flat_scan": flat,
-                "sa_baseline": sa, "comm_qos": comm, "tail_sim": tail,
+                "phases_ms": phases, "scored_per_step": evals, "gpu_launches": launches, "roofline": roof,
+                "flat_scan": flat, "c4b": hard, "sa_baseline": sa, "comm_qos": comm, "tail_sim": tail,
                 "clocks": clocks,
                 "e2e": e2e, "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)

@@ -227,7 +227,7 @@ RHO = {1: 1.0, 2: 1.0, 3: 1.0, 4: 1.0, 5: 1.0}
 
 
 def config_problems(config: int, preset: str = "v100-dgx2") -> List[Problem]:
-    """The problems of BASELINE.json config `config` (1-based; 6 = C4r)."""
+    """The problems of BASELINE.json config `config` (1-based; 6 = C4r, 7 = C4b)."""
     out = []
     if config == 1:
         for j, (nm, app) in enumerate(C1_APPS.items()):
@@ -252,6 +252,9 @@ def config_problems(config: int, preset: str = "v100-dgx2") -> List[Problem]:
         out.append(build_problem("C5-p2c3m1+p1c1m3",
                                  [["p2", "c3", "m1"], ["p1", "c1", "m3"]], 8, 10,
                                  POW2_32, 2, config_seed(5), RHO[5], preset))
+    elif config == 7:  # C4b: a second C4 instance (other draws, tighter QoS) where pruning is harder
+        out.append(build_problem("C4b-p1c2m2c3m1", [["p1", "c2", "m2", "c3", "m1"]],
+                                 8, 1, POW2_128, 4, config_seed(4, 1), 0.8, preset))
     elif config == 6:  # C4r: C4 on a 10% grid (same seed -> same stage draws)
         out.append(build_problem("C4r-p1c2m2c3m1", [["p1", "c2", "m2", "c3", "m1"]],
                                  8, 10, POW2_128, 4, config_seed(4), RHO[4], preset))

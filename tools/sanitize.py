@@ -17,9 +17,10 @@ for p in probs:
     m = s.plan_min_resource([[0.3 * max(r.objective, 1.0)] * p.n_apps, [0.5 * max(r.objective, 1.0)] * p.n_apps])
     s.predict_index(0, loads=[[1.0] * p.n_apps])
     s.score_range(0, min(5000, 1 << 12))
-    keys = [s.search_local(0, rank=k, world=2).clone() for k in range(2)]
+    ranks = [s, api.Session(p, n_loads=2)]   # one workspace per rank (finalize pairs with its search_local)
+    keys = [ranks[k].search_local(0, rank=k, world=2).clone() for k in range(2)]
     red = torch.stack(keys).min(dim=0).values
-    s.finalize(0, red, rank=0, world=2)
+    ranks[0].finalize(0, red, rank=0, world=2)
     f = api.Session(p, flags=p.flags | L.F_NO_FILTER).plan_max_load()
     g = api.Session(p, flags=p.flags | L.F_PAPER_GLOBAL).plan_max_load()
     print(p.name, r.index, m[0].index, f.index, g.index, flush=True)
