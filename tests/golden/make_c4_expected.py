@@ -14,7 +14,12 @@ the CUDA path.
     [0, 2^32), a seeded 2^32-aligned slice, and the aligned slices holding the
     O7 winners of each policy.
 
-    python tests/golden/make_c4_expected.py [threads] [--no-slices]
+  * --c4b: the second C4 instance C4b (gen config 7: other draws, QoS 0.8x),
+    full space, both policies, by O7.  Its incumbents are the plain-scan optima
+    of its own 10% sub-grid problem (C4b restricted to quotas 10..100, the same
+    table entries), each re-scored in C4b; for min-resource at the C4b load.
+
+    python tests/golden/make_c4_expected.py [threads] [--no-slices] [--c4b]
 """
 import json
 import os
@@ -104,6 +109,52 @@ def main(threads, slices=True):
         json.dump(rec, f, indent=1)
 
 
+def sub_grid(prob):
+    """The same problem restricted to the quotas 10, 20, .., 100 (a subset of the
+    1% grid with the same table entries)."""
+    sub = [int(np.nonzero(prob.quota_pct == q)[0][0]) for q in range(10, 101, 10)]
+    return prob.with_(name=prob.name + "-10pct", quota_pct=prob.quota_pct[sub].copy(),
+                      table=prob.table[:, :, sub, :].copy()), sub
+
+
+def main_c4b(threads):
+    p = G.config_problems(7)[0]
+    pr, sub = sub_grid(p)
+
+    def to_full(x):
+        beta, rho, theta = O.decode(pr, x)
+        return O.encode(p, beta, rho, [sub[t] for t in theta])
+
+    rec = dict(problem=p.name, sha256=p.sha256(), ntot=O.ntot(p), threads=threads,
+               note="written by tests/golden/make_c4_expected.py --c4b (oracle only: O7 with incumbents from the "
+                    "plain scan of the 10% sub-grid)")
+    t = time.time()
+    r = O.search(pr, threads=threads)[0]
+    xi = to_full(r.index)
+    s = O.score(p, xi)
+    assert s.verdict == 0 and s.T == r.T
+    bm = O.search_filtered(p, T_inc=s.T, threads=threads)
+    rec["max_load"] = dict(incumbent=dict(index=xi, T=s.T, source="10% sub-grid max-load optimum"),
+                           **best_dict(bm, time.time() - t))
+    print("max_load", rec["max_load"], flush=True)
+    lam = [LOW_LOAD * bm.T]
+    t = time.time()
+    rm = O.search(pr, "min_resource", loads=[lam], threads=threads)[0]
+    xr = to_full(rm.index)
+    sr = O.score(p, xr, loads=[lam])
+    assert sr.level_verdict == [0]
+    br = O.search_filtered(p, "min_resource", load=lam, u_inc=sr.u, U_inc=sr.U, threads=threads)
+    rec["min_resource"] = dict(loads=[lam], incumbent=dict(index=xr, u=sr.u, U=sr.U,
+                                                           source="10% sub-grid min-resource optimum"),
+                               **best_dict(br, time.time() - t))
+    print("min_resource", rec["min_resource"], flush=True)
+    with open(os.path.join(HERE, "expected_C4b-full.json"), "w") as f:
+        json.dump(rec, f, indent=1)
+
+
 if __name__ == "__main__":
     args = [a for a in sys.argv[1:] if not a.startswith("--")]
-    main(int(args[0]) if args else os.cpu_count(), slices="--no-slices" not in sys.argv)
+    if "--c4b" in sys.argv:
+        main_c4b(int(args[0]) if args else os.cpu_count())
+    else:
+        main(int(args[0]) if args else os.cpu_count(), slices="--no-slices" not in sys.argv)

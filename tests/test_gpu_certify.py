@@ -293,3 +293,19 @@ def test_finalize_pairing_contract(api):
     s.predict_index(0)                                          # rewrites the workspace
     with pytest.raises(L.CamelotError):
         s.finalize(L.POLICY_MIN_RESOURCE, km, [[5.0], [9.0]])
+
+
+def test_c4b_full_golden(api, oracle):
+    """The second C4 instance (C4b, harder pruning), both policies, == O7."""
+    e = json.load(open(os.path.join(GOLD, "expected_C4b-full.json")))
+    prob = G.config_problems(7)[0]
+    assert prob.sha256() == e["sha256"]
+    s = api.Session(prob, n_loads=1)
+    pm = s.plan_max_load()
+    g = e["max_load"]
+    assert pm.index == g["index"] and fb(pm.objective) == fb(g["T"])
+    lam = e["min_resource"]["loads"]
+    assert lam[0][0] == 0.3 * pm.objective
+    pr = s.plan_min_resource(lam)[0]
+    g = e["min_resource"]
+    assert pr.index == g["index"] and (pr.gpus_used, pr.quota_used) == (g["u"], g["U"])
