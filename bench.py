@@ -112,6 +112,14 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+T_START = time.perf_counter()
+
+
+def log(msg):
+    """progress on stderr (the JSON line alone goes to stdout)"""
+    print(f"[bench {time.perf_counter() - T_START:7.1f}s] {msg}", file=sys.stderr, flush=True)
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -244,6 +252,7 @@ def main():
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group("gloo")
+    log("session upload")
     stream = torch.cuda.current_stream(dev)
     sess = api.Session(prob, device=dev_idx, n_loads=1)
     sess.upload()
@@ -305,6 +314,7 @@ def main():
 
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
 
+    log(f"rank {rank}/{world} on cuda:{dev_idx} ({backend if world > 1 else 'single'}): warm-up")
     for _ in range(args.warmup):
         step(sess, prob)
     torch.cuda.synchronize()
@@ -338,6 +348,7 @@ def main():
     evals = sum(pm.n_evaluated + pr.n_evaluated for pm, pr in plans) / args.steps
     k_ns = sum(pm.search_ns + pr.search_ns for pm, pr in plans) / args.steps
 
+    log(f"timed steps done: {statistics.median(ms):.3f} ms median")
     # fixed costs per N: one instrumented step, CUDA events between the phases
     marks = []
     flush.fill_(0)
@@ -361,6 +372,7 @@ def main():
     # memory every step (not resident) and the plans read back to the host
     e2e = None
     if not args.no_e2e:
+        log("e2e leg")
         for _ in range(2):
             step(sess, prob, resident=False)
         torch.cuda.synchronize()
@@ -405,6 +417,7 @@ def main():
     # issue-roofline view and the near-linear scaling leg.
     flat = None
     if not args.no_flat:
+        log("flat-scan leg")
         fp = G.config_problems(args.flat_config)[0]
         fs = api.Session(fp, device=dev_idx, flags=fp.flags | L.F_NO_FILTER)
         fnt = ntot_of(fp)
@@ -455,8 +468,10 @@ def main():
     # a second C4 instance where pruning is harder (other draws, QoS 0.8x): C4b
     hard = None
     if not args.no_hard:
+        log("C4b leg")
         hp = G.config_problems(7)[0]
         hs = api.Session(hp, device=dev_idx, n_loads=1)
+        hs.upload()
         for _ in range(3):
             step(hs, hp)
         torch.cuda.synchronize()
@@ -483,6 +498,7 @@ def main():
     pm, pr = plans[-1]
     sa = None
     if not args.no_sa and rank == 0:
+        log("SA leg")
         ss = api.Session(prob, device=dev_idx, n_loads=1)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -505,6 +521,7 @@ def main():
     # the generator's hand-over sizes; both policies, exact, time of the step
     comm = None
     if not args.no_comm and rank == 0:
+        log("COMM leg")
         cp = G.with_comm(prob, 4)
         cs = api.Session(cp, device=dev_idx, n_loads=1)
         cts = []
@@ -528,6 +545,7 @@ def main():
     # NEXT-4: the simulated tail of the step's max-load plan (reading R32)
     tail = None
     if not args.no_sim and rank == 0:
+        log("tail-simulation leg")
         ss2 = api.Session(prob, device=dev_idx)
         sims, n_q = 64, 20000
         tail = {"plan": "C4 max-load plan of this step", "queries_per_sim": n_q, "sims": sims, "points": []}
@@ -544,6 +562,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        log("CPU oracle leg")
         r = cpu_reference_leg(prob, args, as_main=False)
         cpu = {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "oracle", "sample": r["sample"],
                "single_thread_value": r["single_thread_value"], "cpu_model": r["cpu_model"]}

@@ -191,7 +191,8 @@ typedef struct {
                                  dimensions where fits(g, 1) fails after pass 2,
                                  DESIGN.md 3.2); exact in CAMELOT_F_NO_FILTER mode, a
                                  subset when bounds skip candidates                  */
-    uint64_t n_feasible;      /* feasible candidates seen (exact in NO_FILTER mode)  */
+    uint64_t n_feasible;      /* candidates seen that pass placement and QoS (the   */
+                              /* load-independent checks; exact in NO_FILTER mode)  */
     uint64_t n_scored;        /* candidates fully scored by the search               */
     uint64_t n_covered;       /* candidates covered (scored or excluded by a bound)  */
     float comm_ms[CAMELOT_MAX_STAGES];  /* CAMELOT_F_COMM: hand-over time of edge i -> i+1 (ms) */

@@ -53,7 +53,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     unit (rebuilt when it or an included header changed), compiled in parallel,
     linked into one shared library."""
     extra = os.environ.get("CAMELOT_NVCC_EXTRA", "").split()   # e.g. -DCAMELOT_FTRACE (profiling)
-    objdir = os.path.join(HERE, "build")
+    objdir = os.environ.get("CAMELOT_OBJDIR") or os.path.join(HERE, "build")   # variant builds (profiling)
     os.makedirs(objdir, exist_ok=True)
     stamp = os.path.join(objdir, "flags.txt")
     flags = " ".join(NVCC_FLAGS_OBJ + extra)

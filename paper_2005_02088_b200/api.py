@@ -106,6 +106,7 @@ class Session:
                              mem_mib=int(c.mem_mib), gflops=float(c.gflops),
                              link_gbs=float(getattr(c, "link_gbs", 1.0)), ipc_ms=float(getattr(c, "ipc_ms", 0.0)))
         self.ws = None
+        self._uploaded = False
         self._ensure(n_loads)
 
     # ------------------------------------------------------------------ plumbing
@@ -115,12 +116,19 @@ class Session:
             raise L.CamelotError(L.EINVAL, L.lib().camelot_last_error().decode())
         if self.ws is None or self.ws.numel() < nb:
             self.ws = torch.empty(nb, dtype=torch.uint8, device=f"cuda:{self.device}")
+            self._uploaded = False
 
     def _stream_ptr(self):
         s = self.stream if self.stream is not None else torch.cuda.current_stream(self.device)
         return s.cuda_stream
 
     def exec(self, rank: int = 0, world: int = 1, lo: int = 0, hi: int = 0, resident: bool = False) -> L.Exec:
+        if resident and not self._uploaded:
+            # CAMELOT_EXEC_RESIDENT reuses the problem image already in the workspace:
+            # a workspace that never saw camelot_upload holds no problem
+            raise L.CamelotError(L.EINVAL, "resident=True before upload() on this session")
+        if not resident:
+            self._uploaded = True   # a non-resident call uploads the problem image itself
         return L.Exec(device=self.device, stream=self._stream_ptr(), rank=rank, world=world,
                       index_lo=lo, index_hi=hi, workspace=self.ws.data_ptr(),
                       workspace_bytes=self.ws.numel(), exec_flags=L.EXEC_RESIDENT if resident else 0)
@@ -133,6 +141,7 @@ class Session:
     def upload(self):
         ex = self.exec()
         L.check(L.lib().camelot_upload(C.byref(self.cprob), C.byref(self.ccl), C.byref(ex)), False)
+        self._uploaded = True
 
     def plan_max_load(self, lo: int = 0, hi: int = 0, resident: bool = False) -> PlanResult:
         out = L.Plan()

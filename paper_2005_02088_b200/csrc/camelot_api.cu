@@ -17,7 +17,7 @@
 #include <vector>
 
 #include "../../include/camelot.h"
-#include "camelot_kernels.cuh"
+#include "camelot_inst.cuh"
 #include "camelot_sweep_args.h"
 
 namespace cam {   // camelot_sweep.cu
@@ -318,9 +318,8 @@ int grid_for(int dev, int &grid) {
             return CAMELOT_OK;
         }
     const size_t sm = search_smem<CM>();
-    CU(cudaFuncSetAttribute(search_kernel<CM, NS, POL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     int per = 0, nsm = 0;
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, search_kernel<CM, NS, POL>, SEARCH_THREADS, sm));
+    CU((k_search_occupancy<CM, NS, POL>(sm, &per)));
     CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     grid = std::max(1, std::min(MAXSLOTS, per * nsm));
     g_grid_cache.push_back({GridKey{dev, CM, NS, POL}, grid});
@@ -367,9 +366,8 @@ int setup(const camelot_problem *p, const camelot_cluster *c, const camelot_exec
 template <int CM, int NS, int POL>
 int launch_search(const Ctx &X, const SearchArgs &S, int grid) {
     const size_t sm = search_smem<CM>();
-    search_kernel<CM, NS, POL><<<grid, SEARCH_THREADS, sm, X.st>>>(X.P, S);
+    CU((k_search_launch<CM, NS, POL>(X.P, S, grid, sm, X.st)));
     COUNT_LAUNCH();
-    CU(cudaGetLastError());
     return CAMELOT_OK;
 }
 
@@ -403,9 +401,8 @@ int coop_grid_for(int dev, int &grid) {
             return CAMELOT_OK;
         }
     const size_t sm = level_smem<CM>();
-    CU(cudaFuncSetAttribute(search_level_kernel<CM, NS, POL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     int per = 0, nsm = 0;
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, search_level_kernel<CM, NS, POL>, SEARCH_THREADS, sm));
+    CU((k_level_occupancy<CM, NS, POL>(sm, &per)));
     CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     grid = std::max(1, std::min(MAXSLOTS, per * nsm));
     cache.push_back({dev, grid});
@@ -426,9 +423,7 @@ int launch_level(const Ctx &X, int dev, const std::vector<LevelArgs> &levels) {
         LS.L[l].F.nslots = grid * LS.L[l].S.nlev;
     }
     const size_t sm = level_smem<CM>();
-    void *args[] = {(void *)&X.P, (void *)&LS};
-    CU(cudaLaunchCooperativeKernel((const void *)search_level_kernel<CM, NS, POL>, dim3(grid), dim3(SEARCH_THREADS),
-                                   args, sm, X.st));
+    CU((k_level_launch<CM, NS, POL>(X.P, LS, grid, sm, X.st)));
     COUNT_LAUNCH();
     return CAMELOT_OK;
 }
@@ -896,7 +891,7 @@ int finalize_impl(const Ctx &X, const camelot_exec *ex, int policy, int nlev, co
         }
     }
     camelot_plan *dplans = reinterpret_cast<camelot_plan *>(ws + X.L.plans);
-    plan_kernel<<<(nlev + 63) / 64, 64, 0, X.st>>>(X.P, policy, nlev, winner, reinterpret_cast<const float *>(ws + X.L.lam),
+    plan_kernel<<<nlev, PLAN_THREADS, 0, X.st>>>(X.P, policy, nlev, winner, reinterpret_cast<const float *>(ws + X.L.lam),
                                                    reinterpret_cast<const DevHeader *>(ws + X.L.hdr2), dplans);
     COUNT_LAUNCH();
     CU(cudaGetLastError());
@@ -1230,7 +1225,7 @@ int camelot_sa(const camelot_problem *p, const camelot_cluster *c, int policy, c
     CU(cudaGetLastError());
     CU(cudaMemcpyAsync(ws + X.L.hdr2, ws + X.L.hdr, sizeof(DevHeader), cudaMemcpyDeviceToDevice, X.st));
     camelot_plan *dplans = reinterpret_cast<camelot_plan *>(ws + X.L.plans);
-    plan_kernel<<<1, 64, 0, X.st>>>(X.P, policy, 1, winner, reinterpret_cast<const float *>(ws + X.L.lam),
+    plan_kernel<<<1, PLAN_THREADS, 0, X.st>>>(X.P, policy, 1, winner, reinterpret_cast<const float *>(ws + X.L.lam),
                                     reinterpret_cast<const DevHeader *>(ws + X.L.hdr2), dplans);
     COUNT_LAUNCH();
     CU(cudaGetLastError());

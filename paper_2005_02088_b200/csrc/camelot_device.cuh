@@ -7,6 +7,14 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// Non-inline device functions of the shared headers: private copies in the
+// translation units that only instantiate the search templates (camelot_inst_*.cu).
+#ifdef CAMELOT_INST_TU
+#define CAM_DEVFN static __device__
+#else
+#define CAM_DEVFN __device__
+#endif
+
 namespace cam {
 
 constexpr int NMAX = 8;      // stages

@@ -1,0 +1,8 @@
+// camelot_inst_c8_n4.cu -- instantiations of the search launchers (camelot_inst.cuh): CM=8, NS in {4}, policy in {0,1}.
+#define CAMELOT_INST_TU
+#include "camelot_inst.cuh"
+
+namespace cam {
+CAMELOT_INSTANTIATE(8, 4, 0)
+CAMELOT_INSTANTIATE(8, 4, 1)
+}  // namespace cam

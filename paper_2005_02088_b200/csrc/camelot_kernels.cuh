@@ -11,6 +11,15 @@
 #include "camelot_score.cuh"
 #include "camelot_search.cuh"
 
+// Translation units that only instantiate the search templates (camelot_inst_*.cu)
+// get private copies of the plain kernels, so that their host stubs do not clash
+// with camelot_api.cu's at link time.
+#ifdef CAMELOT_INST_TU
+#define CAM_GLOBAL static __global__
+#else
+#define CAM_GLOBAL __global__
+#endif
+
 namespace cam {
 
 constexpr int FILTER_THREADS = 512;
@@ -31,7 +40,7 @@ struct FilterArgs {
     int d0;
 };
 
-__device__ void item_offsets(const DevProb &P, const StageBound *sb, int d0, unsigned long long *item_off,
+CAM_DEVFN void item_offsets(const DevProb &P, const StageBound *sb, int d0, unsigned long long *item_off,
                              DevHeader *hdr);
 
 // One CTA per batch index b: filters the options of every stage at batch b.
@@ -52,7 +61,7 @@ struct FilterSmem {
 #else
 #define FTRACE(t)
 #endif
-__device__ void filter_body(const DevProb &P, const FilterArgs &F, int b, FilterSmem &fsm) {
+CAM_DEVFN void filter_body(const DevProb &P, const FilterArgs &F, int b, FilterSmem &fsm) {
     auto &keep = fsm.keep;
     auto &mindur = fsm.mindur;
     auto &minNP = fsm.minNP;
@@ -208,7 +217,7 @@ __device__ void filter_body(const DevProb &P, const FilterArgs &F, int b, Filter
 
 // One CTA per batch index b: filters the options of every stage at batch b
 // (+ fused: search-slot reset and, by the last block, the item offsets).
-__global__ void __launch_bounds__(FILTER_THREADS) filter_kernel(const DevProb P, const FilterArgs F) {
+CAM_GLOBAL void __launch_bounds__(FILTER_THREADS) filter_kernel(const DevProb P, const FilterArgs F) {
     __shared__ FilterSmem fsm;
     const int tid = threadIdx.x;
     filter_body(P, F, blockIdx.x, fsm);
@@ -231,7 +240,7 @@ __global__ void __launch_bounds__(FILTER_THREADS) filter_kernel(const DevProb P,
     }
 }
 
-__global__ void init_slots_kernel(Slot *s, int n) {
+CAM_GLOBAL void init_slots_kernel(Slot *s, int n) {
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
         s[k].key = 0xFFFFFFFFull;
         s[k].x = ~0ull;
@@ -239,7 +248,7 @@ __global__ void init_slots_kernel(Slot *s, int n) {
 }
 
 // item space: for batch combo bc, items = prod_{i<d0} cnt_i(b_app(i)), 0 if any stage is empty
-__device__ void item_offsets(const DevProb &P, const StageBound *sb, int d0, unsigned long long *item_off,
+CAM_DEVFN void item_offsets(const DevProb &P, const StageBound *sb, int d0, unsigned long long *item_off,
                              DevHeader *hdr) {
     unsigned long long acc = 0;
     for (int bc = 0; bc < P.nbc; ++bc) {
@@ -265,7 +274,7 @@ __device__ void item_offsets(const DevProb &P, const StageBound *sb, int d0, uns
 
 // The same offsets computed by a whole CTA from shared-memory bounds into shared
 // memory (nbc <= ITEM_SMEM): per-combo counts in parallel, then an inclusive scan.
-__device__ void item_offsets_block(const DevProb &P, const StageBound *sb, int d0, unsigned long long *out) {
+CAM_DEVFN void item_offsets_block(const DevProb &P, const StageBound *sb, int d0, unsigned long long *out) {
     for (int bc = threadIdx.x; bc < P.nbc; bc += blockDim.x) {
         int bb[AMAX];
         int t = bc;
@@ -294,7 +303,7 @@ __device__ void item_offsets_block(const DevProb &P, const StageBound *sb, int d
     }
 }
 
-__global__ void eq2_kernel(const DevProb P, const float *lam, int nlev, int *y) {
+CAM_GLOBAL void eq2_kernel(const DevProb P, const float *lam, int nlev, int *y) {
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= P.nbc * nlev) return;
     const int bc = idx / nlev, k = idx % nlev;
@@ -308,7 +317,7 @@ __global__ void eq2_kernel(const DevProb P, const float *lam, int nlev, int *y) 
 }
 
 // slots -> result[k] and packed keys (stand-alone kernel: naive path)
-__global__ void reduce_kernel(const DevProb P, const Slot *slots, int nslots, int nlev, Slot *result,
+CAM_GLOBAL void reduce_kernel(const DevProb P, const Slot *slots, int nslots, int nlev, Slot *result,
                               long long *keys, const StageBound *sb, const OptRec *rec,
                               const unsigned long long *item_off, int d0, int chunk_items, int flat_shift) {
     __shared__ unsigned long long sk[256], sx[256];
@@ -325,7 +334,7 @@ struct FinalArgs {
     unsigned long long *rescan;// [nlev] out: chunk to re-scan or ~0
 };
 
-__global__ void resolve_kernel(const DevProb P, const FinalArgs F) {
+CAM_GLOBAL void resolve_kernel(const DevProb P, const FinalArgs F) {
     const int k = threadIdx.x;
     if (k >= F.nlev) return;
     const unsigned long long packed = (unsigned long long)F.keys[k] ^ 0x8000000000000000ull;
@@ -349,59 +358,77 @@ __global__ void resolve_kernel(const DevProb P, const FinalArgs F) {
 }
 
 // winner index -> full plan (device), with the search counters
-__global__ void plan_kernel(const DevProb P, int policy, int nlev, const Slot *winner, const float *lam,
-                            const DevHeader *hdr, camelot_plan *out) {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+// One block per load level: thread 0 scores the winner (score_digits, scratch and
+// result in shared memory), then the block fills the plan in shared memory and
+// copies it out word by word (the serial part stays short: no local-memory plan).
+constexpr int PLAN_THREADS = 64;
+CAM_GLOBAL void __launch_bounds__(PLAN_THREADS) plan_kernel(const DevProb P, int policy, int nlev, const Slot *winner,
+                                                            const float *lam, const DevHeader *hdr, camelot_plan *out) {
+    const int k = blockIdx.x, tid = threadIdx.x;
     if (k >= nlev) return;
-    camelot_plan pl;
-    memset(&pl, 0, sizeof(pl));
-    for (int i = 0; i < CAMELOT_MAX_STAGES * CAMELOT_MAX_REPLICAS; ++i) pl.gpu_of_instance[i] = -1;
-    pl.n_scored = hdr->n_scored;
-    pl.n_evaluated = hdr->cum_scored + hdr->cum_nodes;
-    pl.search_ns = 0;
-    pl.n_feasible = hdr->n_feasible;
-    pl.n_covered = 0;
+    __shared__ __align__(16) camelot_plan pl;
+    __shared__ FullScore s;
+    __shared__ ScoreScratch scr;
+    __shared__ int beta[AMAX], rho[NMAX], theta[NMAX];
+    __shared__ int eq2y;
     const Slot w = winner[k];
-    if (w.x == ~0ull) {
-        pl.index = ~0ull;
-        pl.status = CAMELOT_INFEASIBLE;
-        pl.violations = hdr->viol_or;
-        out[k] = pl;
-        return;
+    {
+        uint32_t *pw = reinterpret_cast<uint32_t *>(&pl);
+        for (int q = tid; q < (int)(sizeof(camelot_plan) / 4); q += blockDim.x) pw[q] = 0u;
     }
-    int beta[AMAX], rho[NMAX], theta[NMAX];
-    decode_index(P, w.x, beta, rho, theta);
-    FullScore s;
-    __shared__ ScoreScratch scr[64];   // blockDim <= 64: shared instead of local memory (serial path)
-    score_digits(P, beta, rho, theta, s, &scr[threadIdx.x]);
-    pl.index = w.x;
-    pl.status = CAMELOT_OK;
-    for (int a = 0; a < P.A; ++a) {
-        pl.batch[a] = P.S[beta[a]];
-        pl.e2e_latency_ms[a] = s.Lsum[a];
-        pl.throughput_qps[a] = s.Tmin[a];
+    __syncthreads();
+    for (int q = tid; q < CAMELOT_MAX_STAGES * CAMELOT_MAX_REPLICAS; q += blockDim.x) pl.gpu_of_instance[q] = -1;
+    if (tid == 0) {
+        pl.n_scored = hdr->n_scored;
+        pl.n_evaluated = hdr->cum_scored + hdr->cum_nodes;
+        pl.n_feasible = hdr->n_feasible;
+        if (w.x == ~0ull) {
+            pl.index = ~0ull;
+            pl.status = CAMELOT_INFEASIBLE;
+            pl.violations = hdr->viol_or;
+        } else {
+            decode_index(P, w.x, beta, rho, theta);
+            score_digits(P, beta, rho, theta, s, &scr);
+            eq2y = policy == 1 ? eq2_gpus(P, beta, lam + k * P.A) : 0;
+            pl.index = w.x;
+            pl.status = CAMELOT_OK;
+            pl.quota_used = s.U;
+            pl.gpus_used = s.u;
+            if (policy == 1) {
+                pl.eq2_gpus = eq2y;
+                pl.violations = level_verdict(P, s, lam + k * P.A, eq2y);
+                pl.objective = (float)s.U;
+            } else {
+                pl.violations = s.verdict;
+                pl.objective = s.T;
+            }
+        }
     }
-    for (int i = 0; i < P.n; ++i) {
-        pl.replicas[i] = rho[i] + 1;
-        pl.quota_pct[i] = P.Q[theta[i]];
-        pl.stage_latency_ms[i] = s.L[i];
-        pl.stage_throughput_qps[i] = s.Ti[i];
-        pl.kappa[i] = s.kappa[i];
-        pl.comm_ms[i] = s.comm[i];
-        for (int r = 0; r < CAMELOT_MAX_REPLICAS && r < SCORE_RMAX; ++r)
-            pl.gpu_of_instance[i * CAMELOT_MAX_REPLICAS + r] = s.goi[i * SCORE_RMAX + r];
+    __syncthreads();
+    if (w.x != ~0ull) {
+        if (tid < P.A) {
+            pl.batch[tid] = P.S[beta[tid]];
+            pl.e2e_latency_ms[tid] = s.Lsum[tid];
+            pl.throughput_qps[tid] = s.Tmin[tid];
+        }
+        if (tid < P.n) {
+            const int i = tid;
+            pl.replicas[i] = rho[i] + 1;
+            pl.quota_pct[i] = P.Q[theta[i]];
+            pl.stage_latency_ms[i] = s.L[i];
+            pl.stage_throughput_qps[i] = s.Ti[i];
+            pl.kappa[i] = s.kappa[i];
+            pl.comm_ms[i] = s.comm[i];
+        }
+        for (int q = tid; q < P.n * CAMELOT_MAX_REPLICAS; q += blockDim.x) {
+            const int i = q / CAMELOT_MAX_REPLICAS, r = q % CAMELOT_MAX_REPLICAS;
+            if (r < SCORE_RMAX) pl.gpu_of_instance[q] = s.goi[i * SCORE_RMAX + r];
+        }
     }
-    pl.quota_used = s.U;
-    pl.gpus_used = s.u;
-    if (policy == 1) {
-        pl.eq2_gpus = eq2_gpus(P, beta, lam + k * P.A);
-        pl.violations = level_verdict(P, s, lam + k * P.A, pl.eq2_gpus);
-        pl.objective = (float)s.U;
-    } else {
-        pl.violations = s.verdict;
-        pl.objective = s.T;
-    }
-    out[k] = pl;
+    __syncthreads();
+    const uint32_t *src = reinterpret_cast<const uint32_t *>(&pl);
+    uint32_t *dst = reinterpret_cast<uint32_t *>(out + k);
+    for (int q = tid; q < (int)(sizeof(camelot_plan) / 4); q += blockDim.x) dst[q] = src[q];
 }
 
 // Naive exhaustive search (kernel N5 as a search): one thread scores one
@@ -422,7 +449,7 @@ struct FlatArgs {
     DevHeader *hdr;
 };
 
-__global__ void __launch_bounds__(FLAT_THREADS) flat_search_kernel(const DevProb P, const FlatArgs F) {
+CAM_GLOBAL void __launch_bounds__(FLAT_THREADS) flat_search_kernel(const DevProb P, const FlatArgs F) {
     __shared__ unsigned long long bk_s[FLAT_THREADS / 32][LMAX], bx_s[FLAT_THREADS / 32][LMAX];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (int k = lane; k < F.nlev; k += 32) {
@@ -524,7 +551,7 @@ __global__ void __launch_bounds__(FLAT_THREADS) flat_search_kernel(const DevProb
 }
 
 // explicit plan (predict) -> plan
-__global__ void predict_kernel(const DevProb P, unsigned long long x, const float *lam, int nlev, camelot_plan *out) {
+CAM_GLOBAL void predict_kernel(const DevProb P, unsigned long long x, const float *lam, int nlev, camelot_plan *out) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     camelot_plan pl;
     memset(&pl, 0, sizeof(pl));
@@ -561,7 +588,7 @@ __global__ void predict_kernel(const DevProb P, unsigned long long x, const floa
     out[0] = pl;
 }
 
-__global__ void score_range_kernel(const DevProb P, unsigned long long lo, unsigned long long cnt, uint8_t *verdict,
+CAM_GLOBAL void score_range_kernel(const DevProb P, unsigned long long lo, unsigned long long cnt, uint8_t *verdict,
                                    float *T, int *u, int *U) {
     const unsigned long long t = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
     if (t >= cnt) return;
@@ -771,7 +798,7 @@ __device__ __forceinline__ unsigned sa_key_of(const DevProb &P, int policy, cons
     return level_verdict(P, s, lam, y) ? 0xFFFFFFFFu : objkey_minres(s.u, s.U);
 }
 
-__global__ void __launch_bounds__(256) sa_kernel(const DevProb P, const SAArgs A) {
+CAM_GLOBAL void __launch_bounds__(256) sa_kernel(const DevProb P, const SAArgs A) {
     __shared__ unsigned long long sk[8], sx[8];
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -881,7 +908,7 @@ __global__ void __launch_bounds__(256) sa_kernel(const DevProb P, const SAArgs A
 // the device into the predictor table: one thread per (tree, batch, quota).
 namespace cam {
 
-__global__ void tree_table_kernel(int n_trees, const int4 *nodes, const float *values, const int *off,
+CAM_GLOBAL void tree_table_kernel(int n_trees, const int4 *nodes, const float *values, const int *off,
                                   int nS, const int *batch, int nQ, const int *quota, float *table) {
     const long long total = (long long)n_trees * nS * nQ;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
@@ -935,7 +962,7 @@ struct SimArgs {
     double *out;                           // [n_sims][A][2] = (p99, mean)
 };
 
-__global__ void __launch_bounds__(256) simulate_kernel(const DevProb P, const SimArgs A) {
+CAM_GLOBAL void __launch_bounds__(256) simulate_kernel(const DevProb P, const SimArgs A) {
     __shared__ FullScore sc;
     __shared__ double freet[NMAX][CAMELOT_MAX_REPLICAS];
     __shared__ unsigned int hist[256];

@@ -60,7 +60,7 @@ struct ScoreScratch {
     uint8_t hcnt[NMAX][SCORE_CMAX];
 };
 
-__device__ void score_digits(const DevProb &P, const int *beta, const int *rho, const int *theta,
+CAM_DEVFN void score_digits(const DevProb &P, const int *beta, const int *rho, const int *theta,
                              FullScore &out, ScoreScratch *scr = nullptr) {
     const int n = P.n, C = P.C;
     float dur[NMAX], thr[NMAX], bwv[NMAX];

@@ -959,7 +959,7 @@ __device__ inline unsigned long long item_of(const DevProb &P, const StageBound 
 
 // slots -> result[k] (exact local best), packed keys and (optionally) the next
 // incumbent; executed by ONE block of 256 threads (sk/sx: 256-entry scratch)
-__device__ void reduce_slots_block(const DevProb &P, const Slot *slots, int nslots, int nlev, Slot *result,
+CAM_DEVFN void reduce_slots_block(const DevProb &P, const Slot *slots, int nslots, int nlev, Slot *result,
                                    long long *keys, Slot *inc_out, const StageBound *sb, const OptRec *rec,
                                    const unsigned long long *item_off, int d0, int chunk_items, int flat_shift,
                                    unsigned long long *sk, unsigned long long *sx) {
