@@ -227,6 +227,23 @@ int camelot_plan_min_resource(const camelot_problem *p, const camelot_cluster *c
                               const float *load_qps, int n_loads,
                               const camelot_exec *exec, camelot_plan *out);
 
+/* Both policies back to back, as Camelot uses them (the
+ * low-load allocation is planned at 30% of the peak the max-load policy
+ * supports): out[0] = the max-load plan (Eq. 1), out[1] = the min-resource plan
+ * (Eq. 3) at load_a = fl32(low_load_frac * T*) for every application a, T* =
+ * out[0].objective (the float64 product rounded to binary32, as a host caller
+ * computing it in double would).  The load is derived ON THE DEVICE from the
+ * max-load winner, so the two exact searches run back to back on exec->stream
+ * with one host synchronisation at the end (no host round trip between the
+ * policies).  No feasible peak: out[1] is INFEASIBLE with violations = V_LOAD
+ * (the min-resource search then runs at load +inf and finds nothing).  Same result
+ * as camelot_plan_max_load followed by camelot_plan_min_resource at that load.
+ * low_load_frac in (0, 1]; world must be 1; out: host [2].  Returns CAMELOT_OK
+ * if both plans are feasible, else CAMELOT_INFEASIBLE (plans still written). */
+int camelot_plan_max_then_min(const camelot_problem *p, const camelot_cluster *c,
+                              double low_load_frac, const camelot_exec *exec,
+                              camelot_plan *out);
+
 /* Score ONE explicit plan (oracle_predict counterpart).  batch: [A] batch SIZES
  * (values on the grid), replicas: [n] N_i, quota_pct: [n] p_i (on the grid);
  * a value off the grid is CAMELOT_EINVAL.  load_qps [n_loads][A] may be NULL.

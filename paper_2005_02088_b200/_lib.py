@@ -123,7 +123,8 @@ class Tree(C.Structure):
 
 
 EXPORTS = ["camelot_last_error", "camelot_version", "camelot_workspace_bytes", "camelot_upload",
-           "camelot_plan_max_load", "camelot_plan_min_resource", "camelot_predict", "camelot_predict_index",
+           "camelot_plan_max_load", "camelot_plan_min_resource", "camelot_plan_max_then_min", "camelot_predict",
+           "camelot_predict_index",
            "camelot_score_range", "camelot_search_local", "camelot_finalize", "camelot_last_stats",
            "camelot_kernel_launches", "camelot_sa", "camelot_trace",
            "camelot_trees_workspace_bytes", "camelot_tables_from_trees", "camelot_simulate_workspace_bytes",
@@ -154,6 +155,7 @@ def lib():
         L.camelot_upload.argtypes = [P, Cl, E]
         L.camelot_plan_max_load.argtypes = [P, Cl, E, Pl]
         L.camelot_plan_min_resource.argtypes = [P, Cl, fp, C.c_int, E, Pl]
+        L.camelot_plan_max_then_min.argtypes = [P, Cl, C.c_double, E, Pl]
         ip = C.POINTER(C.c_int32)
         L.camelot_predict.argtypes = [P, Cl, ip, ip, ip, fp, C.c_int, E, Pl]
         L.camelot_predict_index.argtypes = [P, Cl, C.c_uint64, fp, C.c_int, E, Pl]

@@ -9,7 +9,7 @@ from __future__ import annotations
 
 import ctypes as C
 import dataclasses
-from typing import List, Optional, Sequence
+from typing import Tuple, List, Optional, Sequence
 
 import numpy as np
 import torch
@@ -158,6 +158,17 @@ class Session:
                                                   arr.ctypes.data_as(C.POINTER(C.c_float)), nl,
                                                   C.byref(ex), out))
         return [_plan(o, self.n, self.A) for o in out]
+
+    def plan_max_then_min(self, low_load_frac: float = 0.3, lo: int = 0, hi: int = 0,
+                          resident: bool = False) -> Tuple[PlanResult, PlanResult]:
+        """Max-load plan, then the min-resource plan at low_load_frac x its T*
+        (PAPER.md L1088), the load derived on the device: one call, one host
+        synchronisation (camelot_plan_max_then_min)."""
+        out = (L.Plan * 2)()
+        ex = self.exec(lo=lo, hi=hi, resident=resident)
+        L.check(L.lib().camelot_plan_max_then_min(C.byref(self.cprob), C.byref(self.ccl), float(low_load_frac),
+                                                  C.byref(ex), out))
+        return _plan(out[0], self.n, self.A), _plan(out[1], self.n, self.A)
 
     def predict(self, batch: Sequence[int], replicas: Sequence[int], quota_pct: Sequence[int],
                 loads=None) -> PlanResult:

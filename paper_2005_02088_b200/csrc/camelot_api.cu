@@ -39,6 +39,7 @@ struct EvPair {
     bool armed = false;
 };
 thread_local EvPair t_ev;
+thread_local EvPair t_ev_spare;   // camelot_plan_max_then_min: the first search's events
 
 // What the last camelot_search_local left in a workspace: camelot_finalize reads
 // that state (local best, filter records, loads, Eq. 2 estimates), so it must be
@@ -201,7 +202,7 @@ Layout make_layout(const Dims &d, int nlev) {
     L.keys = put((size_t)L.nlev * sizeof(long long));
     L.winner = put((size_t)L.nlev * sizeof(Slot));
     L.rescan = put((size_t)L.nlev * sizeof(unsigned long long));
-    L.plans = put((size_t)L.nlev * sizeof(camelot_plan));
+    L.plans = put((size_t)(L.nlev + 1) * sizeof(camelot_plan));   // + the max-load plan of camelot_plan_max_then_min
     L.slots = put((size_t)MAXSLOTS * L.nlev * sizeof(Slot));
     // frontier of placement-state nodes: as many as there are leaf parents in the
     // whole space, clamped to [256, 2^20] (overflow falls back to inline DFS)
@@ -587,21 +588,23 @@ int sweep_pass(const Ctx &X, int dev, int policy, int nlev, const Slot *inc, Slo
     A.hi = hi;
     A.qstride = qstride;
     A.nQs = (X.d.nQ - 1) / qstride + 1;
+    const unsigned long long Os = (unsigned long long)X.d.Rmax * A.nQs;
+    A.nchunk = (int)((Os + 31) / 32);
+    A.gpack = Os <= 16 ? (int)(32 / Os) : 1;   // small option lists: several grandparents per warp
     if (qstride == 1) {
-        const unsigned long long O2 = (unsigned long long)X.d.O * (unsigned long long)X.d.O;
-        A.nchunk = (X.d.O + 31) / 32;
+        const unsigned long long O2 = Os * Os;
         if (hi > lo) {
             A.g_lo = lo / O2;
-            A.n_items = ((hi - 1) / O2 + 1 - A.g_lo) * (unsigned long long)A.nchunk;
+            A.n_gp = (hi - 1) / O2 + 1 - A.g_lo;
         }
     } else {   // sub-grid (incumbent cascade): the whole sub-space, world 1
-        const unsigned long long Os = (unsigned long long)X.d.Rmax * A.nQs;
-        A.nchunk = (int)((Os + 31) / 32);
         unsigned long long ngp = (unsigned long long)X.d.nbc;
         for (int i = 0; i < X.d.n - 2; ++i) ngp *= Os;
         A.g_lo = 0;
-        A.n_items = ngp * (unsigned long long)A.nchunk;
+        A.n_gp = ngp;
     }
+    A.n_items = A.gpack == 1 ? A.n_gp * (unsigned long long)A.nchunk
+                             : (A.n_gp + (unsigned long long)A.gpack - 1) / (unsigned long long)A.gpack;
     A.lam = reinterpret_cast<const float *>(ws + X.L.lam);
     A.y = reinterpret_cast<const int *>(ws + X.L.y);
     A.ystride = nlev;
@@ -861,8 +864,10 @@ int local_search(const Ctx &X, const camelot_exec *ex, int policy, int nlev, lon
     return CAMELOT_OK;
 }
 
-int finalize_impl(const Ctx &X, const camelot_exec *ex, int policy, int nlev, const long long *d_keys,
-                  camelot_plan *out) {
+// resolve the reduced keys (+ chunk re-scan when sharded) and score the winners into
+// dplans[0..nlev) on the device; no host synchronisation when world == 1
+int finalize_enqueue(const Ctx &X, const camelot_exec *ex, int policy, int nlev, const long long *d_keys,
+                     camelot_plan *dplans) {
     const bool prune = !(X.P.flags & F_NO_FILTER);
     char *ws = X.ws;
     Slot *winner = reinterpret_cast<Slot *>(ws + X.L.winner);
@@ -890,11 +895,18 @@ int finalize_impl(const Ctx &X, const camelot_exec *ex, int policy, int nlev, co
             if (rc) return rc;
         }
     }
-    camelot_plan *dplans = reinterpret_cast<camelot_plan *>(ws + X.L.plans);
     plan_kernel<<<nlev, PLAN_THREADS, 0, X.st>>>(X.P, policy, nlev, winner, reinterpret_cast<const float *>(ws + X.L.lam),
                                                    reinterpret_cast<const DevHeader *>(ws + X.L.hdr2), dplans);
     COUNT_LAUNCH();
     CU(cudaGetLastError());
+    return CAMELOT_OK;
+}
+
+int finalize_impl(const Ctx &X, const camelot_exec *ex, int policy, int nlev, const long long *d_keys,
+                  camelot_plan *out) {
+    camelot_plan *dplans = reinterpret_cast<camelot_plan *>(X.ws + X.L.plans);
+    int rc = finalize_enqueue(X, ex, policy, nlev, d_keys, dplans);
+    if (rc) return rc;
     CU(cudaMemcpyAsync(out, dplans, nlev * sizeof(camelot_plan), cudaMemcpyDeviceToHost, X.st));
     CU(cudaStreamSynchronize(X.st));
     unsigned long long lo, hi;
@@ -1036,6 +1048,55 @@ int camelot_plan_min_resource(const camelot_problem *p, const camelot_cluster *c
     rc = local_search(X, ex, 1, n_loads, nullptr);
     if (rc) return rc;
     return finalize_impl(X, ex, 1, n_loads, reinterpret_cast<const long long *>(X.ws + X.L.keys), out);
+}
+
+int camelot_plan_max_then_min(const camelot_problem *p, const camelot_cluster *c, double low_load_frac,
+                              const camelot_exec *ex, camelot_plan *out) {
+    t_call_launches = 0;
+    if (!out) return fail(CAMELOT_EINVAL, "null out");
+    if (ex && ex->world != 1) return fail(CAMELOT_EINVAL, "plan_* is single-process: use search_local + finalize for world > 1");
+    if (!(low_load_frac > 0.0 && low_load_frac <= 1.0)) return fail(CAMELOT_EINVAL, "low_load_frac must be in (0, 1]");
+    Ctx X;
+    int rc = setup(p, c, ex, 1, X, true);
+    if (rc) return rc;
+    camelot_plan *dplans = reinterpret_cast<camelot_plan *>(X.ws + X.L.plans);   // [0] min-resource, [1] max-load
+    // max-load search and its plan, kept on the device
+    rc = local_search(X, ex, 0, 1, nullptr);
+    if (rc) return rc;
+    rc = finalize_enqueue(X, ex, 0, 1, reinterpret_cast<const long long *>(X.ws + X.L.keys), dplans + 1);
+    if (rc) return rc;
+    std::swap(t_ev, t_ev_spare);   // keep the max-load search's events
+    // the low load from the peak, on the device (no host round trip), then min resource
+    low_load_kernel<<<1, 32, 0, X.st>>>(X.P, dplans + 1, low_load_frac, reinterpret_cast<float *>(X.ws + X.L.lam));
+    COUNT_LAUNCH();
+    CU(cudaGetLastError());
+    rc = local_search(X, ex, 1, 1, nullptr);
+    if (rc) return rc;
+    rc = finalize_enqueue(X, ex, 1, 1, reinterpret_cast<const long long *>(X.ws + X.L.keys), dplans);
+    if (rc) return rc;
+    camelot_plan both[2];
+    CU(cudaMemcpyAsync(both, dplans, 2 * sizeof(camelot_plan), cudaMemcpyDeviceToHost, X.st));
+    CU(cudaStreamSynchronize(X.st));
+    out[0] = both[1];
+    out[1] = both[0];
+    if (out[0].status != CAMELOT_OK) {   // no peak, no low load (camelot.h): every level fails LOAD
+        out[1].status = CAMELOT_INFEASIBLE;
+        out[1].index = ~0ull;
+        out[1].violations = CAMELOT_V_LOAD;
+    }
+    unsigned long long lo, hi;
+    range_of(X, ex, lo, hi);
+    EvPair *evs[2] = {&t_ev_spare, &t_ev};
+    for (int k = 0; k < 2; ++k) {
+        out[k].n_covered = hi - lo;
+        out[k].search_ns = 0;
+        float ms = 0.0f;
+        if (evs[k]->armed && evs[k]->dev == ex->device) {
+            if (cudaEventElapsedTime(&ms, evs[k]->a, evs[k]->b) == cudaSuccess) out[k].search_ns = (uint64_t)((double)ms * 1e6);
+            else cudaGetLastError();
+        }
+    }
+    return (out[0].status == CAMELOT_OK && out[1].status == CAMELOT_OK) ? CAMELOT_OK : CAMELOT_INFEASIBLE;
 }
 
 int camelot_predict(const camelot_problem *p, const camelot_cluster *c, const int32_t *batch, const int32_t *replicas,

@@ -53,6 +53,8 @@ struct FilterSmem {
     int minNP[NMAX];
     int Qs[CAMELOT_MAX_QUOTAS];
     unsigned char oth[OMAX], oN[OMAX];        // option code -> (theta, N) (no divisions in the rounds)
+    unsigned char qpass[NMAX][CAMELOT_MAX_QUOTAS];   // (stage, quota): the duration passes the QoS bound
+    long long ulim[NMAX];                     // per stage: largest N p passing the quota bounds
 };
 
 // Filter body for batch b, executed by one whole CTA (any blockDim multiple of 32).
@@ -135,14 +137,15 @@ CAM_DEVFN void filter_body(const DevProb &P, const FilterArgs &F, int b, FilterS
         __syncthreads();
         FTRACE(6);
         if (it == rounds) break;
-        bool changed = false;
-        for (int i = 0; i < n; ++i)
-        for (int o = tid; o < O; o += blockDim.x) {
-            if (!keep[i][o]) continue;
-            const int th = fsm.oth[o], N = fsm.oN[o];
-            const int a = P.app[i];
+        // The QoS test depends on the option only through its duration, i.e. its quota
+        // theta (not N): it is evaluated once per (stage, theta).  The quota tests are
+        // monotone in U = N p + rest_i: U <= C R, and (min-resource with an incumbent
+        // (u*, U*)) not (ceil(U/R) > u* or (ceil(U/R) >= u* and U > U*)), i.e.
+        // U <= min(u* R, max((u* - 1) R, U*)); so N p <= ulim_i (one threshold per stage).
+        for (int q = tid; q < n * nQ; q += blockDim.x) {
+            const int i = q / nQ, th = q % nQ, a = P.app[i];
             const float dur = tabs[i * nQ + th].x;
-            // QoS: ordered fp32 sum with this option's duration and the others' minima
+            // ordered fp32 sum with this duration at position i and the others' minima
             float ls = 0.0f;
             for (int k2 = P.first_of_app[a]; k2 <= P.last_of_app[a]; ++k2) {
                 const float t = (k2 == i) ? dur : mindur[k2];
@@ -150,19 +153,30 @@ CAM_DEVFN void filter_body(const DevProb &P, const FilterArgs &F, int b, FilterS
                     ls = __fadd_rn(ls, fminf(P.ipc_ms, __fmul_rn(__fmul_rn(P.comm_mb[k2 - 1], (float)P.S[b]), P.inv_link)));
                 ls = (k2 == P.first_of_app[a]) ? t : __fadd_rn(ls, t);
             }
-            bool k = ls <= P.qos[a];
-            // quota: N p + sum of the other stages' minimal N p  <=  C R
-            long long U = (long long)N * Qs[th];
+            fsm.qpass[i][th] = ls <= P.qos[a];
+        }
+        if (tid < n) {
+            const int i = tid, a = P.app[i];
+            long long rest = 0;
             for (int k2 = 0; k2 < n; ++k2)
-                if (k2 != i) U += (P.app[k2] == a) ? (long long)minNP[k2] : (long long)P.Q[0];
-            if (U > (long long)P.C * P.R) k = false;
-            if (F.policy == 1 && has_inc) {
-                const long long ulb = (U + P.R - 1) / P.R;
-                if (ulb > uinc || (ulb >= uinc && U > Uinc)) k = false;
-            }
-            if (!k) {
-                keep[i][o] = 0;
-                changed = true;
+                if (k2 != i) rest += (P.app[k2] == a) ? (long long)minNP[k2] : (long long)Qs[0];
+            long long lim = (long long)P.C * P.R;
+            if (F.policy == 1 && has_inc)
+                lim = min(lim, min((long long)uinc * P.R, max((long long)(uinc - 1) * P.R, (long long)Uinc)));
+            fsm.ulim[i] = lim - rest;
+        }
+        __syncthreads();
+        bool changed = false;
+        for (int i = 0; i < n; ++i) {
+            const long long ul = fsm.ulim[i];
+            for (int o = tid; o < O; o += blockDim.x) {
+                if (!keep[i][o]) continue;
+                const int th = fsm.oth[o], N = fsm.oN[o];
+                const bool k = fsm.qpass[i][th] && (long long)N * Qs[th] <= ul;
+                if (!k) {
+                    keep[i][o] = 0;
+                    changed = true;
+                }
             }
         }
         // fixpoint reached: the minima of the next round would be the same
@@ -429,6 +443,17 @@ CAM_GLOBAL void __launch_bounds__(PLAN_THREADS) plan_kernel(const DevProb P, int
     const uint32_t *src = reinterpret_cast<const uint32_t *>(&pl);
     uint32_t *dst = reinterpret_cast<uint32_t *>(out + k);
     for (int q = tid; q < (int)(sizeof(camelot_plan) / 4); q += blockDim.x) dst[q] = src[q];
+}
+
+// The low load of camelot_plan_max_then_min (low load = a fraction
+// of the peak): load_a = fl(frac * T*) for every application, T* the max-load
+// plan's objective (the binary32 rounding of the float64 product, as a host caller
+// computing frac * T* in double and storing it as float); +inf when there is no
+// feasible peak (every min-resource candidate then fails LOAD).
+CAM_GLOBAL void low_load_kernel(const DevProb P, const camelot_plan *ml, double frac, float *lam) {
+    const int a = threadIdx.x;
+    if (a >= P.A) return;
+    lam[a] = ml->status == CAMELOT_OK ? __double2float_rn(frac * (double)ml->objective) : __int_as_float(0x7f800000);
 }
 
 // Naive exhaustive search (kernel N5 as a search): one thread scores one

@@ -35,7 +35,10 @@ __device__ __forceinline__ bool getenv_tmode_off() {
 #endif
 }
 
-constexpr int SEARCH_THREADS = 256;
+#ifndef CAMELOT_SEARCH_THREADS
+#define CAMELOT_SEARCH_THREADS 256
+#endif
+constexpr int SEARCH_THREADS = CAMELOT_SEARCH_THREADS;
 constexpr int SEARCH_WARPS = SEARCH_THREADS / 32;
 #ifndef SEARCH_MINB
 #define SEARCH_MINB 1   // measured with the thread-per-parent mode: 255 regs x 1 CTA (no spills) beats 128 x 2 (C4 1.51 vs 1.75 ms)
@@ -991,12 +994,12 @@ CAM_DEVFN void reduce_slots_block(const DevProb &P, const Slot *slots, int nslot
             }
             result[k].key = bk;
             result[k].x = bx;
-            if (inc_out) {
+            if (inc_out) {   // incumbent-cascade level: its packed key is never read (no item_of walk)
                 inc_out[k].key = bk;
                 inc_out[k].x = bx;
             }
             unsigned long long packed;
-            if (bk == 0xFFFFFFFFull) packed = ~0ull;
+            if (bk == 0xFFFFFFFFull || inc_out) packed = ~0ull;
             else {
                 unsigned long long low = (P.ntot <= (1ull << 32)) ? bx
                                          : flat_shift >= 0 ? (bx >> flat_shift)
@@ -1328,6 +1331,7 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
     bool first = true;
     while (true) {
         if (!first) {
+            if (nw >= items) break;   // every item was assigned statically: no queue round trip
             if (lane == 0) e0 = nw + atomicAdd(S.head, (unsigned long long)grab);
             e0 = __shfl_sync(0xffffffffu, e0, 0);
         }
@@ -1337,13 +1341,24 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
 #endif
         PTM(1);
         if (e0 >= items) break;
-        if (lane == 0) {   // refresh the pruning bounds from the device-wide best
-            const unsigned long long g = (unsigned long long)(*(volatile unsigned int *)&S.hdr->best_obj);
-            if (g < wb->bound) wb->bound = g;
-            const unsigned long long gp = *(volatile unsigned long long *)&S.hdr->best_packed;
-            if (gp < wb->gpack) wb->gpack = gp;
+        // refresh the pruning bounds from the device-wide best: both loads issued
+        // together; the warp mode applies them only after the parent copy (the two
+        // round trips overlap)
+        unsigned long long g_obj = ~0ull, g_pk = ~0ull;
+        if (lane == 0) {
+            g_obj = (unsigned long long)(*(volatile unsigned int *)&S.hdr->best_obj);
+            g_pk = *(volatile unsigned long long *)&S.hdr->best_packed;
         }
-        __syncwarp();
+        bool bounds_pending = true;
+        auto apply_bounds = [&]() {
+            if (lane == 0) {
+                if (g_obj < wb->bound) wb->bound = g_obj;
+                if (g_pk < wb->gpack) wb->gpack = g_pk;
+            }
+            __syncwarp();
+            bounds_pending = false;
+        };
+        if (screen || tmode) apply_bounds();
         const unsigned long long e1 = min(e0 + (unsigned long long)grab, items);
         unsigned live = 0xffffffffu;
         if (screen || tmode) {
@@ -1384,15 +1399,14 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
             if (!((live >> (unsigned)(it - e0)) & 1u)) continue;
             if (screen && it > e0) {   // refresh the bounds per parent
                 if (lane == 0) {
-                    const unsigned long long g = (unsigned long long)(*(volatile unsigned int *)&S.hdr->best_obj);
-                    if (g < wb->bound) wb->bound = g;
-                    const unsigned long long gp = *(volatile unsigned long long *)&S.hdr->best_packed;
-                    if (gp < wb->gpack) wb->gpack = gp;
+                    g_obj = (unsigned long long)(*(volatile unsigned int *)&S.hdr->best_obj);
+                    g_pk = *(volatile unsigned long long *)&S.hdr->best_packed;
                 }
-                __syncwarp();
+                apply_bounds();
             }
             const unsigned long long e = split == 1 ? it : it / (unsigned)split;
             const int blk = split == 1 ? 0 : (int)(it % (unsigned)split);
+            __syncwarp();   // the previous item's readers of the stack are done (WAR)
             if (!have_in) {
                 build_root<CM>(P, (int)e, stack[0], lane);
                 if (lane < NMAX) stack[0].kidx[lane] = 0;
@@ -1400,6 +1414,7 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
             } else {
                 copy_node<CM>(stack[jtop], in, e, lane);
             }
+            if (bounds_pending) apply_bounds();
             PTM(2);
             {
                 const int cnt0 = (int)sb_at(P, S, jtop, stack[jtop].b[P.app[jtop]]).cnt;

@@ -242,14 +242,28 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
         if (lane == 0) it = atomicAdd(&A.hdr->chunk_counter, 1ull);
         it = __shfl_sync(0xffffffffu, it, 0);
         if (it >= A.n_items) break;
-        const unsigned long long gp = A.g_lo + it / (unsigned)A.nchunk;
-        const int ch = (int)(it % (unsigned)A.nchunk);
+        // work item: one grandparent x 32 parents, or (small sub-grids, Os <= 16) gpack
+        // grandparents x Os parents, lane = (grandparent, parent) pair
+        const int gpk = A.gpack;
+        const int lg = gpk == 1 ? 0 : lane / Os;   // this lane's grandparent in the item
+        bool lane_ok = true;
+        unsigned long long gp;
+        int ch;
+        if (gpk == 1) {
+            gp = A.g_lo + it / (unsigned)A.nchunk;
+            ch = (int)(it % (unsigned)A.nchunk);
+        } else {
+            const unsigned long long g0 = it * (unsigned long long)gpk + (unsigned long long)lg;
+            lane_ok = lg < gpk && g0 < A.n_gp;
+            gp = A.g_lo + (lane_ok ? g0 : 0ull);
+            ch = 0;
+        }
         // bound: the best objective key found anywhere so far (a feasible candidate), so a
         // leaf whose key bound is strictly worse cannot win (skips only the divisions)
         unsigned long long gkey = 0;
         if (lane == 0) gkey = *(volatile unsigned int *)&A.hdr->best_obj;
         gkey = min(__shfl_sync(0xffffffffu, gkey, 0), bk);
-        // ---- grandparent (warp-uniform): batch combo + options of stages 0..n-3
+        // ---- grandparent (warp-uniform unless gpack > 1): batch combo + options of stages 0..n-3
         int beta[AMAX];
         int o[NS];
         {
@@ -268,7 +282,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
         }
         SwState<CM, NS> st;
         sw_init<CM, NS>(P, st);
-        bool ok = true;
+        bool ok = lane_ok;
         float dur[NS], bwv[NS], ntv[NS];
 #pragma unroll
         for (int i = 0; i < NS; ++i) {
@@ -286,9 +300,9 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
                 ntv[i] = __fmul_rn((float)N, e.y);
             }
         }
-        if (!ok) continue;   // the whole grandparent is infeasible (uniform)
+        if (gpk == 1 && !ok) continue;   // the whole grandparent is infeasible (uniform)
         // ---- parent (per lane): option of stage n-2
-        const int ops = ch * 32 + lane;              // parent option in the (sub-)grid
+        const int ops = gpk == 1 ? ch * 32 + lane : lane % Os;   // parent option in the (sub-)grid
         const int op = canon(min(ops, Os - 1));      // canonical option code
         unsigned long long gpc = 0;                  // canonical grandparent index
         {
@@ -304,7 +318,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
         int clo = 0, chi = O;
         if (A.lo > xpO) clo = (int)min(A.lo - xpO, (unsigned long long)O);
         if (A.hi < xpO + O) chi = A.hi > xpO ? (int)(A.hi - xpO) : 0;
-        bool act = ops < Os && clo < chi;
+        bool act = ok && ops < Os && clo < chi;
         if (act && A.world > 1) {
             const unsigned long long item = xp / P.opow[n - 1 - A.d0];
             act = ((item / 64ull) % (unsigned long long)A.world) == (unsigned long long)A.rank;
@@ -427,7 +441,10 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
             } else {
                 for (int N = 1; N <= Rmax; ++N) c_sc += (unsigned)((N - 1) * nQ + th - clo) < span;
             }
-            if (nok < Rmax) {   // the failing leaves: first-failing dimensions (OR over GPUs, k = 1)
+            // the failing leaves: first-failing dimensions (OR over GPUs, k = 1).  Only an
+            // INFEASIBLE result reports them, so they are skipped once a feasible candidate
+            // is known (the lane's best, the incumbent or the device-wide best)
+            if (nok < Rmax && bk >= 0xFFFFFFFFull && gkey >= 0xFFFFFFFFull) {
                 bool any = full;
                 for (int N = nok + 1; N <= Rmax && !any; ++N) any = (unsigned)((N - 1) * nQ + th - clo) < span;
                 if (any)

@@ -12,6 +12,9 @@ struct SweepArgs {
     unsigned long long g_lo;          // first grandparent
     unsigned long long n_items;       // grandparents x nchunk
     int nchunk;                       // ceil(Os / 32) parent chunks per grandparent
+    int gpack;                        // grandparents per warp item: 1, or 32 / Os when Os <= 16
+                                      // (lane = (grandparent, parent) pair; nchunk = 1)
+    unsigned long long n_gp;          // grandparents in [g_lo, g_lo + n_gp) (bound for gpack > 1)
     int qstride;                      // quota sub-grid: every qstride-th quota from the top (1 = all)
     int nQs;                          // sub-grid size (nQ - 1) / qstride + 1; Os = Rmax * nQs
     const float *lam;                 // [A] load level (min-resource)
