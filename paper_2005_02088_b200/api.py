@@ -302,8 +302,8 @@ class Session:
         L.check(min(n, 0), False)
         if n == 0:
             return []
-        t0 = out[0] & ((1 << 48) - 1)
         m = (1 << 48) - 1
+        t0 = next((out[i] & m for i in range(min(n, 256)) if (out[i] >> 48) < 64), 0)   # the first timestamp
         # tags < 64 are timestamps (ns since the first mark), tags >= 64 are values
         return [(out[i] >> 48, (out[i] & m) - (t0 if (out[i] >> 48) < 64 else 0)) for i in range(min(n, 256))]
 

@@ -384,11 +384,29 @@ int launch_search(const Ctx &X, const SearchArgs &S, int grid) {
         return policy ? FN<16, 8, 1>(__VA_ARGS__) : FN<16, 8, 0>(__VA_ARGS__);                         \
     } while (0)
 
+// staged option lists (TMA bulk copy of the level's compacted lists into every CTA's
+// shared memory): the shared memory left after the level state, up to the opt-in
+// per-block maximum.  Opt-in (CAMELOT_STAGE_RECORDS=1): measured on C4 it costs
+// ~45 us per step (the staging phase per level, and 48-byte-strided LDS.128 reads are
+// no faster than the L1 hits they replace)
 template <int CM>
-size_t level_smem() {   // filter scratch, then search state + StageBound cache (n x nS <= 8 x 64)
-    return std::max(search_smem_bytes<CM>() + (size_t)NMAX * CAMELOT_MAX_BATCHES * sizeof(StageBound) +
-                        (ITEM_SMEM + 1) * sizeof(unsigned long long),
-                    sizeof(FilterSmem));
+unsigned rec_budget_for(int dev, bool honour_env = true) {
+    static int cache[64] = {0};
+    int mx = dev < 64 ? cache[dev] : 0;
+    if (!mx) {
+        if (cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) {
+            cudaGetLastError();
+            mx = 48 * 1024;
+        }
+        if (dev < 64) cache[dev] = mx;
+    }
+    if (honour_env && (!getenv("CAMELOT_STAGE_RECORDS") || getenv("CAMELOT_NO_STAGE"))) return 0;
+    const size_t fixed = level_fixed_bytes<CM>() + 16;
+    return mx > (int)fixed + 1024 ? (unsigned)((mx - fixed - 1024) / 16 * 16) : 0u;
+}
+template <int CM>
+size_t level_smem(int dev, bool honour_env = true) {   // filter scratch / search state, mbarrier, staged lists
+    return level_fixed_bytes<CM>() + 16 + rec_budget_for<CM>(dev, honour_env);
 }
 
 template <int CM, int NS, int POL>
@@ -401,7 +419,7 @@ int coop_grid_for(int dev, int &grid) {
             grid = e.second;
             return CAMELOT_OK;
         }
-    const size_t sm = level_smem<CM>();
+    const size_t sm = level_smem<CM>(dev, false);   // the largest launch (attribute + occupancy)
     int per = 0, nsm = 0;
     CU((k_level_occupancy<CM, NS, POL>(sm, &per)));
     CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
@@ -419,11 +437,13 @@ int launch_level(const Ctx &X, int dev, const std::vector<LevelArgs> &levels) {
     memset(&LS, 0, sizeof(LS));
     if (levels.empty() || levels.size() > (size_t)MAX_LEVELS) return fail(CAMELOT_EINVAL, "bad level count");
     LS.count = (int)levels.size();
+    const unsigned budget = rec_budget_for<CM>(dev);
     for (int l = 0; l < LS.count; ++l) {
         LS.L[l] = levels[l];
         LS.L[l].F.nslots = grid * LS.L[l].S.nlev;
+        LS.L[l].rec_budget = budget;
     }
-    const size_t sm = level_smem<CM>();
+    const size_t sm = level_smem<CM>(dev);
     CU((k_level_launch<CM, NS, POL>(X.P, LS, grid, sm, X.st)));
     COUNT_LAUNCH();
     return CAMELOT_OK;
@@ -614,6 +634,8 @@ int sweep_pass(const Ctx &X, int dev, int policy, int nlev, const Slot *inc, Slo
     A.hdr = hdr;
     A.result = result;
     A.keys = keys;
+    const size_t tb = (size_t)X.d.nS * X.d.nQ * sizeof(float4);
+    A.tabL_bytes = (tb <= SWEEP_TABL_MAX && !getenv("CAMELOT_NO_STAGE")) ? (unsigned)tb : 0u;
     CU(sweep_launch(X.P, A, dev, X.st));
     COUNT_LAUNCH();
     return CAMELOT_OK;

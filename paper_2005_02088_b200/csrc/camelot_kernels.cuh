@@ -47,7 +47,7 @@ CAM_DEVFN void item_offsets(const DevProb &P, const StageBound *sb, int d0, unsi
 // An option survives unless it provably cannot be part of a feasible
 // candidate at least as good as the incumbent.
 struct FilterSmem {
-    float4 tabs[NMAX * CAMELOT_MAX_QUOTAS];   // this batch's table slice (staged once)
+    float4 tabs[NMAX * CAMELOT_MAX_QUOTAS];   // this batch's table slice (TMA: one bulk copy per stage row)
     unsigned char keep[NMAX][OMAX];
     float mindur[NMAX];
     int minNP[NMAX];
@@ -63,7 +63,10 @@ struct FilterSmem {
 #else
 #define FTRACE(t)
 #endif
-CAM_DEVFN void filter_body(const DevProb &P, const FilterArgs &F, int b, FilterSmem &fsm) {
+// bar: an initialised mbarrier outside fsm (count 1) whose next phase has parity
+// `phase & 1`; the table staging uses one phase (phase is advanced)
+CAM_DEVFN void filter_body(const DevProb &P, const FilterArgs &F, int b, FilterSmem &fsm, unsigned long long *bar,
+                           unsigned &phase) {
     auto &keep = fsm.keep;
     auto &mindur = fsm.mindur;
     auto &minNP = fsm.minNP;
@@ -71,12 +74,22 @@ CAM_DEVFN void filter_body(const DevProb &P, const FilterArgs &F, int b, FilterS
     auto &Qs = fsm.Qs;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int n = P.n, O = P.O, nQ = P.nQ;
-    for (int q = tid; q < n * nQ; q += blockDim.x) tabs[q] = P.tab[((size_t)(q / nQ) * P.nS + b) * nQ + q % nQ];
+    // the per-stage predictor rows of batch b (table [n][nS][nQ] of float4: row (i, b) is
+    // nQ x 16 contiguous bytes) -> shared memory with the TMA engine, one bulk copy per stage
+    __syncthreads();   // earlier generic accesses of the scratch are complete
+    if (tid == 0) {
+        fence_proxy_async();
+        mbar_arrive_expect_tx(bar, (uint32_t)(n * nQ * sizeof(float4)));
+        for (int i = 0; i < n; ++i)
+            bulk_g2s(tabs + i * nQ, P.tab + ((size_t)i * P.nS + b) * nQ, (uint32_t)(nQ * sizeof(float4)), bar);
+    }
     for (int q = tid; q < nQ; q += blockDim.x) Qs[q] = P.Q[q];
     for (int o = tid; o < O; o += blockDim.x) {
         fsm.oth[o] = (unsigned char)(o % nQ);
         fsm.oN[o] = (unsigned char)(o / nQ + 1);
     }
+    mbar_wait(bar, phase & 1u);
+    ++phase;
     __syncthreads();
     FTRACE(4);
     const bool cap = !(P.flags & F_NO_BW_CAP);
@@ -233,8 +246,12 @@ CAM_DEVFN void filter_body(const DevProb &P, const FilterArgs &F, int b, FilterS
 // (+ fused: search-slot reset and, by the last block, the item offsets).
 CAM_GLOBAL void __launch_bounds__(FILTER_THREADS) filter_kernel(const DevProb P, const FilterArgs F) {
     __shared__ FilterSmem fsm;
+    __shared__ unsigned long long bar;
     const int tid = threadIdx.x;
-    filter_body(P, F, blockIdx.x, fsm);
+    if (tid == 0) mbar_init(&bar, 1);
+    __syncthreads();
+    unsigned phase = 0;
+    filter_body(P, F, blockIdx.x, fsm, &bar, phase);
     if (F.slots)
         for (int q = blockIdx.x * blockDim.x + tid; q < F.nslots; q += gridDim.x * blockDim.x) {
             F.slots[q].key = 0xFFFFFFFFull;
@@ -402,7 +419,39 @@ CAM_GLOBAL void __launch_bounds__(PLAN_THREADS) plan_kernel(const DevProb P, int
             pl.violations = hdr->viol_or;
         } else {
             decode_index(P, w.x, beta, rho, theta);
-            score_digits(P, beta, rho, theta, s, &scr);
+        }
+    }
+    __syncthreads();
+    // the winner's placement: warp 0 in parallel (one lane per GPU); the serial
+    // score_digits only for PAPER_GLOBAL problems or a placement failure
+    if (w.x != ~0ull && tid < 32) {
+        bool placed = false;
+        if (!(P.flags & F_PAPER_GLOBAL)) {
+            float dur[NMAX], thr[NMAX], bwv[NMAX], kmax[NMAX];
+            uint32_t hm[NMAX];
+            for (int i = 0; i < P.n; ++i) {
+                const float4 e = P.tab[((size_t)i * P.nS + beta[P.app[i]]) * P.nQ + theta[i]];
+                dur[i] = e.x;
+                thr[i] = e.y;
+                bwv[i] = e.z;
+            }
+            for (int q = tid; q < NMAX * SCORE_RMAX; q += 32) s.goi[q] = -1;
+            __syncwarp();
+            int u = 0;
+            placed = place_warp(P, beta, rho, theta, bwv, kmax, hm, s.goi, u);
+            __syncwarp();
+            if (placed && tid == 0) {
+                int U = 0;
+                for (int i = 0; i < P.n; ++i) U += (rho[i] + 1) * P.Q[theta[i]];
+                s.U = U;
+                score_finish(P, beta, rho, dur, thr, kmax, hm, 0u, u, s);
+            }
+        }
+        if (!placed && tid == 0) score_digits(P, beta, rho, theta, s, &scr);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        if (w.x != ~0ull) {
             eq2y = policy == 1 ? eq2_gpus(P, beta, lam + k * P.A) : 0;
             pl.index = w.x;
             pl.status = CAMELOT_OK;
@@ -644,13 +693,28 @@ struct LevelArgs {
     FilterArgs F;
     void *buf0, *buf1; // frontier ping-pong buffers
     unsigned long long fcap;
+    unsigned rec_budget;   // bytes of shared memory for the staged option lists (0: never stage)
 };
+
+// Dynamic shared memory of a search level: max(filter scratch, search state +
+// StageBound cache + item offsets + list offsets), then the staging mbarrier (16 B),
+// then the staged option lists (LevelArgs::rec_budget bytes).
+template <int CM>
+__host__ __device__ constexpr size_t level_state_bytes() {
+    return search_smem_bytes<CM>() + (size_t)NMAX * CAMELOT_MAX_BATCHES * sizeof(StageBound) +
+           (ITEM_SMEM + 1) * sizeof(unsigned long long) + (NMAX * CAMELOT_MAX_BATCHES + 1) * sizeof(int);
+}
+template <int CM>
+__host__ __device__ constexpr size_t level_fixed_bytes() {
+    return ((level_state_bytes<CM>() > sizeof(FilterSmem) ? level_state_bytes<CM>() : sizeof(FilterSmem)) + 15) /
+           16 * 16;
+}
 
 // One search level (incumbent cascade level or main pass) executed by the whole
 // cooperative grid; levels are chained inside one launch (search_level_kernel).
 template <int CM, int NS, int POLICY>
 __device__ __forceinline__ void level_body(const DevProb &P, const LevelArgs &LA, unsigned char *smem_raw,
-                                           cooperative_groups::grid_group &grid) {
+                                           cooperative_groups::grid_group &grid, unsigned &stage_phase) {
     SearchArgs S = LA.S;
     DevHeader *hdr = S.hdr;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -670,7 +734,8 @@ __device__ __forceinline__ void level_body(const DevProb &P, const LevelArgs &LA
     if (tr) trace_mark(hdr, 1);
     // phase 1: option filter (one CTA per batch) and slot reset
     for (int b = blockIdx.x; b < P.nS; b += gridDim.x) {
-        filter_body(P, LA.F, b, *reinterpret_cast<FilterSmem *>(smem_raw));
+        filter_body(P, LA.F, b, *reinterpret_cast<FilterSmem *>(smem_raw),
+                    reinterpret_cast<unsigned long long *>(smem_raw + level_fixed_bytes<CM>()), stage_phase);
         __syncthreads();
     }
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < gridDim.x * S.nlev; q += gridDim.x * blockDim.x) {
@@ -700,6 +765,36 @@ __device__ __forceinline__ void level_body(const DevProb &P, const LevelArgs &LA
             grid.sync();
             if (blockIdx.x == 0 && threadIdx.x == 0) item_offsets(P, S.sb, S.d0, LA.F.item_off, hdr);
             grid.sync();
+        }
+        // the level's compacted option lists -> this CTA's shared memory with the TMA
+        // engine (cp.async.bulk, one copy per (stage, batch) list), when they fit
+        int *recoff = reinterpret_cast<int *>(reinterpret_cast<unsigned long long *>(sbs + NMAX * CAMELOT_MAX_BATCHES) +
+                                              ITEM_SMEM + 1);
+        unsigned long long *mbar = reinterpret_cast<unsigned long long *>(smem_raw + level_fixed_bytes<CM>());
+        OptRec *rec_s = reinterpret_cast<OptRec *>(smem_raw + level_fixed_bytes<CM>() + 16);
+        const int nl = P.n * P.nS;
+        if (threadIdx.x == 0) {
+            int acc = 0;
+            for (int q = 0; q < nl; ++q) {
+                recoff[q] = acc;
+                acc += (int)sbs[q].cnt;
+            }
+            recoff[nl] = acc;
+        }
+        __syncthreads();
+        const unsigned long long bytes = (unsigned long long)recoff[nl] * sizeof(OptRec);
+        if (bytes > 0 && bytes <= LA.rec_budget) {
+            if (threadIdx.x == 0) {
+                fence_proxy_async();   // the filter's generic stores (before the grid barrier) -> async reads
+                mbar_arrive_expect_tx(mbar, (uint32_t)bytes);
+                for (int q = 0; q < nl; ++q)
+                    if (sbs[q].cnt)
+                        bulk_g2s(rec_s + recoff[q], S.rec + (size_t)q * P.O, sbs[q].cnt * (uint32_t)sizeof(OptRec), mbar);
+            }
+            mbar_wait(mbar, stage_phase & 1u);
+            ++stage_phase;
+            S.rec_stage = rec_s;
+            S.rec_off = recoff;
         }
         if (tr) trace_mark(hdr, 3);
     }
@@ -756,6 +851,10 @@ __device__ __forceinline__ void level_body(const DevProb &P, const LevelArgs &LA
         unsigned long long *sk = reinterpret_cast<unsigned long long *>(smem_raw);
         reduce_slots_block(P, S.slots, gridDim.x, S.nlev, S.result, S.keys, S.inc_out, S.sb, S.rec, S.item_off, S.d0,
                            S.chunk_items, -1, sk, sk + SEARCH_THREADS);
+        if (tr) {   // the level's optimum (objective key, canonical index) in the phase trace
+            trace_value(hdr, 200, S.result[0].key);
+            trace_value(hdr, 201, S.result[0].x);
+        }
     }
 }
 
@@ -774,8 +873,11 @@ __global__ void __launch_bounds__(SEARCH_THREADS, SEARCH_MINB)
 search_level_kernel(const DevProb P, const LevelSet LS) {
     cooperative_groups::grid_group grid = cooperative_groups::this_grid();
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    unsigned stage_phase = 0;   // phase of the staging mbarrier (one per staged level)
+    if (threadIdx.x == 0) mbar_init(reinterpret_cast<unsigned long long *>(smem_raw + level_fixed_bytes<CM>()), 1);
+    __syncthreads();
     for (int l = 0; l < LS.count; ++l) {
-        level_body<CM, NS, POLICY>(P, LS.L[l], smem_raw, grid);
+        level_body<CM, NS, POLICY>(P, LS.L[l], smem_raw, grid, stage_phase);
         __syncthreads();   // block 0's reduction used shared memory
     }
 }

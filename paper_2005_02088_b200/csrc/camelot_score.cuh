@@ -60,6 +60,10 @@ struct ScoreScratch {
     uint8_t hcnt[NMAX][SCORE_CMAX];
 };
 
+__device__ __forceinline__ void score_finish(const DevProb &P, const int *beta, const int *rho, const float *dur,
+                                             const float *thr, const float *kmax, const uint32_t *out_hmask,
+                                             uint32_t pv, int u, FullScore &out);
+
 CAM_DEVFN void score_digits(const DevProb &P, const int *beta, const int *rho, const int *theta,
                              FullScore &out, ScoreScratch *scr = nullptr) {
     const int n = P.n, C = P.C;
@@ -183,6 +187,16 @@ CAM_DEVFN void score_digits(const DevProb &P, const int *beta, const int *rho, c
             for (int i = 0; i < n; ++i) kmax[i] = 1.0f;
         }
     }
+    score_finish(P, beta, rho, dur, thr, kmax, out_hmask, pv, u, out);
+}
+
+// The predictions and verdict of a placed candidate (shared by score_digits and the
+// warp-parallel placement of plan_kernel): kmax = contention factor per stage,
+// hmask = GPU mask per stage, pv = placement failure bits (0 = placed), u = GPUs used.
+__device__ __forceinline__ void score_finish(const DevProb &P, const int *beta, const int *rho, const float *dur,
+                                             const float *thr, const float *kmax, const uint32_t *out_hmask,
+                                             uint32_t pv, int u, FullScore &out) {
+    const int n = P.n;
     out.u = u;
     out.place_viol = pv;
     for (int i = 0; i < n; ++i) {
@@ -222,6 +236,88 @@ CAM_DEVFN void score_digits(const DevProb &P, const int *beta, const int *rho, c
     }
     out.T = T;
     out.verdict = pv ? pv : (qos_fail ? V_QOS : 0u);
+}
+
+// Warp-parallel placement of ONE candidate (plan_kernel; all 32 lanes of a warp):
+// lane g < C owns GPU g.  The same deployment as score_digits (DESIGN.md 3.2,
+// PAPER.md L929-945): the order is (remaining MiB, remaining quota, id) ascending
+// (rank = number of GPUs with a smaller packed key); pass 1 = the GPU of smallest rank
+// that fits all N replicas; pass 2 = greedy k_g = min(c_g, N - (capacity of the GPUs
+// before g)), with c_g = canHold(g, N) (fits is monotone in k, and deploying on other
+// GPUs does not change g's state).  Writes kmax / hmask / goi / u for score_finish.
+// Returns false (uniformly) when a stage does not fit: the caller then scores the
+// candidate with score_digits, which also derives the failure bits.
+__device__ __forceinline__ bool place_warp(const DevProb &P, const int *beta, const int *rho, const int *theta,
+                                           const float *bwv, float *kmax, uint32_t *hmask, int8_t *goi, int &u) {
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31, C = P.C, n = P.n;
+    const bool own = lane < C;
+    int rq = own ? P.R : 0, cnt = 0;
+    uint32_t rm = own ? P.FM : 0u;
+    float dem = 0.0f;
+    int hc[NMAX];
+#pragma unroll
+    for (int i = 0; i < NMAX; ++i) hc[i] = 0;
+#pragma unroll
+    for (int i = 0; i < NMAX; ++i) {
+        if (i < n) {
+            const int p = P.Q[theta[i]], N = rho[i] + 1;
+            const uint32_t As = P.Am[i] * (uint32_t)P.S[beta[P.app[i]]], W = P.W[i];
+            const float bw = bwv[i];
+            auto fits = [&](int k) { return own && fit_viol(P, rq, cnt, rm, dem, k, p, W, As, bw) == 0u; };
+            const unsigned long long key =
+                own ? (((unsigned long long)rm << 12) | ((unsigned long long)(uint32_t)rq << 4) | (unsigned)lane) : ~0ull;
+            int rank = 0;
+            for (int h = 0; h < C; ++h) rank += __shfl_sync(FULL, key, h) < key;
+            int k = 0;
+            const int r1 = __reduce_min_sync(FULL, fits(N) ? rank : 0x7fffffff);
+            if (r1 != 0x7fffffff) {
+                k = (own && rank == r1) ? N : 0;
+            } else {
+                int c = 0;
+                if (own)
+                    for (int kk = N; kk >= 1; --kk)
+                        if (fits(kk)) {
+                            c = kk;
+                            break;
+                        }
+                int pre = 0, tot = 0;
+                for (int h = 0; h < C; ++h) {
+                    const int ch = __shfl_sync(FULL, c, h), rh = __shfl_sync(FULL, rank, h);
+                    tot += ch;
+                    if (rh < rank) pre += ch;
+                }
+                if (tot < N) return false;
+                k = own ? min(c, max(0, N - pre)) : 0;
+            }
+            if (k > 0) {
+                rq -= k * p;
+                cnt += k;
+                rm -= W + (uint32_t)k * As;
+                dem = __fadd_rn(dem, __fmul_rn((float)k, bw));
+            }
+            hc[i] = k;
+        }
+    }
+    u = __popc(__ballot_sync(FULL, own && cnt > 0));
+#pragma unroll
+    for (int i = 0; i < NMAX; ++i) {
+        if (i < n) {
+            hmask[i] = __ballot_sync(FULL, hc[i] > 0);
+            float dm = hc[i] > 0 ? dem : 0.0f;   // max demand over the GPUs hosting stage i
+            for (int off = 16; off; off >>= 1) dm = fmaxf(dm, __shfl_xor_sync(FULL, dm, off));
+            kmax[i] = kappa_of(dm, bwv[i], P.gamma[i], P.invBW, P.flags);
+            int pre = hc[i];   // inclusive prefix over GPU index: replicas listed by GPU index
+            for (int off = 1; off < 32; off <<= 1) {
+                const int v = __shfl_up_sync(FULL, pre, off);
+                if (lane >= off) pre += v;
+            }
+            pre -= hc[i];
+            for (int r = 0; r < hc[i]; ++r)
+                if (pre + r < SCORE_RMAX) goi[i * SCORE_RMAX + pre + r] = (int8_t)lane;
+        }
+    }
+    return true;
 }
 
 // level verdict for min-resource load level (lam: [A]); y = Eq. 2 estimate

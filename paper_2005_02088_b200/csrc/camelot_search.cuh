@@ -53,6 +53,8 @@ struct SearchArgs {
     int prune;                  // 0 = flat scan (bounds off)
     unsigned long long lo, hi;  // canonical index range
     const OptRec *rec;          // [n][nS][O] compacted surviving options (ascending code)
+    const OptRec *rec_stage;    // per-CTA shared-memory copy of the compacted lists (or nullptr)
+    const int *rec_off;         // [n][nS] offset of list (i, b) in rec_stage (when staged)
     const StageBound *sb;       // [n][nS]
     const unsigned long long *item_off;  // [nbc + 1]
     const float *lam;           // [nlev][A] load levels (min-resource)
@@ -234,9 +236,13 @@ __device__ __forceinline__ uint32_t place_fail_bits(const DevProb &P, const Node
     return v ? v : V_QUOTA;
 }
 
-__device__ __forceinline__ const OptRec &opt_at(const DevProb &P, const SearchArgs &S, int i, int b, int k) {
-    return S.rec[((size_t)i * P.nS + b) * P.O + k];
+// compacted option list of (stage i, batch b): the CTA's shared-memory copy when the
+// level staged it (TMA bulk copy after the filter), else the global [n][nS][O] array
+__device__ __forceinline__ const OptRec *list_of(const DevProb &P, const SearchArgs &S, int i, int b) {
+    return S.rec_off ? S.rec_stage + S.rec_off[i * P.nS + b] : S.rec + ((size_t)i * P.nS + b) * P.O;
 }
+// one 16-byte chunk of a record (generic load: the list may be in shared or global memory)
+__device__ __forceinline__ uint4 rec_chunk(const OptRec *r, int c) { return reinterpret_cast<const uint4 *>(r)[c]; }
 __device__ __forceinline__ const StageBound &sb_at(const DevProb &P, const SearchArgs &S, int i, int b) {
     return S.sb[(size_t)i * P.nS + b];
 }
@@ -1093,7 +1099,7 @@ __device__ __forceinline__ void thread_chunk(const DevProb &P, const SearchArgs 
             if (POLICY == 1 && P.A == 1 && c.tub < wb->lmin) go_node = false;
         }
         const int cnt = go_node ? (int)sb_at(P, S, j, bj).cnt : 0;
-        const OptRec *list = S.rec + ((size_t)j * P.nS + bj) * P.O;
+        const OptRec *list = list_of(P, S, j, bj);
 #ifdef CAMELOT_FTRACE
         if (tme) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt[1]));
 #endif
@@ -1105,8 +1111,8 @@ __device__ __forceinline__ void thread_chunk(const DevProb &P, const SearchArgs 
             const bool valid = t < my_iters;
             OptRec r;
             {
-                const uint4 *src = reinterpret_cast<const uint4 *>(list + (valid ? k : 0));
-                const uint4 a = __ldg(src), b = __ldg(src + 1);
+                const OptRec *src = list + (valid ? k : 0);
+                const uint4 a = rec_chunk(src, 0), b = rec_chunk(src, 1);
                 r.code = a.x;
                 r.NP = a.y;
                 r.N = a.z;
@@ -1232,8 +1238,8 @@ __device__ __forceinline__ void thread_chunk(const DevProb &P, const SearchArgs 
                 smask &= smask - 1u;
                 OptRec r;
                 {
-                    const uint4 *src = reinterpret_cast<const uint4 *>(list + k);
-                    const uint4 a = __ldg(src), b = __ldg(src + 1);
+                    const OptRec *src = list + k;
+                    const uint4 a = rec_chunk(src, 0), b = rec_chunk(src, 1);
                     r.code = a.x;
                     r.NP = a.y;
                     r.N = a.z;
@@ -1434,7 +1440,7 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
             while (true) {
                 const Node<CM> &nd = stack[j];
                 const int bj = nd.b[P.app[j]];
-                const OptRec *list = S.rec + ((size_t)j * P.nS + bj) * P.O;
+                const OptRec *list = list_of(P, S, j, bj);
                 if (reload) {
                     reload = false;
                     load_ctx<CM, NS>(P, S, nd, j, c);
@@ -1503,9 +1509,9 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
                 OptRec r;
                 uint4 cold = make_uint4(0u, 0u, 0u, 0u);   // p, W, A*s, MEM (emission only)
                 {
-                    const uint4 *src = reinterpret_cast<const uint4 *>(list + (valid ? opt : base));
-                    const uint4 a = __ldg(src), b = __ldg(src + 1);
-                    if (!leaf) cold = __ldg(src + 2);
+                    const OptRec *src = list + (valid ? opt : base);
+                    const uint4 a = rec_chunk(src, 0), b = rec_chunk(src, 1);
+                    if (!leaf) cold = rec_chunk(src, 2);
                     r.code = a.x;
                     r.NP = a.y;
                     r.N = a.z;

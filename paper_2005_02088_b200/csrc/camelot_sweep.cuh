@@ -66,29 +66,33 @@ __device__ __forceinline__ void sw_init(const DevProb &P, SwState<CM, NS> &s) {
 // Deploy stage i with N replicas of quota p:
 // pass 1 = the first GPU in (rm, rq, id) order that holds all N, pass 2 = greedy
 // min(canHold, remaining) in the same order.  Returns false if it does not fit.
+// Division-free: floor(rq / p) = (rq * pmul) >> 16 with pmul = ceil(2^16 / p) (rq <= 127),
+// and the memory capacity counts k = 1..N with W + k As <= rm (N <= 4 in the sweep).
+// The deployment order packs (rm, rq, id) into 32 bits (rm < 2^21, rq < 2^7, id < 2^4).
 template <int CM, int NS>
-__device__ __forceinline__ bool sw_place(const DevProb &P, SwState<CM, NS> &s, int i, int N, int p,
+__device__ __forceinline__ bool sw_place(const DevProb &P, SwState<CM, NS> &s, int i, int N, int p, uint32_t pmul,
                                          uint32_t W, uint32_t As, float bw) {
     const bool cap = !(P.flags & F_NO_BW_CAP);
     int c[CM];
-    unsigned long long key[CM];
+    uint32_t key[CM];
 #pragma unroll
     for (int g = 0; g < CM; ++g) {
         int k = 0;
         if (g < P.C) {
-            k = min(N, s.rq[g] / p);
+            k = min(N, (int)(((uint32_t)s.rq[g] * pmul) >> 16));
             k = min(k, P.I - s.cnt[g]);
-            if (s.rm[g] < W) k = 0;
-            else if (As > 0u) k = min(k, (int)min((uint32_t)N, (s.rm[g] - W) / As));
+            int km = 0;   // memory: k' <= k with W + k' As <= rm
+#pragma unroll
+            for (int t = 1; t <= 4; ++t) km += (t <= k) & (W + (uint32_t)t * As <= s.rm[g]);
+            k = km;
             if (cap)
                 while (k > 0 && __fadd_rn(s.dem[g], __fmul_rn((float)k, bw)) > P.BW) --k;
-            k = max(k, 0);
         }
         c[g] = k;
-        key[g] = ((unsigned long long)s.rm[g] << 12) | ((unsigned long long)s.rq[g] << 4) | (unsigned)g;
+        key[g] = (s.rm[g] << 11) | ((uint32_t)s.rq[g] << 4) | (uint32_t)g;
     }
     int gs = -1;
-    unsigned long long best = ~0ull;
+    uint32_t best = 0xffffffffu;
 #pragma unroll
     for (int g = 0; g < CM; ++g)
         if (c[g] == N && key[g] < best) {
@@ -108,8 +112,7 @@ __device__ __forceinline__ bool sw_place(const DevProb &P, SwState<CM, NS> &s, i
         for (int g = 0; g < CM; ++g) {
             int pre = 0;   // capacity of the GPUs before g in deployment order
 #pragma unroll
-            for (int h = 0; h < CM; ++h)
-                if (key[h] < key[g]) pre += c[h];
+            for (int h = 0; h < CM; ++h) pre += (key[h] < key[g]) ? c[h] : 0;
             kk[g] = min(c[g], max(0, N - pre));
         }
     }
@@ -229,11 +232,24 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
     const int jl = n - 1;                     // leaf stage
     const bool cont = !(P.flags & F_NO_CONTENTION);
     const bool cap = !(P.flags & F_NO_BW_CAP);
+    // the leaf stage's predictor rows of every batch (nS x nQ float4, contiguous in the
+    // [n][nS][nQ] table) -> shared memory with the TMA engine (one bulk copy per CTA)
+    extern __shared__ __align__(16) float4 tabL_s[];
+    __shared__ unsigned long long tbar;
+    const bool staged = A.tabL_bytes > 0;
+    if (staged && tid == 0) {
+        mbar_init(&tbar, 1);
+        fence_proxy_async();
+        mbar_arrive_expect_tx(&tbar, A.tabL_bytes);
+        bulk_g2s(tabL_s, P.tab + (size_t)jl * P.nS * nQ, A.tabL_bytes, &tbar);
+    }
     for (int t = tid; t < nQ; t += blockDim.x) {
         const uint32_t p = (uint32_t)P.Q[t];
         qpm_s[t] = p | (((65536u + p - 1u) / p) << 7);
     }
-    __syncthreads();
+    __syncthreads();   // (also publishes the initialised barrier)
+    if (staged) mbar_wait(&tbar, 0);
+    const float4 *tabLall = staged ? tabL_s : P.tab + (size_t)jl * P.nS * nQ;
     unsigned long long bk = A.inc[0].key, bx = A.inc[0].x;
     unsigned long long n_sc = 0, n_fe = 0;
     unsigned viol = 0;
@@ -294,7 +310,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
                 const int th = o[i] % nQ, N = o[i] / nQ + 1;
                 const float4 e = __ldg(&P.tab[((size_t)i * P.nS + b) * nQ + th]);
                 const uint32_t As = P.Am[i] * (uint32_t)P.S[b];
-                ok = sw_place<CM, NS>(P, st, i, N, (int)(qpm_s[th] & 127u), P.W[i], As, e.z);
+                ok = sw_place<CM, NS>(P, st, i, N, (int)(qpm_s[th] & 127u), qpm_s[th] >> 7, P.W[i], As, e.z);
                 dur[i] = e.x;
                 bwv[i] = e.z;
                 ntv[i] = __fmul_rn((float)N, e.y);
@@ -329,7 +345,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
             const int th = op % nQ, N = op / nQ + 1;
             const float4 e = __ldg(&P.tab[((size_t)i * P.nS + b) * nQ + th]);
             const uint32_t As = P.Am[i] * (uint32_t)P.S[b];
-            act = sw_place<CM, NS>(P, st, i, N, (int)(qpm_s[th] & 127u), P.W[i], As, e.z);
+            act = sw_place<CM, NS>(P, st, i, N, (int)(qpm_s[th] & 127u), qpm_s[th] >> 7, P.W[i], As, e.z);
             dur[i] = e.x;
             bwv[i] = e.z;
             ntv[i] = __fmul_rn((float)N, e.y);
@@ -359,22 +375,20 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
             hb[g] = __int_as_float(0xff800000);   // -inf: nothing fits (padding GPUs)
             if (g < P.C) {
                 k = min(Rmax, P.I - st.cnt[g]);
-                if (st.rm[g] < WL) k = 0;
-                else if (AsL > 0u) k = min(k, (int)min((uint32_t)Rmax, (st.rm[g] - WL) / AsL));
-                k = max(k, 0);
+                int km = 0;   // memory: k' <= k with WL + k' AsL <= rm (Rmax <= 4; no division)
+#pragma unroll
+                for (int t = 1; t <= 4; ++t) km += (t <= k) & (WL + (uint32_t)t * AsL <= st.rm[g]);
+                k = km;
                 if (st.cnt[g] == 0) E |= 1u << g;
                 hb[g] = cap ? bw_threshold(st.dem[g], P.BW) : __int_as_float(0x7f800000);
             }
             kim[g] = k;
             int r = 0;
-            if (g < P.C) {
+            if (g < P.C) {   // rank in the (rm, rq, id) order: packed 32-bit keys (see sw_place)
+                const uint32_t kg = (st.rm[g] << 11) | ((uint32_t)st.rq[g] << 4) | (uint32_t)g;
 #pragma unroll
                 for (int h = 0; h < CM; ++h)
-                    if (h < P.C && h != g) {
-                        const bool lt = st.rm[h] < st.rm[g] ||
-                                        (st.rm[h] == st.rm[g] && (st.rq[h] < st.rq[g] || (st.rq[h] == st.rq[g] && h < g)));
-                        r += lt;
-                    }
+                    if (h < P.C) r += ((st.rm[h] << 11) | ((uint32_t)st.rq[h] << 4) | (uint32_t)h) < kg;
             } else {
                 r = g;
             }
@@ -391,7 +405,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
                 const float k = sw_kappa(st.dm[i], bwv[i], cont ? P.gamma[i] : 0.0f, P.invBW);
                 ptub = fminf(ptub, k == 1.0f ? ntv[i] : __fdiv_rn(ntv[i], k));
             }
-        const float4 *tabL = P.tab + ((size_t)jl * P.nS + bL) * nQ;
+        const float4 *tabL = tabLall + (size_t)bL * nQ;
         const float qos0 = P.qos[0], qos1 = TWO ? P.qos[1] : 0.0f;
         const int f1 = TWO ? P.first_of_app[1] : n;   // first stage of application 2
         float gam[NS];
@@ -416,7 +430,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
         // within the ~6 KB L0 instruction cache.
         for (int ts = 0; ts < nQs; ++ts) {
             const int th = nQ - 1 - qs * (nQs - 1 - ts);
-            const float4 e = __ldg(&tabL[th]);
+            const float4 e = tabL[th];
             const uint32_t qp = qpm_s[th];
             const uint32_t pmul = qp >> 7;
             const float bw = e.z;
@@ -607,6 +621,8 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
         }
         A.result[0].key = k2;
         A.result[0].x = x2;
+        trace_value(A.hdr, 202, k2);   // the sweep's optimum in the phase trace
+        trace_value(A.hdr, 203, x2);
         unsigned long long packed = ~0ull;
         if (k2 != 0xFFFFFFFFull) {
             // chunk id = 64 depth-d0 items (NO_FILTER: item = x / O^(n-d0)), as the tree search

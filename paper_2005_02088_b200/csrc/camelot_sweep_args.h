@@ -5,6 +5,8 @@
 
 namespace cam {
 
+constexpr unsigned SWEEP_TABL_MAX = 20 * 1024;   // staged leaf-stage rows (static smem ~25 KB: 2 CTAs/SM)
+
 struct SweepArgs {
     int policy;                       // 0 max-load, 1 min-resource (one load level)
     int rank, world, d0;              // chunk ownership: chunk = (x / O^(n-d0)) / 64
@@ -25,6 +27,7 @@ struct SweepArgs {
     DevHeader *hdr;
     Slot *result;                     // exact local best
     long long *keys;                  // packed key (NCCL transport)
+    unsigned tabL_bytes;              // leaf-stage table rows staged in shared memory (0: read global)
 };
 
 }  // namespace cam

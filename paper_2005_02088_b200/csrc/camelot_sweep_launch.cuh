@@ -25,7 +25,8 @@ cudaError_t launch_ns(const DevProb &P, const SweepArgs &A, int dev, cudaStream_
         int &gg = g_grid[dev & 63][NS - 1][POL][TWO][COMM];
         if (!gg) {
             int per = 0, nsm = 0;
-            cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, sweep_kernel<8, NS, POL, TWO, COMM>, SWEEP_THREADS, 0);
+            cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, sweep_kernel<8, NS, POL, TWO, COMM>,
+                                                                          SWEEP_THREADS, SWEEP_TABL_MAX);
             if (e != cudaSuccess) return e;
             e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
             if (e != cudaSuccess) return e;
@@ -33,7 +34,7 @@ cudaError_t launch_ns(const DevProb &P, const SweepArgs &A, int dev, cudaStream_
         }
         grid = gg;
     }
-    sweep_kernel<8, NS, POL, TWO, COMM><<<grid, SWEEP_THREADS, 0, st>>>(P, A);
+    sweep_kernel<8, NS, POL, TWO, COMM><<<grid, SWEEP_THREADS, A.tabL_bytes, st>>>(P, A);
     return cudaGetLastError();
 }
 

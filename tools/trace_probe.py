@@ -1,6 +1,7 @@
 """Phase trace of the C4 plan calls (development aid): per search-level launch,
 the time between grid barriers.   python tools/trace_probe.py [config] [reps]"""
 import os
+import struct
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -17,7 +18,15 @@ def show(tag, tr, st):
     line, prev = [], None
     t0s = [0]
     for t, ns in tr:
-        if t == 0:
+        if t in (200, 201, 202, 203):
+            if t in (200, 202):
+                kk = ns & 0xFFFFFFFF
+                T = struct.unpack("<f", struct.pack("<I", (0xFFFFFFFF - kk) & 0xFFFFFFFF))[0]
+                line.append(f"{'sweep ' if t == 202 else ''}key={kk:#x} (T={T:.6g} | u={kk >> 24},U={kk & 0xFFFFFF})")
+            else:
+                line.append(f"x={ns}")
+            continue
+        elif t == 0:
             if line:
                 print("   " + " ".join(line))
             line = []
