@@ -710,27 +710,35 @@ __host__ __device__ constexpr size_t level_fixed_bytes() {
            16 * 16;
 }
 
+// reset a level's header state (the cumulative counters stay); one whole CTA
+__device__ __forceinline__ void level_reset(DevHeader *hdr) {
+    unsigned *h = reinterpret_cast<unsigned *>(hdr);
+    for (int w = threadIdx.x; w < (int)(offsetof(DevHeader, cum_scored) / 4); w += blockDim.x) h[w] = 0u;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        hdr->best_obj = 0xFFFFFFFFu;
+        hdr->best_packed = ~0ull;
+    }
+}
+
 // One search level (incumbent cascade level or main pass) executed by the whole
 // cooperative grid; levels are chained inside one launch (search_level_kernel).
+// first: reset the header (block 0) behind a grid barrier; later levels find it reset
+// by the previous level's last CTA.  last: no grid barrier at the end (kernel exit).
 template <int CM, int NS, int POLICY>
 __device__ __forceinline__ void level_body(const DevProb &P, const LevelArgs &LA, unsigned char *smem_raw,
-                                           cooperative_groups::grid_group &grid, unsigned &stage_phase) {
+                                           cooperative_groups::grid_group &grid, unsigned &stage_phase, bool first,
+                                           bool last) {
     SearchArgs S = LA.S;
     DevHeader *hdr = S.hdr;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const bool tr = blockIdx.x == 0 && threadIdx.x == 0;
     if (tr) trace_mark(hdr, 0);
-    // phase 0: reset this level's header state (the cumulative counters stay)
-    if (blockIdx.x == 0) {
-        unsigned *h = reinterpret_cast<unsigned *>(hdr);
-        for (int w = threadIdx.x; w < (int)(offsetof(DevHeader, cum_scored) / 4); w += blockDim.x) h[w] = 0u;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            hdr->best_obj = 0xFFFFFFFFu;
-            hdr->best_packed = ~0ull;
-        }
+    // phase 0 (first level only): reset the header state
+    if (first) {
+        if (blockIdx.x == 0) level_reset(hdr);
+        grid.sync();
     }
-    grid.sync();
     if (tr) trace_mark(hdr, 1);
     // phase 1: option filter (one CTA per batch) and slot reset
     for (int b = blockIdx.x; b < P.nS; b += gridDim.x) {
@@ -820,6 +828,7 @@ __device__ __forceinline__ void level_body(const DevProb &P, const LevelArgs &LA
         S.head = &hdr->head[j];
         S.grab = 1;
         pass_body<CM, NS, POLICY>(P, S, stack, ctl, wb, lane, cn);
+        if (j == n - 1) break;   // the last pass ends at the CTA merge below (no grid barrier)
 #ifdef CAMELOT_FTRACE
         if (lane == 0) {
             unsigned long long t;
@@ -844,24 +853,38 @@ __device__ __forceinline__ void level_body(const DevProb &P, const LevelArgs &LA
         }
     }
     cta_finish<CM>(S, wb_all, lane, wid, cn);
-    grid.sync();
-    if (tr) trace_mark(hdr, 32);
-    // phase 4: reduction of the CTA slots (block 0)
-    if (blockIdx.x == 0) {
+    // phase 4: the LAST CTA to finish reduces the CTA slots (exact local best, packed
+    // key, next incumbent) and resets the header for the next level; one grid barrier
+    // then separates the levels
+    __shared__ int is_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) is_last = atomicAdd(&hdr->done_ctas, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (is_last) {
+        __threadfence();
+        if (threadIdx.x == 0) {
+            trace_mark(hdr, 16 + n - 1);
+            trace_mark(hdr, 32);
+        }
         unsigned long long *sk = reinterpret_cast<unsigned long long *>(smem_raw);
         reduce_slots_block(P, S.slots, gridDim.x, S.nlev, S.result, S.keys, S.inc_out, S.sb, S.rec, S.item_off, S.d0,
                            S.chunk_items, -1, sk, sk + SEARCH_THREADS);
-        if (tr) {   // the level's optimum (objective key, canonical index) in the phase trace
+        if (threadIdx.x == 0) {   // the level's optimum (objective key, canonical index) in the phase trace
             trace_value(hdr, 200, S.result[0].key);
             trace_value(hdr, 201, S.result[0].x);
         }
+        __syncthreads();
+        if (!last) level_reset(hdr);   // (also zeroes done_ctas)
+        else if (threadIdx.x == 0) hdr->done_ctas = 0;
     }
+    if (!last) grid.sync();
 }
 
 
 // All pruned levels of one search in ONE cooperative launch: level l+1 reads the
-// incumbent level l's reduction (block 0) wrote before level l+1's first grid
-// barrier, so no extra barrier or launch is needed between levels.
+// incumbent that level l's last CTA wrote (with the header reset) before the grid
+// barrier that ends level l, so no extra barrier or launch is needed between levels.
 constexpr int MAX_LEVELS = 4;
 struct LevelSet {
     int count;
@@ -877,8 +900,8 @@ search_level_kernel(const DevProb P, const LevelSet LS) {
     if (threadIdx.x == 0) mbar_init(reinterpret_cast<unsigned long long *>(smem_raw + level_fixed_bytes<CM>()), 1);
     __syncthreads();
     for (int l = 0; l < LS.count; ++l) {
-        level_body<CM, NS, POLICY>(P, LS.L[l], smem_raw, grid, stage_phase);
-        __syncthreads();   // block 0's reduction used shared memory
+        level_body<CM, NS, POLICY>(P, LS.L[l], smem_raw, grid, stage_phase, l == 0, l == LS.count - 1);
+        __syncthreads();   // the last CTA's reduction used shared memory
     }
 }
 }  // namespace cam
