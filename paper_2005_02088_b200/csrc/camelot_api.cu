@@ -707,6 +707,7 @@ int search_pass(const Ctx &X, int dev, int policy, int nlev, bool prune, int str
     S.inc_out = inc_out;
     if (coop) {
         LevelArgs LA;
+        memset(&LA, 0, sizeof(LA));
         LA.S = S;
         LA.F = F;
         LA.buf0 = ws + X.L.front0;

@@ -174,6 +174,13 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned pari
             : "memory");
     }
 }
+// 4-byte asynchronous global -> shared copies (cp.async, L1-cached): the parent-node
+// prefetch of the search passes; wait_all + a warp barrier before the data is read
+__device__ __forceinline__ void cp_async4(void *dst_smem, const void *src_gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst_smem)), "l"(src_gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 // generic-proxy writes (this or other threads, ordered by a barrier) before async-proxy
 // accesses of the same memory (the bulk copy reads global records written by the filter,
 // and overwrites shared memory read by the previous level)

@@ -389,20 +389,24 @@ CAM_GLOBAL void resolve_kernel(const DevProb P, const FinalArgs F) {
 }
 
 // winner index -> full plan (device), with the search counters
-// One block per load level: thread 0 scores the winner (score_digits, scratch and
-// result in shared memory), then the block fills the plan in shared memory and
-// copies it out word by word (the serial part stays short: no local-memory plan).
 constexpr int PLAN_THREADS = 64;
-CAM_GLOBAL void __launch_bounds__(PLAN_THREADS) plan_kernel(const DevProb P, int policy, int nlev, const Slot *winner,
-                                                            const float *lam, const DevHeader *hdr, camelot_plan *out) {
-    const int k = blockIdx.x, tid = threadIdx.x;
-    if (k >= nlev) return;
-    __shared__ __align__(16) camelot_plan pl;
-    __shared__ FullScore s;
-    __shared__ ScoreScratch scr;
-    __shared__ int beta[AMAX], rho[NMAX], theta[NMAX];
-    __shared__ int eq2y;
-    const Slot w = winner[k];
+struct PlanScratch {
+    camelot_plan pl;
+    FullScore s;
+    ScoreScratch scr;
+    int beta[AMAX], rho[NMAX], theta[NMAX];
+    int eq2y;
+};
+// The full plan of winner w, scored by ONE whole CTA (>= 32 threads; every thread
+// calls): thread 0 decodes, warp 0 places in parallel (place_warp; score_digits only
+// for PAPER_GLOBAL or a failed placement), the CTA fills the plan in shared memory and
+// copies it out.  lamk: this level's loads [A] (min-resource); hdr: the search's counters.
+CAM_DEVFN void plan_block(const DevProb &P, int policy, const Slot w, const float *lamk, const DevHeader *hdr,
+                          camelot_plan *out, PlanScratch &ps) {
+    const int tid = threadIdx.x;
+    camelot_plan &pl = ps.pl;
+    FullScore &s = ps.s;
+    int *beta = ps.beta, *rho = ps.rho, *theta = ps.theta;
     {
         uint32_t *pw = reinterpret_cast<uint32_t *>(&pl);
         for (int q = tid; q < (int)(sizeof(camelot_plan) / 4); q += blockDim.x) pw[q] = 0u;
@@ -422,8 +426,6 @@ CAM_GLOBAL void __launch_bounds__(PLAN_THREADS) plan_kernel(const DevProb P, int
         }
     }
     __syncthreads();
-    // the winner's placement: warp 0 in parallel (one lane per GPU); the serial
-    // score_digits only for PAPER_GLOBAL problems or a placement failure
     if (w.x != ~0ull && tid < 32) {
         bool placed = false;
         if (!(P.flags & F_PAPER_GLOBAL)) {
@@ -447,24 +449,22 @@ CAM_GLOBAL void __launch_bounds__(PLAN_THREADS) plan_kernel(const DevProb P, int
                 score_finish(P, beta, rho, dur, thr, kmax, hm, 0u, u, s);
             }
         }
-        if (!placed && tid == 0) score_digits(P, beta, rho, theta, s, &scr);
+        if (!placed && tid == 0) score_digits(P, beta, rho, theta, s, &ps.scr);
     }
     __syncthreads();
-    if (tid == 0) {
-        if (w.x != ~0ull) {
-            eq2y = policy == 1 ? eq2_gpus(P, beta, lam + k * P.A) : 0;
-            pl.index = w.x;
-            pl.status = CAMELOT_OK;
-            pl.quota_used = s.U;
-            pl.gpus_used = s.u;
-            if (policy == 1) {
-                pl.eq2_gpus = eq2y;
-                pl.violations = level_verdict(P, s, lam + k * P.A, eq2y);
-                pl.objective = (float)s.U;
-            } else {
-                pl.violations = s.verdict;
-                pl.objective = s.T;
-            }
+    if (tid == 0 && w.x != ~0ull) {
+        ps.eq2y = policy == 1 ? eq2_gpus(P, beta, lamk) : 0;
+        pl.index = w.x;
+        pl.status = CAMELOT_OK;
+        pl.quota_used = s.U;
+        pl.gpus_used = s.u;
+        if (policy == 1) {
+            pl.eq2_gpus = ps.eq2y;
+            pl.violations = level_verdict(P, s, lamk, ps.eq2y);
+            pl.objective = (float)s.U;
+        } else {
+            pl.violations = s.verdict;
+            pl.objective = s.T;
         }
     }
     __syncthreads();
@@ -490,8 +490,17 @@ CAM_GLOBAL void __launch_bounds__(PLAN_THREADS) plan_kernel(const DevProb P, int
     }
     __syncthreads();
     const uint32_t *src = reinterpret_cast<const uint32_t *>(&pl);
-    uint32_t *dst = reinterpret_cast<uint32_t *>(out + k);
+    uint32_t *dst = reinterpret_cast<uint32_t *>(out);
     for (int q = tid; q < (int)(sizeof(camelot_plan) / 4); q += blockDim.x) dst[q] = src[q];
+}
+
+// One block per load level: plan_block of that level's winner.
+CAM_GLOBAL void __launch_bounds__(PLAN_THREADS) plan_kernel(const DevProb P, int policy, int nlev, const Slot *winner,
+                                                            const float *lam, const DevHeader *hdr, camelot_plan *out) {
+    const int k = blockIdx.x;
+    if (k >= nlev) return;
+    __shared__ PlanScratch ps;
+    plan_block(P, policy, winner[k], lam + k * P.A, hdr, out + k, ps);
 }
 
 // The low load of camelot_plan_max_then_min (low load = a fraction

@@ -1334,14 +1334,46 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
     const unsigned grab = tmode ? 32u / (unsigned)G : screen ? 8u : (unsigned)S.grab;
     const unsigned long long nw = nwarps * grab;
     unsigned long long e0 = ((unsigned long long)blockIdx.x * SEARCH_WARPS + (threadIdx.x >> 5)) * grab;
+    // Parent prefetch (warp mode on a frontier, jtop >= 1 so stack[0] is free): the next
+    // parent's node is copied asynchronously (cp.async) into stack[0] while the current
+    // one is searched, and the next work item is popped one item ahead, so neither the
+    // queue atomic nor the node copy sits on the warp's critical path.
+    const bool pipe = have_in && jtop >= 1 && !tmode;
+    unsigned long long pf_e = ~0ull;    // parent node in stack[0] (copy issued)
+    unsigned long long top_e = ~0ull;   // parent node in stack[jtop]
+    unsigned long long nx_raw = 0;      // lane 0: the popped-ahead item (nx_state == 1)
+    int nx_state = 0;                   // 0 none, 1 popped (lane 0 holds it), 2 known (nx_e)
+    unsigned long long nx_e = 0;
+    auto prefetch = [&](unsigned long long e) {
+        uint32_t *d = reinterpret_cast<uint32_t *>(&stack[0]);
+        for (int w = lane; w < Frontier<CM>::WORDS; w += 32) cp_async4(d + w, in.base + (size_t)w * in.cap + e);
+        cp_async_commit();
+        pf_e = e;
+    };
+    auto parent_of = [&](unsigned long long item) { return split == 1 ? item : item / (unsigned)split; };
     bool first = true;
     while (true) {
         if (!first) {
-            if (nw >= items) break;   // every item was assigned statically: no queue round trip
-            if (lane == 0) e0 = nw + atomicAdd(S.head, (unsigned long long)grab);
-            e0 = __shfl_sync(0xffffffffu, e0, 0);
+            if (nx_state == 1) {
+                nx_e = __shfl_sync(0xffffffffu, nx_raw, 0);
+                nx_state = 2;
+            }
+            if (nx_state == 2) {
+                e0 = nx_e;
+                nx_state = 0;
+            } else {
+                if (nw >= items) break;   // every item was assigned statically: no queue round trip
+                if (lane == 0) e0 = nw + atomicAdd(S.head, (unsigned long long)grab);
+                e0 = __shfl_sync(0xffffffffu, e0, 0);
+            }
         }
         first = false;
+        // pop the next item now (its value is read later) -- only when items are plentiful:
+        // holding an item ahead starves idle warps in passes with few items per warp
+        if (pipe && e0 < items && nw < items && items >= 8ull * nwarps) {
+            if (lane == 0) nx_raw = nw + atomicAdd(S.head, (unsigned long long)grab);
+            nx_state = 1;
+        }
 #ifdef CAMELOT_FTRACE
         ++dbg_item;
 #endif
@@ -1417,6 +1449,34 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
                 build_root<CM>(P, (int)e, stack[0], lane);
                 if (lane < NMAX) stack[0].kidx[lane] = 0;
                 __syncwarp();
+            } else if (pipe) {
+                if (top_e != e) {   // (consecutive blocks of one parent reuse stack[jtop])
+                    if (pf_e != e) prefetch(e);
+                    cp_async_wait_all();
+                    __syncwarp();
+                    const uint32_t *src = reinterpret_cast<const uint32_t *>(&stack[0]);
+                    uint32_t *dst = reinterpret_cast<uint32_t *>(&stack[jtop]);
+                    for (int w = lane; w < Frontier<CM>::WORDS; w += 32) dst[w] = src[w];
+                    __syncwarp();
+                    top_e = e;
+                    pf_e = ~0ull;
+                }
+                // prefetch the next parent: the next live one of this item, else the
+                // first of the popped-ahead item
+                unsigned long long e2 = ~0ull;
+                for (unsigned long long it2 = it + 1; it2 < e1; ++it2)
+                    if ((live >> (unsigned)(it2 - e0)) & 1u) {
+                        e2 = parent_of(it2);
+                        break;
+                    }
+                if (e2 == ~0ull && nx_state != 0) {
+                    if (nx_state == 1) {
+                        nx_e = __shfl_sync(0xffffffffu, nx_raw, 0);
+                        nx_state = 2;
+                    }
+                    if (nx_e < items) e2 = parent_of(nx_e);
+                }
+                if (e2 != ~0ull && e2 != top_e && e2 != pf_e) prefetch(e2);
             } else {
                 copy_node<CM>(stack[jtop], in, e, lane);
             }
@@ -1606,6 +1666,10 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
             }
             PTM(6);
         }
+    }
+    if (pipe) {   // no copy may still be in flight into stack[0] when the pass ends
+        cp_async_wait_all();
+        __syncwarp();
     }
     PTM(7);
 #ifdef CAMELOT_FTRACE
