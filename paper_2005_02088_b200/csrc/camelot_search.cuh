@@ -869,11 +869,10 @@ __device__ __forceinline__ void emit_child(const DevProb &P, const ND &nd, const
         As2 = P.Am[i2] * (uint32_t)P.S[nd.b[P.app[i2]]];
     }
     // deployment order for the next stage: (remaining MiB, remaining quota, id) packed
-    // into one orderable 64-bit key (rq <= 127, id < 16)
-    unsigned long long okey[CM];
+    // into one orderable 32-bit key (rm < 2^21 as FM < 2^21, 0 <= rq <= 127, id < 16)
+    uint32_t okey[CM];
 #pragma unroll
-    for (int q = 0; q < CM; ++q)
-        okey[q] = ((unsigned long long)rm[q] << 12) | ((unsigned long long)(uint32_t)rq[q] << 4) | (unsigned)g[q];
+    for (int q = 0; q < CM; ++q) okey[q] = (rm[q] << 11) | ((uint32_t)rq[q] << 4) | (uint32_t)g[q];
 #pragma unroll
     for (int q = 0; q < CM; ++q) {
         if (q < P.C) {
@@ -883,13 +882,14 @@ __device__ __forceinline__ void emit_child(const DevProb &P, const ND &nd, const
                 if (h < P.C && h != q) rank += okey[h] < okey[q];
             int kim = 0;
             if (more) {
-                // largest k <= min(Rmax, I - cnt) with W2 + k As2 <= rm (binary search, no division)
+                // largest k <= min(Rmax, I - cnt) with W2 + k As2 <= rm (binary search, no
+                // division; 32-bit: W + Rmax A s < 2^31 is validated and t <= lim <= Rmax)
                 const int lim = min(P.Rmax, P.I - cnt[q]);
                 if (lim > 0 && rm[q] >= W2) {
 #pragma unroll
                     for (int step = 16; step >= 1; step >>= 1) {
                         const int t = kim + step;
-                        if (t <= lim && (unsigned long long)W2 + (unsigned long long)t * As2 <= rm[q]) kim = t;
+                        if (t <= lim && W2 + (uint32_t)t * As2 <= rm[q]) kim = t;
                     }
                 }
             }

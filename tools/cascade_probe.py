@@ -14,7 +14,7 @@ cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 p = G.config_problems(cfg)[0]
 s = api.Session(p, n_loads=1)
 ref = None
-for spec in ["", "50,20,5", "50,20", "50,10", "50,25,10,5", "50,10,5", "34,10,3", "20,5", "25,5", "50,20,10,5", "50,5"]:
+for spec in (sys.argv[2].split(";") if len(sys.argv) > 2 else ["", "50,20,5", "50,20", "50,10", "50,25,10,5", "50,10,5", "34,10,3", "20,5", "25,5", "50,20,10,5", "50,5"]):
     if spec:
         os.environ["CAMELOT_COARSE"] = spec
     else:
