@@ -1305,7 +1305,7 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
     int dbg_item = 0;
     const bool dbg_me = blockIdx.x == 0 && threadIdx.x == 0;
 #define PTM(k) \
-    if (dbg_me && dbg_item == 1 && dbg_t[k] == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(dbg_t[k]));
+    if (dbg_me && dbg_item <= 1 && dbg_t[k] == 0) dbg_t[k] = (unsigned long long)clock64();   /* SM cycles */
 #else
 #define PTM(k)
 #endif

@@ -366,7 +366,8 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
                 te[i] = (i + 1 < jl && st.hm[i] == st.hm[i + 1] && __popc(st.hm[i]) == 1) ? P.ipc_ms : tx;
             }
         }
-        int kim[CM], sh[CM];
+        int kim[CM];
+        uint32_t bsh[CM];   // 1 << (4 * rank): the GPU's nibble in the thermometer code
         float hb[CM];      // bandwidth threshold: fits(k) <=> fl(k bw) <= hb
         uint32_t perm = 0u, E = 0u;
 #pragma unroll
@@ -392,7 +393,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
             } else {
                 r = g;
             }
-            sh[g] = 4 * r;
+            bsh[g] = 1u << (4 * r);
             perm |= (uint32_t)g << (4 * r);
             dem_s[g][tid] = st.dem[g];
             rqc_s[g][tid] = (uint32_t)st.rq[g] | ((uint32_t)st.cnt[g] << 8);
@@ -445,7 +446,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
                 const uint32_t nf = (__float_as_uint(__fsub_rn(h, bw)) >> 31) + (__float_as_uint(__fsub_rn(h, nb2)) >> 31) +
                                     (__float_as_uint(__fsub_rn(h, nb3)) >> 31) + (__float_as_uint(__fsub_rn(h, nb4)) >> 31);
                 const int c = min(min(kim[g], (int)(((uint32_t)st.rq[g] * pmul) >> 16)), 4 - (int)nf);
-                M |= (0xFu >> (4 - c)) << sh[g];
+                M += (bsh[g] << c) - bsh[g];   // c ones in the GPU's nibble (c <= 4)
             }
             // deployment succeeds iff the total capacity holds N (pass 1 or pass 2)
             const int sumc = __popc(M);
@@ -468,7 +469,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
 #pragma unroll 1
             for (int N = 1; N <= nok; ++N) {
                 const int code = (N - 1) * nQ + th;
-                if ((unsigned)(code - clo) >= span) continue;
+                if (!full && (unsigned)(code - clo) >= span) continue;
                 // receiving GPUs in deployment order: pass 1 = the first with c >= N (k = N);
                 // pass 2 = greedy k = min(c, remaining) over those with c >= 1
                 const uint32_t mN = (M >> (N - 1)) & 0x11111111u;

@@ -38,8 +38,8 @@ def show(tag, tr, st):
         elif t >= 120:
             line.append(f"tc{t - 120}={ns / 1e3 if t < 123 else ns:.1f}")
             continue
-        elif t >= 112:
-            line.append(f"w{t - 112}={ns/1e3:.1f}")
+        elif t >= 112:   # item 1 of warp 0, block 0: SM cycles since the pass start -> us at 1.965 GHz
+            line.append(f"w{t - 112}={ns / 1965.0:.2f}")
             continue
         elif t >= 64:
             line.append(f"{['par', 'bat', 'maxb'][(t - 64) // 16]}{t % 16}={ns}")
