@@ -1224,15 +1224,19 @@ __device__ __forceinline__ void thread_chunk(const DevProb &P, const SearchArgs 
         __syncwarp();
         if (tme) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt[2]));
 #endif
-        // emission rounds: every lane emits its next survivor in the same round, with
-        // warp-aggregated consecutive slots (coalesced structure-of-arrays stores;
-        // capacity checked by the caller)
+        // emission rounds: every lane emits its next survivor in the same round, into
+        // consecutive slots (coalesced structure-of-arrays stores); the slots of all
+        // rounds come from ONE warp-aggregated atomic (capacity checked by the caller)
+        unsigned total = __popc(smask);
+        for (int off = 16; off; off >>= 1) total += __shfl_xor_sync(0xffffffffu, total, off);
+        unsigned long long fbase = 0;
+        if (lane == 0 && total) fbase = atomicAdd(S.out_tail, (unsigned long long)total);
+        fbase = __shfl_sync(0xffffffffu, fbase, 0);
         while (true) {
             const unsigned m = __ballot_sync(0xffffffffu, smask != 0u);
             if (!m) break;
-            unsigned long long fbase = 0;
-            if (lane == 0) fbase = atomicAdd(S.out_tail, (unsigned long long)__popc(m));
-            fbase = __shfl_sync(0xffffffffu, fbase, 0);
+            const unsigned long long rbase = fbase;
+            fbase += __popc(m);
             if (smask) {
                 const int k = sub + (__ffs(smask) - 1) * G;
                 smask &= smask - 1u;
@@ -1250,7 +1254,7 @@ __device__ __forceinline__ void thread_chunk(const DevProb &P, const SearchArgs 
                     r.dur = __uint_as_float(b.w);
                 }
                 const OptRec &full = list[k];
-                emit_child<CM, NS>(P, nd, c, j, r, full.p, full.W, full.As, k, outf, fbase + __popc(m & ((1u << lane) - 1u)));
+                emit_child<CM, NS>(P, nd, c, j, r, full.p, full.W, full.As, k, outf, rbase + __popc(m & ((1u << lane) - 1u)));
             }
         }
     }

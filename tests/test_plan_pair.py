@@ -101,3 +101,16 @@ def test_pair_bad_fraction(api, frac):
     s = api.Session(prob, n_loads=1)
     with pytest.raises(L.CamelotError):
         s.plan_max_then_min(frac)
+
+
+def test_resident_needs_upload(api):
+    """CAMELOT_EXEC_RESIDENT reuses the workspace's problem image: a Session refuses it
+    before anything uploaded the problem (the round-2 bench hang), and accepts it after."""
+    from paper_2005_02088_b200 import _lib as L
+    prob = G.config_problems(2)[0]
+    s = api.Session(prob, n_loads=1)
+    with pytest.raises(L.CamelotError):
+        s.plan_max_then_min(0.3, resident=True)
+    ref = s.plan_max_then_min(0.3)          # a non-resident call uploads the image
+    got = s.plan_max_then_min(0.3, resident=True)
+    assert got[0].index == ref[0].index and got[1].index == ref[1].index
