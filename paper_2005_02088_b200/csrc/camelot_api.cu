@@ -778,10 +778,13 @@ void range_of(const Ctx &X, const camelot_exec *ex, unsigned long long &lo, unsi
 
 bool use_coarse(const Ctx &X, bool prune) { return prune && !X.naive && X.d.nQ >= 8 && X.d.ntot > 4000000ull; }
 // quota sub-grid strides of the incumbent cascade (every stride-th quota counted
-// from the top, so 100% is always included).  CAMELOT_COARSE="25,10" overrides.
-std::vector<int> coarse_strides(const Ctx &X) {
+// from the top, so 100% is always included).  CAMELOT_COARSE="25,10" overrides (and
+// CAMELOT_COARSE_P0 / _P1 per policy: experiments).
+std::vector<int> coarse_strides(const Ctx &X, int policy) {
     std::vector<int> v;
-    if (const char *e = getenv("CAMELOT_COARSE")) {
+    const char *e = getenv(policy == 0 ? "CAMELOT_COARSE_P0" : "CAMELOT_COARSE_P1");
+    if (!e) e = getenv("CAMELOT_COARSE");
+    if (e) {
         const char *p = e;
         while (*p) {
             char *q = nullptr;
@@ -792,10 +795,21 @@ std::vector<int> coarse_strides(const Ctx &X) {
         }
         return v;
     }
-    // measured on C4 / C5: (nQ/2, nQ/5, nQ/20) = C4 (50, 20, 5) (1.36 ms
-    // both policies vs 1.41 for (50, 25, 5)), C5 (5, 2)
-    for (int s : {X.d.nQ / 2, X.d.nQ / 5, X.d.nQ / 20})
+    // measured: coarse grids (nQ < 50) use (nQ/2, nQ/5, nQ/20), e.g. C5
+    // (5, 2); fine grids use per-policy strides, max load (nQ/2, nQ/9, nQ/25) = (50, 11, 4)
+    // and min resource (nQ/2, nQ/5, nQ/14) = (50, 20, 7) on the 1% grid: over eight
+    // C4-shaped problems (C4, C4b and six other seeds / QoS scales) they cut the plan
+    // pair's geometric-mean time from 4.9 to 2.8 ms, and none got slower
+    const int nQ = X.d.nQ;
+    int div[3] = {2, 5, 20};
+    if (nQ >= 50) {
+        div[1] = policy == 0 ? 9 : 5;
+        div[2] = policy == 0 ? 25 : 14;
+    }
+    for (int d : div) {
+        const int s = nQ / d;
         if (s >= 2 && (v.empty() || s < v.back())) v.push_back(s);
+    }
     return v;
 }
 
@@ -842,7 +856,7 @@ int local_search(const Ctx &X, const camelot_exec *ex, int policy, int nlev, lon
         // pass seeds the next); replicated on every rank.  The coarse levels small
         // enough for an exhaustive scan are replaced by ONE leaf sweep of the finest
         // of them (its optimum is at least as good as any coarser level's).
-        std::vector<int> strides = coarse_strides(X);
+        std::vector<int> strides = coarse_strides(X, policy);
         if (sweep_supported(X.P, policy, nlev) && lo == 0 && hi == X.d.ntot && !getenv("CAMELOT_NO_SWEEP")) {
             int flat_s = 0;
             for (int s2 : strides) {
