@@ -100,6 +100,7 @@ __device__ __forceinline__ bool sw_place(const DevProb &P, SwState<CM, NS> &s, i
             gs = g;
         }
     int kk[CM];
+    uint32_t hmask = 0u;
     if (gs >= 0) {
 #pragma unroll
         for (int g = 0; g < CM; ++g) kk[g] = g == gs ? N : 0;
@@ -125,9 +126,12 @@ __device__ __forceinline__ bool sw_place(const DevProb &P, SwState<CM, NS> &s, i
             s.cnt[g] += k;
             s.rm[g] -= W + (uint32_t)k * As;
             s.dem[g] = __fadd_rn(s.dem[g], __fmul_rn((float)k, bw));
-            s.hm[i] |= 1u << g;
+            hmask |= 1u << g;
         }
     }
+#pragma unroll
+    for (int i2 = 0; i2 < NS; ++i2)
+        if (i2 == i) s.hm[i2] = hmask;   // stage i is new (i may be a runtime value: no local array)
     // max demand over the hosting GPUs of every placed stage (demand only grows)
 #pragma unroll
     for (int i2 = 0; i2 < NS; ++i2) {
@@ -203,6 +207,56 @@ __device__ __forceinline__ float bw_threshold(float dem, float BW) {
     return __fadd_rn(h, 0.0f);   // -0 -> +0 (the sign-bit test of the sweep needs +0)
 }
 
+// fits in bandwidth of k replicas of one-replica demand bw under the threshold h of
+// bw_threshold: fl(k bw) <= h  <=>  fl(h - fl(k bw)) has a clear sign bit (exact: RN
+// keeps the sign and gradual underflow never rounds a non-zero difference to 0)
+__device__ __forceinline__ bool bw_fits(float h, float kbw) { return !(__float_as_uint(__fsub_rn(h, kbw)) >> 31); }
+
+// First sub-grid index ts in [0, hi) at which k replicas no longer fit in bandwidth
+// (hi if they fit everywhere).  Valid when the row's bw is non-decreasing along the
+// sub-grid (then fl(k bw(ts)) is non-decreasing and the fitting ts form a prefix).
+__device__ __forceinline__ int bw_break(const float4 *row, int nQ, int qs, int nQs, int k, float h, int hi) {
+    auto kbw = [&](int ts) {
+        const float bw = row[nQ - 1 - qs * (nQs - 1 - ts)].z;
+        return k == 1 ? bw : __fmul_rn((float)k, bw);
+    };
+    if (hi <= 0 || bw_fits(h, kbw(hi - 1))) return hi;
+    int lo = 0, up = hi - 1;   // the answer is in [lo, up]: ts = up fails
+    while (lo < up) {
+        const int mid = (lo + up) >> 1;
+        if (bw_fits(h, kbw(mid))) lo = mid + 1;
+        else up = mid;
+    }
+    return lo;
+}
+
+// The thermometer code M of one quota (see the leaf loop) straight from the definition:
+// c_g = min(instance+memory capacity, floor(rq/p), #{k in 1..4 : fl(dem + fl(k bw)) <= BW})
+// per GPU, c_g ones in the nibble of the GPU's rank.  Out of line: only leaf rows whose
+// bandwidth is not non-decreasing in the quota take it (never for the generated tables).
+static __device__ __noinline__ uint32_t sw_therm_slow(const DevProb &P, int Rmax, uint32_t WL, uint32_t AsL, int p, float bw,
+                                                   bool cap, uint32_t perm, const uint32_t *rqc, const uint32_t *rmv,
+                                                   const float *demv, int stride) {
+    uint32_t M = 0u;
+    for (int r = 0; r < P.C; ++r) {
+        const int g = (perm >> (4 * r)) & 0xF;
+        const uint32_t w = rqc[g * stride];
+        const int rq = (int)(w & 0xFFu), cnt = (int)(w >> 8);
+        const float dem = demv[g * stride];
+        int c = min(Rmax, P.I - cnt);
+        int km = 0;
+        for (int t = 1; t <= 4; ++t) km += (t <= c) & (WL + (uint32_t)t * AsL <= rmv[g * stride]);
+        c = min(km, rq / p);
+        if (cap) {
+            int kb = 0;
+            for (int t = 1; t <= 4; ++t) kb += __fadd_rn(dem, __fmul_rn((float)t, bw)) <= P.BW;
+            c = min(c, kb);
+        }
+        M += ((1u << c) - 1u) << (4 * r);
+    }
+    return M;
+}
+
 __device__ __forceinline__ void sw_better(unsigned long long key, unsigned long long x, unsigned long long &bk,
                                           unsigned long long &bx) {
     if (key < bk || (key == bk && x < bx)) {
@@ -218,6 +272,8 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
     __shared__ float dem_s[CM][SWEEP_THREADS];
     __shared__ uint32_t rqc_s[CM][SWEEP_THREADS], rm_s[CM][SWEEP_THREADS];   // cold: failure bits
     __shared__ uint32_t qpm_s[CAMELOT_MAX_QUOTAS];   // p | ceil(2^16/p) << 7
+    __shared__ unsigned char qcnt_s[128];            // #{sub-grid ts : p(ts) <= v}, v < 128
+    __shared__ unsigned char mono_s[CAMELOT_MAX_BATCHES];   // leaf row of batch b: bw >= 0, non-decreasing
     __shared__ unsigned long long red_k[SWEEP_THREADS / 32], red_x[SWEEP_THREADS / 32];
     __shared__ unsigned long long red_c[SWEEP_THREADS / 32][2];
     __shared__ unsigned red_v[SWEEP_THREADS / 32];
@@ -247,9 +303,26 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
         const uint32_t p = (uint32_t)P.Q[t];
         qpm_s[t] = p | (((65536u + p - 1u) / p) << 7);
     }
+    for (int v = tid; v < 128; v += blockDim.x) {
+        int c = 0;
+        for (int ts = 0; ts < nQs; ++ts) c += P.Q[nQ - 1 - qs * (nQs - 1 - ts)] <= v;
+        qcnt_s[v] = (unsigned char)c;
+    }
     __syncthreads();   // (also publishes the initialised barrier)
     if (staged) mbar_wait(&tbar, 0);
     const float4 *tabLall = staged ? tabL_s : P.tab + (size_t)jl * P.nS * nQ;
+    for (int b = tid; b < P.nS; b += blockDim.x) {
+        const float4 *row = tabLall + (size_t)b * nQ;
+        float prev = 0.0f;
+        bool m = true;
+        for (int ts = 0; ts < nQs; ++ts) {
+            const float z = row[nQ - 1 - qs * (nQs - 1 - ts)].z;
+            m = m && z >= prev;   // (false for NaN)
+            prev = z;
+        }
+        mono_s[b] = m;
+    }
+    __syncthreads();
     unsigned long long bk = A.inc[0].key, bx = A.inc[0].x;
     unsigned long long n_sc = 0, n_fe = 0;
     unsigned viol = 0;
@@ -291,39 +364,19 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
                     t /= (unsigned)Os;
                 }
             int bc = (int)t;
-            for (int a = P.A - 1; a >= 0; --a) {
-                beta[a] = bc % P.nS;
+            beta[0] = beta[1] = 0;
+            if (P.A > 1) {
+                beta[1] = bc % P.nS;
                 bc /= P.nS;
             }
+            beta[0] = bc;
         }
-        SwState<CM, NS> st;
-        sw_init<CM, NS>(P, st);
-        bool ok = lane_ok;
-        float dur[NS], bwv[NS], ntv[NS];
-#pragma unroll
-        for (int i = 0; i < NS; ++i) {
-            dur[i] = 0.0f;
-            bwv[i] = 0.0f;
-            ntv[i] = 0.0f;
-            if (i < n - 2 && ok) {
-                const int b = beta[P.app[i]];
-                const int th = o[i] % nQ, N = o[i] / nQ + 1;
-                const float4 e = __ldg(&P.tab[((size_t)i * P.nS + b) * nQ + th]);
-                const uint32_t As = P.Am[i] * (uint32_t)P.S[b];
-                ok = sw_place<CM, NS>(P, st, i, N, (int)(qpm_s[th] & 127u), qpm_s[th] >> 7, P.W[i], As, e.z);
-                dur[i] = e.x;
-                bwv[i] = e.z;
-                ntv[i] = __fmul_rn((float)N, e.y);
-            }
-        }
-        if (gpk == 1 && !ok) continue;   // the whole grandparent is infeasible (uniform)
-        // ---- parent (per lane): option of stage n-2
+        // ---- parent (per lane): option of stage n-2, its canonical index and range
         const int ops = gpk == 1 ? ch * 32 + lane : lane % Os;   // parent option in the (sub-)grid
         const int op = canon(min(ops, Os - 1));      // canonical option code
         unsigned long long gpc = 0;                  // canonical grandparent index
         {
-            int bc = 0;
-            for (int a = 0; a < P.A; ++a) bc = bc * P.nS + beta[a];
+            const int bc = P.A > 1 ? beta[0] * P.nS + beta[1] : beta[0];
             gpc = (unsigned long long)bc;
 #pragma unroll
             for (int k = 0; k < NS; ++k)
@@ -334,25 +387,42 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
         int clo = 0, chi = O;
         if (A.lo > xpO) clo = (int)min(A.lo - xpO, (unsigned long long)O);
         if (A.hi < xpO + O) chi = A.hi > xpO ? (int)(A.hi - xpO) : 0;
-        bool act = ok && ops < Os && clo < chi;
+        bool act = lane_ok && ops < Os && clo < chi;
         if (act && A.world > 1) {
             const unsigned long long item = xp / P.opow[n - 1 - A.d0];
             act = ((item / 64ull) % (unsigned long long)A.world) == (unsigned long long)A.rank;
         }
-        if (act && n >= 2) {
-            const int i = n - 2;
-            const int b = beta[P.app[i]];
-            const int th = op % nQ, N = op / nQ + 1;
+        // ---- placement of stages 0..n-2: the grandparent's options (warp-uniform unless
+        // gpack > 1), then the lane's parent option.  A rolled loop (one copy of sw_place):
+        // this code runs once per work item, and unrolled it thrashed the instruction cache.
+        SwState<CM, NS> st;
+        sw_init<CM, NS>(P, st);
+        float dur[NS], bwv[NS], ntv[NS];
+#pragma unroll
+        for (int i = 0; i < NS; ++i) dur[i] = bwv[i] = ntv[i] = 0.0f;
+#pragma unroll 1
+        for (int i = 0; i <= n - 2 && act; ++i) {
+            int oi = op;
+#pragma unroll
+            for (int k = 0; k < NS; ++k)
+                if (k == i && k < n - 2) oi = o[k];
+            const int b = P.app[i] ? beta[1] : beta[0];
+            const int th = oi % nQ, N = oi / nQ + 1;
             const float4 e = __ldg(&P.tab[((size_t)i * P.nS + b) * nQ + th]);
             const uint32_t As = P.Am[i] * (uint32_t)P.S[b];
             act = sw_place<CM, NS>(P, st, i, N, (int)(qpm_s[th] & 127u), qpm_s[th] >> 7, P.W[i], As, e.z);
-            dur[i] = e.x;
-            bwv[i] = e.z;
-            ntv[i] = __fmul_rn((float)N, e.y);
+            const float nt = __fmul_rn((float)N, e.y);
+#pragma unroll
+            for (int k = 0; k < NS; ++k)
+                if (k == i) {
+                    dur[k] = e.x;
+                    bwv[k] = e.z;
+                    ntv[k] = nt;
+                }
         }
         if (act) {
         // ---- leaf context: capacities, deployment order, bounds (per lane)
-        const int bL = beta[P.app[jl]];
+        const int bL = P.app[jl] ? beta[1] : beta[0];
         const uint32_t WL = P.W[jl], AsL = P.Am[jl] * (uint32_t)P.S[bL];
         const float gL = cont ? P.gamma[jl] : 0.0f;
         // COMM (R29): hand-over times of the edges between placed stages (exact), and the
@@ -362,42 +432,69 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
         for (int i = 0; i < NS; ++i) {
             te[i] = 0.0f;
             if (COMM && i + 1 < n && P.app[i] == P.app[i + 1]) {
-                const float tx = __fmul_rn(__fmul_rn(P.comm_mb[i], (float)P.S[beta[P.app[i]]]), P.inv_link);
+                const float tx = __fmul_rn(__fmul_rn(P.comm_mb[i], (float)P.S[P.app[i] ? beta[1] : beta[0]]), P.inv_link);
                 te[i] = (i + 1 < jl && st.hm[i] == st.hm[i + 1] && __popc(st.hm[i]) == 1) ? P.ipc_ms : tx;
             }
         }
-        int kim[CM];
-        uint32_t bsh[CM];   // 1 << (4 * rank): the GPU's nibble in the thermometer code
-        float hb[CM];      // bandwidth threshold: fits(k) <=> fl(k bw) <= hb
+        const float4 *tabL = tabLall + (size_t)bL * nQ;
+        const bool mono = mono_s[bL];
+        // Capacities as BREAKPOINTS in the quota: over the sub-grid
+        // ts = 0..nQs-1 the quota p(ts) increases and (mono rows) so does bw(ts), so
+        // c_g(ts) >= k  <=>  ts < brk[g][k] with brk[g][k] = the first ts where k replicas
+        // no longer fit (0 if k exceeds the instance+memory capacity).  The breakpoints
+        // are packed as bytes b | 0x80 (b <= 127): rank r's k-th breakpoint is byte r >> 1
+        // of wE[k-1] (even r) or wO[k-1] (odd r), so that per quota one subtraction of
+        // (ts + 1) per byte sets bit 7 exactly where c >= k, in rank order.
+        uint32_t wE[4], wO[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) wE[k] = wO[k] = 0x80808080u;
         uint32_t perm = 0u, E = 0u;
 #pragma unroll
         for (int g = 0; g < CM; ++g) {
-            int k = 0;
-            hb[g] = __int_as_float(0xff800000);   // -inf: nothing fits (padding GPUs)
-            if (g < P.C) {
-                k = min(Rmax, P.I - st.cnt[g]);
-                int km = 0;   // memory: k' <= k with WL + k' AsL <= rm (Rmax <= 4; no division)
-#pragma unroll
-                for (int t = 1; t <= 4; ++t) km += (t <= k) & (WL + (uint32_t)t * AsL <= st.rm[g]);
-                k = km;
-                if (st.cnt[g] == 0) E |= 1u << g;
-                hb[g] = cap ? bw_threshold(st.dem[g], P.BW) : __int_as_float(0x7f800000);
-            }
-            kim[g] = k;
-            int r = 0;
+            int r = g;
             if (g < P.C) {   // rank in the (rm, rq, id) order: packed 32-bit keys (see sw_place)
+                r = 0;
                 const uint32_t kg = (st.rm[g] << 11) | ((uint32_t)st.rq[g] << 4) | (uint32_t)g;
 #pragma unroll
                 for (int h = 0; h < CM; ++h)
                     if (h < P.C) r += ((st.rm[h] << 11) | ((uint32_t)st.rq[h] << 4) | (uint32_t)h) < kg;
-            } else {
-                r = g;
+                if (st.cnt[g] == 0) E |= 1u << g;
             }
-            bsh[g] = 1u << (4 * r);
             perm |= (uint32_t)g << (4 * r);
             dem_s[g][tid] = st.dem[g];
             rqc_s[g][tid] = (uint32_t)st.rq[g] | ((uint32_t)st.cnt[g] << 8);
             rm_s[g][tid] = st.rm[g];
+        }
+        // the breakpoints, rank by rank (rolled; the GPU's state from its shared-memory copy)
+        if (mono) {
+#pragma unroll 1
+            for (int r = 0; r < P.C; ++r) {
+                const int g = (perm >> (4 * r)) & 0xF;
+                const uint32_t w = rqc_s[g][tid], rm = rm_s[g][tid];
+                const int rq = (int)(w & 0xFFu), kc = min(Rmax, P.I - (int)(w >> 8));
+                const float hb = cap ? bw_threshold(dem_s[g][tid], P.BW) : __int_as_float(0x7f800000);
+                int prev = nQs;
+                uint32_t bytes = 0u;   // byte k-1 = the k-th breakpoint (non-increasing in k)
+#pragma unroll 1
+                for (int k = 1; k <= 4 && prev > 0; ++k) {
+                    int b = 0;
+                    // instance + memory: k <= cap, WL + k AsL <= rm
+                    if (k <= kc && WL + (uint32_t)k * AsL <= rm) {
+                        const int ql = k == 1 ? rq : k == 2 ? rq >> 1 : k == 3 ? (rq * 43691) >> 17 : rq >> 2;
+                        b = min((int)qcnt_s[ql], prev);   // quota: p(ts) <= floor(rq / k)
+                        if (cap) b = bw_break(tabL, nQ, qs, nQs, k, hb, b);
+                    }
+                    prev = b;
+                    bytes |= (uint32_t)b << (8 * (k - 1));
+                }
+                const int sh = 8 * (r >> 1);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t v = ((bytes >> (8 * k)) & 0xFFu) << sh;
+                    if (r & 1) wO[k] |= v;
+                    else wE[k] |= v;
+                }
+            }
         }
         float ptub = __int_as_float(0x7f800000);
 #pragma unroll
@@ -406,7 +503,6 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
                 const float k = sw_kappa(st.dm[i], bwv[i], cont ? P.gamma[i] : 0.0f, P.invBW);
                 ptub = fminf(ptub, k == 1.0f ? ntv[i] : __fdiv_rn(ntv[i], k));
             }
-        const float4 *tabL = tabLall + (size_t)bL * nQ;
         const float qos0 = P.qos[0], qos1 = TWO ? P.qos[1] : 0.0f;
         const int f1 = TWO ? P.first_of_app[1] : n;   // first stage of application 2
         float gam[NS];
@@ -418,8 +514,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
             lam0 = A.lam[0];
             lam1 = TWO ? A.lam[1] : 0.0f;
             if (P.flags & F_EQ2_BUDGET) {
-                int bc = 0;
-                for (int a = 0; a < P.A; ++a) bc = bc * P.nS + beta[a];
+                const int bc = P.A > 1 ? beta[0] * P.nS + beta[1] : beta[0];
                 ybud = A.y[bc * A.ystride + A.yoff];
             }
         }
@@ -429,24 +524,26 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
         // ---- the leaves: quota theta outer (capacities once), replicas N inner.
         // Kept compact (rolled N loop, no per-GPU branches): the hot loop must stay
         // within the ~6 KB L0 instruction cache.
+        uint32_t t1 = 0u;   // (ts + 1) in every byte
         for (int ts = 0; ts < nQs; ++ts) {
             const int th = nQ - 1 - qs * (nQs - 1 - ts);
             const float4 e = tabL[th];
             const uint32_t qp = qpm_s[th];
-            const uint32_t pmul = qp >> 7;
             const float bw = e.z;
-            // fl(k bw) for k = 1..4 (the bandwidth fit test)
-            const float nb2 = __fmul_rn(2.0f, bw), nb3 = __fmul_rn(3.0f, bw), nb4 = __fmul_rn(4.0f, bw);
-            uint32_t M = 0u;   // thermometer code of c_g = canHold(g, Rmax), 4 bits per GPU in deployment order
+            // thermometer code of c_g = canHold(g, Rmax): c_g ones in the nibble of the GPU's
+            // rank (4 bits per GPU in deployment order).  Byte b | 0x80 minus (ts + 1) keeps
+            // bit 7 iff b > ts (no borrow between bytes: b, ts + 1 <= 127), i.e. iff c >= k;
+            // that bit moves to position 4 r + k - 1.
+            t1 += 0x01010101u;
+            uint32_t M = 0u;
+            if (mono) {
 #pragma unroll
-            for (int g = 0; g < CM; ++g) {
-                // fl(k bw) <= h  <=>  fl(h - fl(k bw)) has a clear sign bit (exact: RN keeps
-                // the sign and gradual underflow never rounds a non-zero difference to 0)
-                const float h = hb[g];
-                const uint32_t nf = (__float_as_uint(__fsub_rn(h, bw)) >> 31) + (__float_as_uint(__fsub_rn(h, nb2)) >> 31) +
-                                    (__float_as_uint(__fsub_rn(h, nb3)) >> 31) + (__float_as_uint(__fsub_rn(h, nb4)) >> 31);
-                const int c = min(min(kim[g], (int)(((uint32_t)st.rq[g] * pmul) >> 16)), 4 - (int)nf);
-                M += (bsh[g] << c) - bsh[g];   // c ones in the GPU's nibble (c <= 4)
+                for (int k = 1; k <= 4; ++k)
+                    M |= (((wE[k - 1] - t1) >> (8 - k)) & (0x80808080u >> (8 - k))) |
+                         (((wO[k - 1] - t1) >> (4 - k)) & (0x80808080u >> (4 - k)));
+            } else {
+                M = sw_therm_slow(P, Rmax, WL, AsL, (int)(qp & 127u), bw, cap, perm, &rqc_s[0][tid], &rm_s[0][tid],
+                                  &dem_s[0][tid], SWEEP_THREADS);
             }
             // deployment succeeds iff the total capacity holds N (pass 1 or pass 2)
             const int sumc = __popc(M);

@@ -121,3 +121,38 @@ def test_sweep_c4_slice_vs_oracle_and_tree(api, oracle):
     finally:
         del os.environ["CAMELOT_NO_SWEEP"]
     assert tree.index == got.index and tree.n_feasible == got.n_feasible
+
+
+@pytest.mark.parametrize("case", CASES[:4])
+@pytest.mark.parametrize("mode", ["permuted", "scaled"])
+def test_sweep_bandwidth_rows(api, oracle, case, mode):
+    """permuted: leaf rows whose bandwidth is not non-decreasing in the quota (possible
+    for tables built from decision trees) take the sweep's per-quota capacity path
+    instead of the quota breakpoints -- every second batch row of every stage gets its
+    bandwidths permuted along the quota grid.  scaled: every bandwidth x3 (rows stay
+    non-decreasing), so the bandwidth cap binds often and the breakpoint searches
+    decide.  The result is the oracle's either way."""
+    seed, n, C, A, q, b, R, rho = case
+    prob = G.random_small_problem(seed, n_stages=n, n_gpus=C, n_apps=A, quota_step=q, batches=b,
+                                  max_replicas=R, qos_rho=rho)
+    if oracle.ntot(prob) > 6_000_000:
+        pytest.skip("space too large for the in-test oracle")
+    rng = np.random.default_rng(seed)
+    tab = prob.table.copy()
+    if mode == "scaled":
+        tab[..., 2] *= np.float32(3.0)
+    else:
+        for i in range(tab.shape[0]):
+            for bi in range(0, tab.shape[1], 2):
+                tab[i, bi, :, 2] = tab[i, bi, rng.permutation(tab.shape[2]), 2] * np.float32(1.5)
+    prob = prob.with_(table=tab)
+    flags = _flat(prob)
+    got = api.Session(prob, flags=flags).plan_max_load()
+    ref = oracle.search(prob, threads=8)[0]
+    assert got.index == ref.index and got.n_feasible == ref.n_feasible
+    if ref.index is None:
+        return
+    lam = [[np.float32(0.3) * np.float32(ref.T)] * A]
+    got = api.Session(prob, n_loads=1, flags=flags).plan_min_resource(lam)[0]
+    ref = oracle.search(prob, "min_resource", loads=lam, threads=8)[0]
+    assert got.index == ref.index
