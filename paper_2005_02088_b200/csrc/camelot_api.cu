@@ -40,6 +40,14 @@ struct EvPair {
 };
 thread_local EvPair t_ev;
 thread_local EvPair t_ev_spare;   // camelot_plan_max_then_min: the first search's events
+// camelot_plan_max_then_min: the second stream that scores the max-load plan while the
+// min-resource search runs, and its fork / join events (per thread, per device)
+struct SideStream {
+    int dev = -1;
+    cudaStream_t s = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+thread_local SideStream t_side;
 
 // What the last camelot_search_local left in a workspace: camelot_finalize reads
 // that state (local best, filter records, loads, Eq. 2 estimates), so it must be
@@ -82,7 +90,7 @@ size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
     size_t hdr, hdr2, tab, Q, S, rec, sb, item_off, lam, y, inc, result, keys, winner, rescan, plans, slots,
-        front0, front1, total;
+        front0, front1, side_w, side_h, total;
     int nlev;
     unsigned long long fcap;   // frontier capacity (nodes) of each ping-pong buffer
 };
@@ -203,6 +211,8 @@ Layout make_layout(const Dims &d, int nlev) {
     L.winner = put((size_t)L.nlev * sizeof(Slot));
     L.rescan = put((size_t)L.nlev * sizeof(unsigned long long));
     L.plans = put((size_t)(L.nlev + 1) * sizeof(camelot_plan));   // + the max-load plan of camelot_plan_max_then_min
+    L.side_w = put(sizeof(Slot));          // camelot_plan_max_then_min: the max-load winner and
+    L.side_h = put(sizeof(DevHeader));     // counters, scored on a second stream
     L.slots = put((size_t)MAXSLOTS * L.nlev * sizeof(Slot));
     // frontier of placement-state nodes: as many as there are leaf parents in the
     // whole space, clamped to [256, 2^20] (overflow falls back to inline DFS)
@@ -904,7 +914,7 @@ int local_search(const Ctx &X, const camelot_exec *ex, int policy, int nlev, lon
 // resolve the reduced keys (+ chunk re-scan when sharded) and score the winners into
 // dplans[0..nlev) on the device; no host synchronisation when world == 1
 int finalize_enqueue(const Ctx &X, const camelot_exec *ex, int policy, int nlev, const long long *d_keys,
-                     camelot_plan *dplans) {
+                     camelot_plan *dplans, bool plan = true) {
     const bool prune = !(X.P.flags & F_NO_FILTER);
     char *ws = X.ws;
     Slot *winner = reinterpret_cast<Slot *>(ws + X.L.winner);
@@ -932,6 +942,7 @@ int finalize_enqueue(const Ctx &X, const camelot_exec *ex, int policy, int nlev,
             if (rc) return rc;
         }
     }
+    if (!plan) return CAMELOT_OK;
     plan_kernel<<<nlev, PLAN_THREADS, 0, X.st>>>(X.P, policy, nlev, winner, reinterpret_cast<const float *>(ws + X.L.lam),
                                                    reinterpret_cast<const DevHeader *>(ws + X.L.hdr2), dplans);
     COUNT_LAUNCH();
@@ -1097,19 +1108,43 @@ int camelot_plan_max_then_min(const camelot_problem *p, const camelot_cluster *c
     int rc = setup(p, c, ex, 1, X, true);
     if (rc) return rc;
     camelot_plan *dplans = reinterpret_cast<camelot_plan *>(X.ws + X.L.plans);   // [0] min-resource, [1] max-load
-    // max-load search and its plan, kept on the device
+    // max-load search and its winner
     rc = local_search(X, ex, 0, 1, nullptr);
     if (rc) return rc;
-    rc = finalize_enqueue(X, ex, 0, 1, reinterpret_cast<const long long *>(X.ws + X.L.keys), dplans + 1);
+    rc = finalize_enqueue(X, ex, 0, 1, reinterpret_cast<const long long *>(X.ws + X.L.keys), dplans + 1, false);
     if (rc) return rc;
     std::swap(t_ev, t_ev_spare);   // keep the max-load search's events
-    // the low load from the peak, on the device (no host round trip), then min resource
-    low_load_kernel<<<1, 32, 0, X.st>>>(X.P, dplans + 1, low_load_frac, reinterpret_cast<float *>(X.ws + X.L.lam));
+    if (t_side.dev != ex->device) {
+        if (t_side.s) {
+            cudaStreamDestroy(t_side.s);
+            cudaEventDestroy(t_side.fork);
+            cudaEventDestroy(t_side.join);
+        }
+        CU(cudaStreamCreateWithFlags(&t_side.s, cudaStreamNonBlocking));
+        CU(cudaEventCreateWithFlags(&t_side.fork, cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&t_side.join, cudaEventDisableTiming));
+        t_side.dev = ex->device;
+    }
+    // the low load from the peak, on the device (no host round trip) + a snapshot of the
+    // max-load winner and counters; the max-load plan is then scored on the second
+    // stream while the min-resource search runs on this one
+    Slot *side_w = reinterpret_cast<Slot *>(X.ws + X.L.side_w);
+    DevHeader *side_h = reinterpret_cast<DevHeader *>(X.ws + X.L.side_h);
+    low_load_kernel<<<1, 64, 0, X.st>>>(X.P, reinterpret_cast<const Slot *>(X.ws + X.L.winner),
+                                        reinterpret_cast<const DevHeader *>(X.ws + X.L.hdr2), low_load_frac,
+                                        reinterpret_cast<float *>(X.ws + X.L.lam), side_w, side_h);
     COUNT_LAUNCH();
     CU(cudaGetLastError());
+    CU(cudaEventRecord(t_side.fork, X.st));
+    CU(cudaStreamWaitEvent(t_side.s, t_side.fork, 0));
+    plan_kernel<<<1, PLAN_THREADS, 0, t_side.s>>>(X.P, 0, 1, side_w, reinterpret_cast<const float *>(X.ws + X.L.lam),
+                                                   side_h, dplans + 1);
+    COUNT_LAUNCH();
+    CU(cudaGetLastError());
+    CU(cudaEventRecord(t_side.join, t_side.s));
     rc = local_search(X, ex, 1, 1, nullptr);
-    if (rc) return rc;
-    rc = finalize_enqueue(X, ex, 1, 1, reinterpret_cast<const long long *>(X.ws + X.L.keys), dplans);
+    if (!rc) rc = finalize_enqueue(X, ex, 1, 1, reinterpret_cast<const long long *>(X.ws + X.L.keys), dplans);
+    CU(cudaStreamWaitEvent(X.st, t_side.join, 0));   // join the max-load plan (also on an error)
     if (rc) return rc;
     camelot_plan both[2];
     CU(cudaMemcpyAsync(both, dplans, 2 * sizeof(camelot_plan), cudaMemcpyDeviceToHost, X.st));

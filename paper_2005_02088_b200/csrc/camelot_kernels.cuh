@@ -395,6 +395,9 @@ struct PlanScratch {
     FullScore s;
     ScoreScratch scr;
     int beta[AMAX], rho[NMAX], theta[NMAX];
+    float dur[NMAX], thr[NMAX], bwv[NMAX];
+    int pq[NMAX];
+    uint32_t As[NMAX];
     int eq2y;
 };
 // The full plan of winner w, scored by ONE whole CTA (>= 32 threads; every thread
@@ -421,9 +424,34 @@ CAM_DEVFN void plan_block(const DevProb &P, int policy, const Slot w, const floa
             pl.index = ~0ull;
             pl.status = CAMELOT_INFEASIBLE;
             pl.violations = hdr->viol_or;
-        } else {
-            decode_index(P, w.x, beta, rho, theta);
         }
+    }
+    // mixed-radix decode (decode_index's digits), one digit per thread: option o_i =
+    // (x / O^(n-1-i)) mod O = rho_i nQ + theta_i; the batch combo = x / O^n
+    if (w.x != ~0ull) {
+        if (tid < P.n) {
+            const unsigned o = (unsigned)((w.x / P.opow[P.n - 1 - tid]) % (unsigned long long)P.O);
+            rho[tid] = (int)(o / (unsigned)P.nQ);
+            theta[tid] = (int)(o % (unsigned)P.nQ);
+        } else if (tid == P.n) {
+            unsigned bc = (unsigned)(w.x / P.opow[P.n]);
+            for (int a = P.A - 1; a >= 0; --a) {
+                beta[a] = (int)(bc % (unsigned)P.nS);
+                bc /= (unsigned)P.nS;
+            }
+        }
+    }
+    __syncthreads();
+    // the winner's table rows, quotas and activation sizes, one stage per thread (one
+    // round trip instead of a dependent chain per stage)
+    if (w.x != ~0ull && tid < P.n) {
+        const int i = tid, b = beta[P.app[i]];
+        const float4 e = P.tab[((size_t)i * P.nS + b) * P.nQ + theta[i]];
+        ps.dur[i] = e.x;
+        ps.thr[i] = e.y;
+        ps.bwv[i] = e.z;
+        ps.pq[i] = P.Q[theta[i]];
+        ps.As[i] = P.Am[i] * (uint32_t)P.S[b];
     }
     __syncthreads();
     if (w.x != ~0ull && tid < 32) {
@@ -432,19 +460,18 @@ CAM_DEVFN void plan_block(const DevProb &P, int policy, const Slot w, const floa
             float dur[NMAX], thr[NMAX], bwv[NMAX], kmax[NMAX];
             uint32_t hm[NMAX];
             for (int i = 0; i < P.n; ++i) {
-                const float4 e = P.tab[((size_t)i * P.nS + beta[P.app[i]]) * P.nQ + theta[i]];
-                dur[i] = e.x;
-                thr[i] = e.y;
-                bwv[i] = e.z;
+                dur[i] = ps.dur[i];
+                thr[i] = ps.thr[i];
+                bwv[i] = ps.bwv[i];
             }
             for (int q = tid; q < NMAX * SCORE_RMAX; q += 32) s.goi[q] = -1;
             __syncwarp();
             int u = 0;
-            placed = place_warp(P, beta, rho, theta, bwv, kmax, hm, s.goi, u);
+            placed = place_warp(P, rho, ps.pq, ps.As, bwv, kmax, hm, s.goi, u);
             __syncwarp();
             if (placed && tid == 0) {
                 int U = 0;
-                for (int i = 0; i < P.n; ++i) U += (rho[i] + 1) * P.Q[theta[i]];
+                for (int i = 0; i < P.n; ++i) U += (rho[i] + 1) * ps.pq[i];
                 s.U = U;
                 score_finish(P, beta, rho, dur, thr, kmax, hm, 0u, u, s);
             }
@@ -477,7 +504,7 @@ CAM_DEVFN void plan_block(const DevProb &P, int policy, const Slot w, const floa
         if (tid < P.n) {
             const int i = tid;
             pl.replicas[i] = rho[i] + 1;
-            pl.quota_pct[i] = P.Q[theta[i]];
+            pl.quota_pct[i] = ps.pq[i];
             pl.stage_latency_ms[i] = s.L[i];
             pl.stage_throughput_qps[i] = s.Ti[i];
             pl.kappa[i] = s.kappa[i];
@@ -505,13 +532,25 @@ CAM_GLOBAL void __launch_bounds__(PLAN_THREADS) plan_kernel(const DevProb P, int
 
 // The low load of camelot_plan_max_then_min (low load = a fraction
 // of the peak): load_a = fl(frac * T*) for every application, T* the max-load
-// plan's objective (the binary32 rounding of the float64 product, as a host caller
-// computing frac * T* in double and storing it as float); +inf when there is no
-// feasible peak (every min-resource candidate then fails LOAD).
-CAM_GLOBAL void low_load_kernel(const DevProb P, const camelot_plan *ml, double frac, float *lam) {
-    const int a = threadIdx.x;
-    if (a >= P.A) return;
-    lam[a] = ml->status == CAMELOT_OK ? __double2float_rn(frac * (double)ml->objective) : __int_as_float(0x7f800000);
+// optimum (the binary32 rounding of the float64 product, as a host caller computing
+// frac * T* in double and storing it as float); +inf when there is no feasible peak
+// (every min-resource candidate then fails LOAD).  T* is read from the resolved
+// winner's objective key (0xFFFFFFFF - bits(T): the same binary32 T
+// the plan reports), so the min-resource search need not wait for the max-load
+// plan.  The kernel also snapshots the winner and the search counters (side_w,
+// side_h) for the max-load plan_kernel, which runs on a second stream meanwhile.
+CAM_GLOBAL void low_load_kernel(const DevProb P, const Slot *winner, const DevHeader *hdr2, double frac, float *lam,
+                                Slot *side_w, DevHeader *side_h) {
+    const int t = threadIdx.x;
+    const Slot w = winner[0];
+    if (t < P.A) {
+        const float T = __uint_as_float(0xFFFFFFFFu - (uint32_t)w.key);
+        lam[t] = w.x != ~0ull ? __double2float_rn(frac * (double)T) : __int_as_float(0x7f800000);
+    }
+    if (t == 0) *side_w = w;
+    const uint32_t *src = reinterpret_cast<const uint32_t *>(hdr2);
+    uint32_t *dst = reinterpret_cast<uint32_t *>(side_h);
+    for (int q = t; q < (int)(offsetof(DevHeader, trace_n) / 4); q += blockDim.x) dst[q] = src[q];
 }
 
 // Naive exhaustive search (kernel N5 as a search): one thread scores one

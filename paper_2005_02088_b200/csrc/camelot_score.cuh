@@ -247,7 +247,7 @@ __device__ __forceinline__ void score_finish(const DevProb &P, const int *beta, 
 // GPUs does not change g's state).  Writes kmax / hmask / goi / u for score_finish.
 // Returns false (uniformly) when a stage does not fit: the caller then scores the
 // candidate with score_digits, which also derives the failure bits.
-__device__ __forceinline__ bool place_warp(const DevProb &P, const int *beta, const int *rho, const int *theta,
+__device__ __forceinline__ bool place_warp(const DevProb &P, const int *rho, const int *pq, const uint32_t *Asv,
                                            const float *bwv, float *kmax, uint32_t *hmask, int8_t *goi, int &u) {
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31, C = P.C, n = P.n;
@@ -261,8 +261,8 @@ __device__ __forceinline__ bool place_warp(const DevProb &P, const int *beta, co
 #pragma unroll
     for (int i = 0; i < NMAX; ++i) {
         if (i < n) {
-            const int p = P.Q[theta[i]], N = rho[i] + 1;
-            const uint32_t As = P.Am[i] * (uint32_t)P.S[beta[P.app[i]]], W = P.W[i];
+            const int p = pq[i], N = rho[i] + 1;   // quota and A_i s (gathered by the caller)
+            const uint32_t As = Asv[i], W = P.W[i];
             const float bw = bwv[i];
             auto fits = [&](int k) { return own && fit_viol(P, rq, cnt, rm, dem, k, p, W, As, bw) == 0u; };
             const unsigned long long key =
