@@ -646,6 +646,9 @@ int sweep_pass(const Ctx &X, int dev, int policy, int nlev, const Slot *inc, Slo
     A.keys = keys;
     const size_t tb = (size_t)X.d.nS * X.d.nQ * sizeof(float4);
     A.tabL_bytes = (tb <= SWEEP_TABL_MAX && !getenv("CAMELOT_NO_STAGE")) ? (unsigned)tb : 0u;
+    // small sub-grids (the coarsest cascade level: a few quotas) compute the capacities
+    // per quota; the breakpoints pay off over many quotas (testing knob CAMELOT_BP_MIN)
+    A.bp_min_nqs = getenv("CAMELOT_BP_MIN") ? atoi(getenv("CAMELOT_BP_MIN")) : 9;
     CU(sweep_launch(X.P, A, dev, X.st));
     COUNT_LAUNCH();
     return CAMELOT_OK;

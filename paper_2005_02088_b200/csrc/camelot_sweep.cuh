@@ -14,7 +14,8 @@
 //     c_g = canHold(g, Rmax) are computed once and packed as a thermometer
 //     code in deployment order (4 bits per GPU), so for every replica count N
 //     pass 1 of the deployment heuristic is one shift+ffs and pass 2's greedy
-//     prefix is one popc;
+//     prefix is one popc; the code is built per quota from the
+//     capacities' quota BREAKPOINTS, packed bytes (one subtract per 4 GPUs);
 //   * contention: only the GPU(s) receiving the leaf's replicas change demand,
 //     so every placed stage's max demand is updated by a bit test + max;
 //   * every lane keeps its own best (objective key, index); one reduction at
@@ -183,7 +184,7 @@ static __device__ __noinline__ uint32_t sw_fail_bits(const DevProb &P, int p, fl
 }
 
 // Largest float h with fl(dem + h) <= BW: fl(dem + y) is monotone in y, so
-// fl(dem + fl(k bw)) <= BW  <=>  fl(k bw) <= h  (exact; DESIGN.md 6.7).
+// fl(dem + fl(k bw)) <= BW  <=>  fl(k bw) <= h  (exact; DESIGN.md 6.6).
 __device__ __forceinline__ float bw_threshold(float dem, float BW) {
     // start at fl(BW - dem) and step by one ulp (integer steps on the bit pattern of
     // the non-negative / negative float) until the largest admissible value is found
@@ -437,7 +438,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
             }
         }
         const float4 *tabL = tabLall + (size_t)bL * nQ;
-        const bool mono = mono_s[bL];
+        const bool mono = nQs >= A.bp_min_nqs && mono_s[bL];
         // Capacities as BREAKPOINTS in the quota: over the sub-grid
         // ts = 0..nQs-1 the quota p(ts) increases and (mono rows) so does bw(ts), so
         // c_g(ts) >= k  <=>  ts < brk[g][k] with brk[g][k] = the first ts where k replicas

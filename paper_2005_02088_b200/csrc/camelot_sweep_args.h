@@ -28,6 +28,7 @@ struct SweepArgs {
     Slot *result;                     // exact local best
     long long *keys;                  // packed key (NCCL transport)
     unsigned tabL_bytes;              // leaf-stage table rows staged in shared memory (0: read global)
+    int bp_min_nqs;                   // quota breakpoints only for sub-grids of >= this many quotas
 };
 
 }  // namespace cam

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "../../include/camelot.h"
@@ -33,6 +34,13 @@ cudaError_t launch_ns(const DevProb &P, const SweepArgs &A, int dev, cudaStream_
             gg = std::max(1, std::min(4096, per * nsm));
         }
         grid = gg;
+    }
+    // small scans (the coarsest cascade level): at most one work item per warp -- idle
+    // CTAs only add to the end-of-kernel reduction (testing knob CAMELOT_SWEEP_FIT=0)
+    static const bool fit = !(getenv("CAMELOT_SWEEP_FIT") && getenv("CAMELOT_SWEEP_FIT")[0] == '0');
+    if (fit) {
+        const unsigned long long per_cta = SWEEP_THREADS / 32;
+        grid = (int)std::max(1ull, std::min((unsigned long long)grid, (A.n_items + per_cta - 1) / per_cta));
     }
     sweep_kernel<8, NS, POL, TWO, COMM><<<grid, SWEEP_THREADS, A.tabL_bytes, st>>>(P, A);
     return cudaGetLastError();
