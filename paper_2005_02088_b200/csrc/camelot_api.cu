@@ -633,7 +633,11 @@ int sweep_pass(const Ctx &X, int dev, int policy, int nlev, const Slot *inc, Slo
         A.g_lo = 0;
         A.n_gp = ngp;
     }
-    A.n_items = A.gpack == 1 ? A.n_gp * (unsigned long long)A.nchunk
+    {   // chunks per work item (testing knob CAMELOT_SWEEP_CPG): the grandparent is placed once per item
+        const int cpg = getenv("CAMELOT_SWEEP_CPG") ? std::max(1, atoi(getenv("CAMELOT_SWEEP_CPG"))) : 4;
+        A.ngroups = A.gpack == 1 ? (A.nchunk + cpg - 1) / cpg : 1;
+    }
+    A.n_items = A.gpack == 1 ? A.n_gp * (unsigned long long)A.ngroups
                              : (A.n_gp + (unsigned long long)A.gpack - 1) / (unsigned long long)A.gpack;
     A.lam = reinterpret_cast<const float *>(ws + X.L.lam);
     A.y = reinterpret_cast<const int *>(ws + X.L.y);

@@ -279,6 +279,12 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
     __shared__ unsigned long long red_c[SWEEP_THREADS / 32][2];
     __shared__ unsigned red_v[SWEEP_THREADS / 32];
     __shared__ int is_last;
+    // per warp: the grandparent's placement state, shared by the chunks of a work item
+    struct GSave {
+        SwState<CM, NS> st;
+        float dur[NS], bwv[NS], ntv[NS];
+    };
+    __shared__ GSave gsave[SWEEP_THREADS / 32];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     // NS == n for n <= 6 (the host dispatches exact widths), so stage guards fold away
     const int n = NS <= 6 ? NS : P.n;
@@ -338,15 +344,17 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
         const int lg = gpk == 1 ? 0 : lane / Os;   // this lane's grandparent in the item
         bool lane_ok = true;
         unsigned long long gp;
-        int ch;
+        int c_begin = 0, c_end = 1;   // this item's parent chunks (32 parents each)
         if (gpk == 1) {
-            gp = A.g_lo + it / (unsigned)A.nchunk;
-            ch = (int)(it % (unsigned)A.nchunk);
+            const unsigned ng = (unsigned)A.ngroups;
+            gp = A.g_lo + it / ng;
+            const int grp = (int)(it % ng);
+            c_begin = grp * A.nchunk / A.ngroups;
+            c_end = (grp + 1) * A.nchunk / A.ngroups;
         } else {
             const unsigned long long g0 = it * (unsigned long long)gpk + (unsigned long long)lg;
             lane_ok = lg < gpk && g0 < A.n_gp;
             gp = A.g_lo + (lane_ok ? g0 : 0ull);
-            ch = 0;
         }
         // bound: the best objective key found anywhere so far (a feasible candidate), so a
         // leaf whose key bound is strictly worse cannot win (skips only the divisions)
@@ -372,6 +380,10 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
             }
             beta[0] = bc;
         }
+        SwState<CM, NS> st;
+        float dur[NS], bwv[NS], ntv[NS];
+        bool gok = lane_ok;   // the grandparent's stages fit (uniform when gpack == 1)
+        for (int ch = c_begin; ch < c_end; ++ch) {
         // ---- parent (per lane): option of stage n-2, its canonical index and range
         const int ops = gpk == 1 ? ch * 32 + lane : lane % Os;   // parent option in the (sub-)grid
         const int op = canon(min(ops, Os - 1));      // canonical option code
@@ -394,15 +406,42 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
             act = ((item / 64ull) % (unsigned long long)A.world) == (unsigned long long)A.rank;
         }
         // ---- placement of stages 0..n-2: the grandparent's options (warp-uniform unless
-        // gpack > 1), then the lane's parent option.  A rolled loop (one copy of sw_place):
-        // this code runs once per work item, and unrolled it thrashed the instruction cache.
-        SwState<CM, NS> st;
-        sw_init<CM, NS>(P, st);
-        float dur[NS], bwv[NS], ntv[NS];
+        // gpack > 1; placed once per work item, saved in shared memory for its further
+        // chunks), then the lane's parent option.  A rolled loop (one copy of sw_place):
+        // this code runs once per chunk, and unrolled it thrashed the instruction cache.
+        int i0 = 0;
+        if (ch > c_begin) {
+            __syncwarp();   // lane 0's save is visible
+            st = gsave[wid].st;
 #pragma unroll
-        for (int i = 0; i < NS; ++i) dur[i] = bwv[i] = ntv[i] = 0.0f;
+            for (int i = 0; i < NS; ++i) {
+                dur[i] = gsave[wid].dur[i];
+                bwv[i] = gsave[wid].bwv[i];
+                ntv[i] = gsave[wid].ntv[i];
+            }
+            i0 = n - 2;
+        } else {
+            sw_init<CM, NS>(P, st);
+#pragma unroll
+            for (int i = 0; i < NS; ++i) dur[i] = bwv[i] = ntv[i] = 0.0f;
+        }
 #pragma unroll 1
-        for (int i = 0; i <= n - 2 && act; ++i) {
+        for (int i = i0; i <= n - 2; ++i) {
+            if (i == n - 2) {
+                if (gpk == 1 && ch == c_begin && c_end - c_begin > 1 && gok && lane == 0) {
+                    gsave[wid].st = st;
+#pragma unroll
+                    for (int k = 0; k < NS; ++k) {
+                        gsave[wid].dur[k] = dur[k];
+                        gsave[wid].bwv[k] = bwv[k];
+                        gsave[wid].ntv[k] = ntv[k];
+                    }
+                }
+                act = act && gok;
+                if (!act) break;
+            } else if (!gok) {
+                break;
+            }
             int oi = op;
 #pragma unroll
             for (int k = 0; k < NS; ++k)
@@ -411,7 +450,9 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
             const int th = oi % nQ, N = oi / nQ + 1;
             const float4 e = __ldg(&P.tab[((size_t)i * P.nS + b) * nQ + th]);
             const uint32_t As = P.Am[i] * (uint32_t)P.S[b];
-            act = sw_place<CM, NS>(P, st, i, N, (int)(qpm_s[th] & 127u), qpm_s[th] >> 7, P.W[i], As, e.z);
+            const bool ok = sw_place<CM, NS>(P, st, i, N, (int)(qpm_s[th] & 127u), qpm_s[th] >> 7, P.W[i], As, e.z);
+            if (i < n - 2) gok = ok;
+            else act = ok;
             const float nt = __fmul_rn((float)N, e.y);
 #pragma unroll
             for (int k = 0; k < NS; ++k)
@@ -421,6 +462,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
                     ntv[k] = nt;
                 }
         }
+        if (gpk == 1 && !gok) break;   // the grandparent does not fit: no chunk of it has work (uniform)
         if (act) {
         // ---- leaf context: capacities, deployment order, bounds (per lane)
         const int bL = P.app[jl] ? beta[1] : beta[0];
@@ -653,8 +695,12 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
         }
         n_sc += c_sc;
         n_fe += c_fe;
-        if (bk < gkey) atomicMin(&A.hdr->best_obj, (unsigned int)bk);
+        if (bk < gkey) {
+            atomicMin(&A.hdr->best_obj, (unsigned int)bk);
+            gkey = bk;
+        }
         }   // act
+        }   // chunks of the item
     }
     // ---- reduction: lane -> warp -> CTA slot; the last CTA reduces the slots
     for (int off = 16; off; off >>= 1) {

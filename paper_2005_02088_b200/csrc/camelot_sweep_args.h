@@ -14,6 +14,8 @@ struct SweepArgs {
     unsigned long long g_lo;          // first grandparent
     unsigned long long n_items;       // grandparents x nchunk
     int nchunk;                       // ceil(Os / 32) parent chunks per grandparent
+    int ngroups;                      // work items per grandparent (gpack == 1): chunk ranges that
+                                      // share one placement of the grandparent
     int gpack;                        // grandparents per warp item: 1, or 32 / Os when Os <= 16
                                       // (lane = (grandparent, parent) pair; nchunk = 1)
     unsigned long long n_gp;          // grandparents in [g_lo, g_lo + n_gp) (bound for gpack > 1)
