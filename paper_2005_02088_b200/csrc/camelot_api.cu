@@ -637,7 +637,12 @@ int sweep_pass(const Ctx &X, int dev, int policy, int nlev, const Slot *inc, Slo
         const int cpg = getenv("CAMELOT_SWEEP_CPG") ? std::max(1, atoi(getenv("CAMELOT_SWEEP_CPG"))) : 4;
         A.ngroups = A.gpack == 1 ? (A.nchunk + cpg - 1) / cpg : 1;
     }
-    A.n_items = A.gpack == 1 ? A.n_gp * (unsigned long long)A.ngroups
+    // guided: the last eighth of the grandparents (the end of the dynamic queue) as
+    // single-chunk items, so that the tail of the scan is fine-grained
+    const unsigned long long tdiv = getenv("CAMELOT_SWEEP_TAIL") ? std::max(1, atoi(getenv("CAMELOT_SWEEP_TAIL"))) : 8;
+    A.gp_split = A.gpack == 1 && A.ngroups < A.nchunk ? A.n_gp - A.n_gp / tdiv : A.n_gp;
+    A.n_grp_items = A.gp_split * (unsigned long long)A.ngroups;
+    A.n_items = A.gpack == 1 ? A.n_grp_items + (A.n_gp - A.gp_split) * (unsigned long long)A.nchunk
                              : (A.n_gp + (unsigned long long)A.gpack - 1) / (unsigned long long)A.gpack;
     A.lam = reinterpret_cast<const float *>(ws + X.L.lam);
     A.y = reinterpret_cast<const int *>(ws + X.L.y);

@@ -345,12 +345,17 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MINB) sweep_kernel(const 
         bool lane_ok = true;
         unsigned long long gp;
         int c_begin = 0, c_end = 1;   // this item's parent chunks (32 parents each)
-        if (gpk == 1) {
+        if (gpk == 1 && it < A.n_grp_items) {
             const unsigned ng = (unsigned)A.ngroups;
             gp = A.g_lo + it / ng;
             const int grp = (int)(it % ng);
             c_begin = grp * A.nchunk / A.ngroups;
             c_end = (grp + 1) * A.nchunk / A.ngroups;
+        } else if (gpk == 1) {   // the tail: one chunk per item
+            const unsigned long long j = it - A.n_grp_items;
+            gp = A.g_lo + A.gp_split + j / (unsigned)A.nchunk;
+            c_begin = (int)(j % (unsigned)A.nchunk);
+            c_end = c_begin + 1;
         } else {
             const unsigned long long g0 = it * (unsigned long long)gpk + (unsigned long long)lg;
             lane_ok = lg < gpk && g0 < A.n_gp;

@@ -16,6 +16,8 @@ struct SweepArgs {
     int nchunk;                       // ceil(Os / 32) parent chunks per grandparent
     int ngroups;                      // work items per grandparent (gpack == 1): chunk ranges that
                                       // share one placement of the grandparent
+    unsigned long long gp_split;      // grandparents [0, gp_split) in ngroups items each, the rest
+    unsigned long long n_grp_items;   // (the tail of the scan) one item per chunk; = gp_split * ngroups
     int gpack;                        // grandparents per warp item: 1, or 32 / Os when Os <= 16
                                       // (lane = (grandparent, parent) pair; nchunk = 1)
     unsigned long long n_gp;          // grandparents in [g_lo, g_lo + n_gp) (bound for gpack > 1)
