@@ -208,6 +208,7 @@ def main():
     ap.add_argument("--no-comm", action="store_true", help="skip the NEXT-2 communication-aware leg")
     ap.add_argument("--no-sim", action="store_true", help="skip the NEXT-4 tail-simulation leg")
     ap.add_argument("--no-hard", action="store_true", help="skip the second C4 instance (C4b)")
+    ap.add_argument("--no-b200", action="store_true", help="skip C4 on the modeled-B200 cluster preset")
     ap.add_argument("--sa-chains", type=int, default=4096)
     ap.add_argument("--sa-iters", type=int, default=500)
     ap.add_argument("--flat-config", type=int, default=4, help="config of the flat scan (4 = C4)")
@@ -472,11 +473,11 @@ def main():
                              "frac": fach / peak, "ops_per_eval": fops,
                              "note": "per GPU: leaf evaluations x ops_per_eval / sweep kernel time"}}
 
-    # a second C4 instance where pruning is harder (other draws, QoS 0.8x): C4b
-    hard = None
-    if not args.no_hard:
-        log("C4b leg")
-        hp = G.config_problems(7)[0]
+    # further C4 instances, timed like the headline step (median / min):
+    #  * C4b: other draws, QoS 0.8x -- pruning is much harder;
+    #  * C4 on the modeled-B200 cluster preset (8 TB/s, 180 GiB per GPU; SURVEY.md 8(d):
+    #    "C4 is also run with b200") -- memory never binds.
+    def instance_leg(hp):
         hs = api.Session(hp, device=dev_idx, n_loads=1)
         hs.upload()
         for _ in range(3):
@@ -494,11 +495,20 @@ def main():
             hms.append(e0.elapsed_time(e1))
             hev.append(hm.n_evaluated + hr.n_evaluated)
         hmed = max_over_ranks(statistics.median(hms))
-        hard = {"problem": hp.name, "sha256": hp.sha256(), "ms_per_step_median": hmed,
+        return {"problem": hp.name, "sha256": hp.sha256(), "ms_per_step_median": hmed,
                 "ms_per_step_min": max_over_ranks(min(hms)),
                 "candidates_per_s": 2 * ntot_of(hp) / (hmed * 1e-3), "evals_per_step": statistics.median(hev),
                 "max_load": {"index": hm.index, "T": hm.objective},
                 "min_resource": {"index": hr.index, "gpus_used": hr.gpus_used, "quota_used": hr.quota_used}}
+
+    hard = b200 = None
+    if not args.no_hard:
+        log("C4b leg")
+        hard = instance_leg(G.config_problems(7)[0])
+    if not args.no_b200:
+        log("C4 b200-preset leg")
+        bp = G.config_problems(4, "b200")[0]
+        b200 = instance_leg(bp.with_(name=bp.name + "-b200"))
 
     # the paper's own solver (simulated annealing, NEXT-1) on the same device:
     # time and quality against the exact plans of this step
@@ -595,7 +605,7 @@ def main():
                           "min_resource": {"index": pr.index, "gpus_used": pr.gpus_used,
                                            "quota_used": pr.quota_used, "load": LOW_LOAD * pm.objective}},
                 "phases_ms": phases, "scored_per_step": evals, "gpu_launches": launches, "roofline": roof,
-                "flat_scan": flat, "c4b": hard, "sa_baseline": sa, "comm_qos": comm, "tail_sim": tail,
+                "flat_scan": flat, "c4b": hard, "c4_b200": b200, "sa_baseline": sa, "comm_qos": comm, "tail_sim": tail,
                 "clocks": clocks,
                 "e2e": e2e, "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)

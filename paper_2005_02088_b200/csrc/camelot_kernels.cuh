@@ -53,6 +53,7 @@ struct FilterSmem {
     int minNP[NMAX];
     int Qs[CAMELOT_MAX_QUOTAS];
     unsigned char oth[OMAX], oN[OMAX];        // option code -> (theta, N) (no divisions in the rounds)
+    unsigned char ongrid[CAMELOT_MAX_QUOTAS]; // quota theta is on the level's sub-grid
     unsigned char qpass[NMAX][CAMELOT_MAX_QUOTAS];   // (stage, quota): the duration passes the QoS bound
     long long ulim[NMAX];                     // per stage: largest N p passing the quota bounds
 };
@@ -88,6 +89,7 @@ CAM_DEVFN void filter_body(const DevProb &P, const FilterArgs &F, int b, FilterS
         fsm.oth[o] = (unsigned char)(o % nQ);
         fsm.oN[o] = (unsigned char)(o / nQ + 1);
     }
+    for (int q = tid; q < nQ; q += blockDim.x) fsm.ongrid[q] = F.stride <= 1 || ((nQ - 1 - q) % F.stride) == 0;
     mbar_wait(bar, phase & 1u);
     ++phase;
     __syncthreads();
@@ -107,13 +109,13 @@ CAM_DEVFN void filter_body(const DevProb &P, const FilterArgs &F, int b, FilterS
             lam_min[a] = m;
         }
     // static conditions
+    const uint32_t Sb = (uint32_t)P.S[b];
     for (int i = 0; i < n; ++i)
     for (int o = tid; o < O; o += blockDim.x) {
         const int th = fsm.oth[o], N = fsm.oN[o];
         const float4 e = tabs[i * nQ + th];
-        const uint32_t As = P.Am[i] * (uint32_t)P.S[b];
-        bool k = true;
-        if (F.stride > 1 && ((nQ - 1 - th) % F.stride) != 0) k = false;
+        const uint32_t As = P.Am[i] * Sb;
+        bool k = fsm.ongrid[th];
         if (F.prune) {
             if (P.W[i] + As > P.FM) k = false;                 // one replica fits no GPU
             if (cap && e.z > P.BW) k = false;

@@ -19,7 +19,11 @@ the CUDA path.
     of its own 10% sub-grid problem (C4b restricted to quotas 10..100, the same
     table entries), each re-scored in C4b; for min-resource at the C4b load.
 
-    python tests/golden/make_c4_expected.py [threads] [--no-slices] [--c4b]
+  * --b200: C4 on the modeled-B200 cluster preset (gen PRESETS["b200"]: 8 TB/s,
+    180 GiB per GPU), full space, both policies, by O7 with the same 10%
+    sub-grid incumbents ("C4 is also run with b200").
+
+    python tests/golden/make_c4_expected.py [threads] [--no-slices] [--c4b | --b200]
 """
 import json
 import os
@@ -117,17 +121,19 @@ def sub_grid(prob):
                       table=prob.table[:, :, sub, :].copy()), sub
 
 
-def main_c4b(threads):
-    p = G.config_problems(7)[0]
+def main_c4b(threads, config=7, preset="v100-dgx2", out="expected_C4b-full.json"):
+    p = G.config_problems(config, preset)[0]
+    if preset != "v100-dgx2":
+        p = p.with_(name=f"{p.name}-{preset}")
     pr, sub = sub_grid(p)
 
     def to_full(x):
         beta, rho, theta = O.decode(pr, x)
         return O.encode(p, beta, rho, [sub[t] for t in theta])
 
-    rec = dict(problem=p.name, sha256=p.sha256(), ntot=O.ntot(p), threads=threads,
-               note="written by tests/golden/make_c4_expected.py --c4b (oracle only: O7 with incumbents from the "
-                    "plain scan of the 10% sub-grid)")
+    rec = dict(problem=p.name, sha256=p.sha256(), ntot=O.ntot(p), threads=threads, preset=preset,
+               note="written by tests/golden/make_c4_expected.py --c4b / --b200 (oracle only: O7 with incumbents "
+                    "from the plain scan of the 10% sub-grid)")
     t = time.time()
     r = O.search(pr, threads=threads)[0]
     xi = to_full(r.index)
@@ -148,7 +154,7 @@ def main_c4b(threads):
                                                            source="10% sub-grid min-resource optimum"),
                                **best_dict(br, time.time() - t))
     print("min_resource", rec["min_resource"], flush=True)
-    with open(os.path.join(HERE, "expected_C4b-full.json"), "w") as f:
+    with open(os.path.join(HERE, out), "w") as f:
         json.dump(rec, f, indent=1)
 
 
@@ -156,5 +162,7 @@ if __name__ == "__main__":
     args = [a for a in sys.argv[1:] if not a.startswith("--")]
     if "--c4b" in sys.argv:
         main_c4b(int(args[0]) if args else os.cpu_count())
+    elif "--b200" in sys.argv:   # C4 on the modeled-B200 preset ("C4 is also run with b200")
+        main_c4b(int(args[0]) if args else os.cpu_count(), config=4, preset="b200", out="expected_C4-b200-full.json")
     else:
         main(int(args[0]) if args else os.cpu_count(), slices="--no-slices" not in sys.argv)

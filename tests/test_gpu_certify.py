@@ -313,3 +313,24 @@ def test_c4b_full_golden(api, oracle):
     pr = s.plan_min_resource(lam)[0]
     g = e["min_resource"]
     assert pr.index == g["index"] and (pr.gpus_used, pr.quota_used) == (g["u"], g["U"])
+
+
+def test_c4_b200_preset_full_golden(api, oracle):
+    """C4 on the modeled-B200 cluster preset (8 TB/s, 180 GiB per GPU; SURVEY.md 8(d):
+    "C4 is also run with b200"), both policies through camelot_plan_max_then_min
+    (the bench's call), == O7."""
+    path = os.path.join(GOLD, "expected_C4-b200-full.json")
+    if not os.path.exists(path):
+        pytest.skip("golden not generated (tests/golden/make_c4_expected.py --b200)")
+    e = json.load(open(path))
+    p = G.config_problems(4, "b200")[0]
+    prob = p.with_(name=p.name + "-b200")
+    assert prob.sha256() == e["sha256"]
+    s = api.Session(prob, n_loads=1)
+    pm, pr = s.plan_max_then_min(0.3)
+    g = e["max_load"]
+    assert pm.index == g["index"] and fb(pm.objective) == fb(g["T"])
+    g = e["min_resource"]
+    assert pr.index == g["index"] and (pr.gpus_used, pr.quota_used) == (g["u"], g["U"])
+    sc = oracle.score(prob, pr.index, loads=e["min_resource"]["loads"])
+    assert sc.level_verdict == [0]
