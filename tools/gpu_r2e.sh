@@ -7,8 +7,8 @@ tail -2 gpurun_out/pytest_gpu.log
 timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_n1.json 2> gpurun_out/bench_n1.err; echo bench1=$?
 python -c "
 import json;d=json.loads(open('gpurun_out/bench_n1.json').read().strip().splitlines()[-1])
-print('step', d['ms_per_step'], d['ms_per_step_median'], 'flat', d['flat_scan']['ms'], d['flat_scan']['roofline']['frac'], 'c4b', d['c4b']['ms_per_step_median'], 'e2e', d['e2e']['ms_per_step'])"
-timeout 600 python bench.py --gpus 2 --steps 5 --warmup 3 --no-cpu-baseline --no-sa --no-comm --no-sim > gpurun_out/bench_n2.json 2> gpurun_out/bench_n2.err; echo bench2=$?
+print('step', d['ms_per_step'], d['ms_per_step_median'], 'flat', d['flat_scan']['ms'], d['flat_scan']['roofline']['frac'], 'c4b', d['c4b']['ms_per_step_median'], 'e2e', d['e2e']['ms_per_step'], 'b200', d['c4_b200']['ms_per_step_median'])"
+timeout 600 python bench.py --gpus 2 --steps 5 --warmup 3 --no-cpu-baseline --no-sa --no-comm --no-sim --no-hard --no-b200 > gpurun_out/bench_n2.json 2> gpurun_out/bench_n2.err; echo bench2=$?
 cut -c1-300 gpurun_out/bench_n2.json
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/prof/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-flat --no-hard --no-sa --no-comm --no-sim > gpurun_out/prof/launch_bench.log 2>&1; echo ncu1=$?
 timeout 900 ncu -f --set full --clock-control none --import-source on -k regex:search_level -s 2 -c 2 -o /tmp/search_full python tools/pair_step.py 4 2 > gpurun_out/prof/ncu_full.log 2>&1; echo ncu2=$?
