@@ -831,7 +831,7 @@ __device__ __forceinline__ void level_body(const DevProb &P, const LevelArgs &LA
         unsigned long long *mbar = reinterpret_cast<unsigned long long *>(smem_raw + level_fixed_bytes<CM>());
         OptRec *rec_s = reinterpret_cast<OptRec *>(smem_raw + level_fixed_bytes<CM>() + 16);
         const int nl = P.n * P.nS;
-        if (threadIdx.x == 0) {
+        if (LA.rec_budget > 0 && threadIdx.x == 0) {   // (staging is opt-in: skip the serial scan when off)
             int acc = 0;
             for (int q = 0; q < nl; ++q) {
                 recoff[q] = acc;
@@ -839,8 +839,8 @@ __device__ __forceinline__ void level_body(const DevProb &P, const LevelArgs &LA
             }
             recoff[nl] = acc;
         }
-        __syncthreads();
-        const unsigned long long bytes = (unsigned long long)recoff[nl] * sizeof(OptRec);
+        if (LA.rec_budget > 0) __syncthreads();
+        const unsigned long long bytes = LA.rec_budget > 0 ? (unsigned long long)recoff[nl] * sizeof(OptRec) : 0ull;
         if (bytes > 0 && bytes <= LA.rec_budget) {
             if (threadIdx.x == 0) {
                 fence_proxy_async();   // the filter's generic stores (before the grid barrier) -> async reads
