@@ -233,9 +233,11 @@ int camelot_plan_min_resource(const camelot_problem *p, const camelot_cluster *c
  * (Eq. 3) at load_a = fl32(low_load_frac * T*) for every application a, T* =
  * out[0].objective (the float64 product rounded to binary32, as a host caller
  * computing it in double would).  The load is derived ON THE DEVICE from the
- * max-load winner, so the two exact searches run back to back on exec->stream
- * with one host synchronisation at the end (no host round trip between the
- * policies).  No feasible peak: out[1] is INFEASIBLE with violations = V_LOAD
+ * max-load winner's objective key, so the two exact searches run back to back on
+ * exec->stream with one host synchronisation at the end (no host round trip
+ * between the policies); the max-load plan itself is scored on an internal second
+ * stream of the calling thread while the min-resource search runs, and exec->stream
+ * waits for it (an event) before the plans are copied out.  No feasible peak: out[1] is INFEASIBLE with violations = V_LOAD
  * (the min-resource search then runs at load +inf and finds nothing).  Same result
  * as camelot_plan_max_load followed by camelot_plan_min_resource at that load.
  * low_load_frac in (0, 1]; world must be 1; out: host [2].  Returns CAMELOT_OK
