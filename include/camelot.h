@@ -154,7 +154,9 @@ typedef struct {
  * by rank c mod world); index_lo/index_hi restrict the search to canonical
  * indices [lo, hi) (0,0 = the whole space). */
 #define CAMELOT_EXEC_RESIDENT 1u  /* the workspace already holds this problem
-                                     (camelot_upload): skip the host->device copy */
+                                     (camelot_upload): skip the host->device copy
+                                     and the host scan of the table values (the
+                                     uploaded image was validated) */
 #define CAMELOT_EXEC_NAIVE 2u     /* use the un-hoisted thread-per-candidate scan
                                      (baseline; always used for PAPER_GLOBAL or n = 1) */
 typedef struct {

@@ -100,7 +100,7 @@ struct Dims {
     unsigned long long ntot;
 };
 
-int check_problem(const camelot_problem *p, const camelot_cluster *c, Dims &d) {
+int check_problem(const camelot_problem *p, const camelot_cluster *c, Dims &d, bool check_table = true) {
     if (!p || !c) return fail(CAMELOT_EINVAL, "null problem or cluster");
     if (p->n_apps < 1 || p->n_apps > CAMELOT_MAX_APPS) return fail(CAMELOT_EINVAL, "n_apps must be 1 or 2");
     if (p->n_stages < 1 || p->n_stages > CAMELOT_MAX_STAGES) return fail(CAMELOT_EINVAL, "n_stages must be in 1..8");
@@ -148,7 +148,9 @@ int check_problem(const camelot_problem *p, const camelot_cluster *c, Dims &d) {
         return fail(CAMELOT_EINVAL, "every application needs at least one stage");
     for (int a = 0; a < p->n_apps; ++a)
         if (!(p->qos_ms[a] > 0.0f) || !std::isfinite(p->qos_ms[a])) return fail(CAMELOT_EINVAL, "qos_ms[%d] must be > 0", a);
-    const size_t ne = (size_t)p->n_stages * p->n_batch * p->n_quota;
+    // (the table values are only read when they are uploaded: a RESIDENT call reuses the
+    // image that camelot_upload validated)
+    const size_t ne = check_table ? (size_t)p->n_stages * p->n_batch * p->n_quota : 0;
     for (size_t e = 0; e < ne; ++e) {
         const float *t = p->table + 4 * e;
         if (!std::isfinite(t[0]) || !std::isfinite(t[1]) || !std::isfinite(t[2]))
@@ -349,7 +351,7 @@ int choose_d0(const Dims &d) {
 }
 
 int setup(const camelot_problem *p, const camelot_cluster *c, const camelot_exec *ex, int nlev, Ctx &X, bool upload) {
-    int rc = check_problem(p, c, X.d);
+    int rc = check_problem(p, c, X.d, !(ex && (ex->exec_flags & CAMELOT_EXEC_RESIDENT)));
     if (rc) return rc;
     rc = device_ok(ex);
     if (rc) return rc;
