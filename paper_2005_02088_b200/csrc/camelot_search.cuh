@@ -76,6 +76,7 @@ struct SearchArgs {
     unsigned long long out_cap;
     unsigned long long *head;   // pop counter of this pass
     int xshift;                 // index >> xshift fits 32 bits (tie pruning key)
+    int tmode_min16;            // thread-per-parent mode from count >= tmode_min16 / 16 x resident warps
     // fused reduction (last pass): the last CTA reduces all slots
     int reduce_last;
     Slot *result;               // [nlev] exact local best
@@ -1332,7 +1333,7 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
     int G = 1;
     while (G < 8 && count * (unsigned long long)(2 * G) <= 32ull * nwarps) G *= 2;
     if (leafp) G = max(G, maxc <= 32 ? 1 : maxc <= 64 ? 2 : 4);
-    const bool tmode = S.prune && have_in && split == 1 && count >= 2ull * nwarps && !getenv_tmode_off() &&
+    const bool tmode = S.prune && have_in && split == 1 && 16ull * count >= (unsigned long long)S.tmode_min16 * nwarps && !getenv_tmode_off() &&
                        ((leafp && maxc <= 128) ||
                         (S.flevel == jtop + 1 && maxc <= 32 && count * (unsigned long long)maxc <= S.out_cap));
     const unsigned grab = tmode ? 32u / (unsigned)G : screen ? 8u : (unsigned)S.grab;
