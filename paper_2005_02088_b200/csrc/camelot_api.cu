@@ -390,16 +390,21 @@ int launch_search(const Ctx &X, const SearchArgs &S, int grid) {
     return CAMELOT_OK;
 }
 
+#ifdef CAMELOT_SHARED_POLICY
+#define CAM_POL(p) 2
+#else
+#define CAM_POL(p) (p)
+#endif
 #define CAM_DISPATCH(FN, ...)                                                                          \
     do {                                                                                               \
         const int cm_ = cm_bucket(X.d.C), ns_ = ns_bucket(X.d.n);                                      \
-        if (cm_ == 4 && ns_ == 4) return policy ? FN<4, 4, 1>(__VA_ARGS__) : FN<4, 4, 0>(__VA_ARGS__); \
-        if (cm_ == 4 && ns_ == 6) return policy ? FN<4, 6, 1>(__VA_ARGS__) : FN<4, 6, 0>(__VA_ARGS__); \
-        if (cm_ == 4) return policy ? FN<4, 8, 1>(__VA_ARGS__) : FN<4, 8, 0>(__VA_ARGS__);             \
-        if (cm_ == 8 && ns_ == 4) return policy ? FN<8, 4, 1>(__VA_ARGS__) : FN<8, 4, 0>(__VA_ARGS__); \
-        if (cm_ == 8 && ns_ == 6) return policy ? FN<8, 6, 1>(__VA_ARGS__) : FN<8, 6, 0>(__VA_ARGS__); \
-        if (cm_ == 8) return policy ? FN<8, 8, 1>(__VA_ARGS__) : FN<8, 8, 0>(__VA_ARGS__);             \
-        return policy ? FN<16, 8, 1>(__VA_ARGS__) : FN<16, 8, 0>(__VA_ARGS__);                         \
+        if (cm_ == 4 && ns_ == 4) return policy ? FN<4, 4, CAM_POL(1)>(__VA_ARGS__) : FN<4, 4, CAM_POL(0)>(__VA_ARGS__); \
+        if (cm_ == 4 && ns_ == 6) return policy ? FN<4, 6, CAM_POL(1)>(__VA_ARGS__) : FN<4, 6, CAM_POL(0)>(__VA_ARGS__); \
+        if (cm_ == 4) return policy ? FN<4, 8, CAM_POL(1)>(__VA_ARGS__) : FN<4, 8, CAM_POL(0)>(__VA_ARGS__);             \
+        if (cm_ == 8 && ns_ == 4) return policy ? FN<8, 4, CAM_POL(1)>(__VA_ARGS__) : FN<8, 4, CAM_POL(0)>(__VA_ARGS__); \
+        if (cm_ == 8 && ns_ == 6) return policy ? FN<8, 6, CAM_POL(1)>(__VA_ARGS__) : FN<8, 6, CAM_POL(0)>(__VA_ARGS__); \
+        if (cm_ == 8) return policy ? FN<8, 8, CAM_POL(1)>(__VA_ARGS__) : FN<8, 8, CAM_POL(0)>(__VA_ARGS__);             \
+        return policy ? FN<16, 8, CAM_POL(1)>(__VA_ARGS__) : FN<16, 8, CAM_POL(0)>(__VA_ARGS__);                         \
     } while (0)
 
 // staged option lists (TMA bulk copy of the level's compacted lists into every CTA's

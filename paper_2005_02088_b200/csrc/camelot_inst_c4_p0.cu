@@ -3,7 +3,13 @@
 #include "camelot_inst.cuh"
 
 namespace cam {
+#ifdef CAMELOT_SHARED_POLICY   // one instantiation serves both policies (policy = runtime argument)
+CAMELOT_INSTANTIATE(4, 4, 2)
+CAMELOT_INSTANTIATE(4, 6, 2)
+CAMELOT_INSTANTIATE(4, 8, 2)
+#else
 CAMELOT_INSTANTIATE(4, 4, 0)
 CAMELOT_INSTANTIATE(4, 6, 0)
 CAMELOT_INSTANTIATE(4, 8, 0)
+#endif
 }  // namespace cam

@@ -3,7 +3,9 @@
 #include "camelot_inst.cuh"
 
 namespace cam {
+#ifndef CAMELOT_SHARED_POLICY
 CAMELOT_INSTANTIATE(4, 4, 1)
 CAMELOT_INSTANTIATE(4, 6, 1)
 CAMELOT_INSTANTIATE(4, 8, 1)
+#endif
 }  // namespace cam

@@ -3,5 +3,9 @@
 #include "camelot_inst.cuh"
 
 namespace cam {
+#ifdef CAMELOT_SHARED_POLICY   // one instantiation serves both policies (policy = runtime argument)
+CAMELOT_INSTANTIATE(8, 6, 2)
+#else
 CAMELOT_INSTANTIATE(8, 6, 0)
+#endif
 }  // namespace cam

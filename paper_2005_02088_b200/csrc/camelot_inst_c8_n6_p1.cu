@@ -3,5 +3,7 @@
 #include "camelot_inst.cuh"
 
 namespace cam {
+#ifndef CAMELOT_SHARED_POLICY
 CAMELOT_INSTANTIATE(8, 6, 1)
+#endif
 }  // namespace cam

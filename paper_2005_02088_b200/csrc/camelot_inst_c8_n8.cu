@@ -3,6 +3,10 @@
 #include "camelot_inst.cuh"
 
 namespace cam {
+#ifdef CAMELOT_SHARED_POLICY   // one instantiation serves both policies (policy = runtime argument)
+CAMELOT_INSTANTIATE(8, 8, 2)
+#else
 CAMELOT_INSTANTIATE(8, 8, 0)
 CAMELOT_INSTANTIATE(8, 8, 1)
+#endif
 }  // namespace cam

@@ -708,6 +708,7 @@ template <int POLICY, int NS, typename NtF>
 __device__ __forceinline__ void score_leaf(const DevProb &P, const SearchArgs &S, WarpBest *wb, int lane, bool inr,
                                            bool placed, const float *lsum, const float *kap, NtF nt, float tub,
                                            int u, int U, int bc, unsigned long long x, Counters &cn) {
+    const int pol = POLICY == 2 ? S.policy : POLICY;   // 2: the policy is a runtime argument (shared code)
     cn.scored += inr;
     bool feas = inr && placed;
     if (feas) {
@@ -718,7 +719,7 @@ __device__ __forceinline__ void score_leaf(const DevProb &P, const SearchArgs &S
     }
     cn.feasible += feas;
     const int n = P.n;
-    if (POLICY == 0) {
+    if (pol == 0) {
         unsigned long long key = 0xFFFFFFFFull;
         if (feas) {
             // T <= min_i fl(N_i thr_i): the divisions only when it can win
@@ -1069,6 +1070,7 @@ template <int CM, int NS, int POLICY>
 __device__ __forceinline__ void thread_chunk(const DevProb &P, const SearchArgs &S, const Frontier<CM> &in,
                                           const Frontier<CM> &outf, unsigned long long e0, unsigned live, int j,
                                           WarpBest *wb, int lane, Counters &cn, int G) {
+    const int pol = POLICY == 2 ? S.policy : POLICY;   // 2: the policy is a runtime argument (shared code)
     // G lanes per parent (G > 1 only for leaf passes): lane l takes parent e0 + l / G
     // and its children sub, sub + G, ... (sub = l % G)
     const int n = P.n, nlev = S.nlev;
@@ -1091,13 +1093,13 @@ __device__ __forceinline__ void thread_chunk(const DevProb &P, const SearchArgs 
         bool go_node = mine;
         if (go_node) {
             unsigned long long kl;
-            if (POLICY == 0) kl = objkey_maxload(fminf(c.tub, fminf(sb_at(P, S, j, bj).maxNT, c.restT)));
+            if (pol == 0) kl = objkey_maxload(fminf(c.tub, fminf(sb_at(P, S, j, bj).maxNT, c.restT)));
             else {
                 const int Ulb = c.U + (int)sb_at(P, S, j, bj).minNP + c.restU;
                 kl = objkey_minres(max(c.u, (Ulb + P.R - 1) / P.R), Ulb);
             }
             go_node = can_win(kl, c.x * P.opow[n - j], wb, nlev, S.xshift);
-            if (POLICY == 1 && P.A == 1 && c.tub < wb->lmin) go_node = false;
+            if (pol == 1 && P.A == 1 && c.tub < wb->lmin) go_node = false;
         }
         const int cnt = go_node ? (int)sb_at(P, S, j, bj).cnt : 0;
         const OptRec *list = list_of(P, S, j, bj);
@@ -1127,7 +1129,7 @@ __device__ __forceinline__ void thread_chunk(const DevProb &P, const SearchArgs 
             bool go = valid;
             if (go) {
                 unsigned long long kl;
-                if (POLICY == 0) {
+                if (pol == 0) {
                     const float t = leaf ? fminf(c.tub, r.NT) : fminf(fminf(c.tub, r.NT), c.restT);
                     kl = objkey_maxload(t);
                 } else {
@@ -1135,7 +1137,7 @@ __device__ __forceinline__ void thread_chunk(const DevProb &P, const SearchArgs 
                     kl = objkey_minres(max(c.u, (Ulb + P.R - 1) / P.R), Ulb);
                 }
                 go = can_win(kl, x * span, wb, nlev, S.xshift);
-                if (go && leaf && POLICY == 0) go = kl < bk || (kl == bk && x < bx);   // the lane's own best
+                if (go && leaf && pol == 0) go = kl < bk || (kl == bk && x < bx);   // the lane's own best
                 if (go && !leaf && c.rqsum - (int)r.NP < c.restU) go = false;
             }
             if (go && !(P.flags & F_COMM)) {
@@ -1167,7 +1169,7 @@ __device__ __forceinline__ void thread_chunk(const DevProb &P, const SearchArgs 
                 }
                 cn.feasible += feas;
                 if (!feas) continue;
-                if (POLICY == 0) {
+                if (pol == 0) {
                     if (bk < 0xFFFFFFFFull) {
                         const float Tb = __uint_as_float(0xFFFFFFFFu - (unsigned)bk);
                         if (t_certainly_below<NS>(P, n - 1, fe.kap, ntf, Tb)) continue;
@@ -1208,12 +1210,12 @@ __device__ __forceinline__ void thread_chunk(const DevProb &P, const SearchArgs 
             if (sv) {
                 sv &= fe.lsum[0] <= P.qos[0];
                 if (P.A > 1) sv &= fe.lsum[1] <= P.qos[1];
-                if (sv && POLICY == 0 && wb->bound < 0xFFFFFFFFull) {
+                if (sv && pol == 0 && wb->bound < 0xFFFFFFFFull) {
                     const float Tbest = __uint_as_float(0xFFFFFFFFu - (unsigned)wb->bound);
                     if (t_certainly_below<NS>(P, j, fe.kap, ntf, Tbest)) sv = false;
                 }
-                if (sv && POLICY == 1 && P.A == 1 && t_certainly_below<NS>(P, j, fe.kap, ntf, wb->lmin)) sv = false;
-                if (sv && POLICY == 1) {
+                if (sv && pol == 1 && P.A == 1 && t_certainly_below<NS>(P, j, fe.kap, ntf, wb->lmin)) sv = false;
+                if (sv && pol == 1) {
                     const int Ulb = fe.U + c.restU;
                     sv = (unsigned long long)objkey_minres(max(fe.u, (Ulb + P.R - 1) / P.R), Ulb) <= wb->bound;
                 }
@@ -1288,6 +1290,7 @@ __device__ __forceinline__ void thread_chunk(const DevProb &P, const SearchArgs 
 template <int CM, int NS, int POLICY>
 __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S, Node<CM> *stack, WarpCtl *ctl,
                                           WarpBest *wb, int lane, Counters &cn) {
+    const int pol = POLICY == 2 ? S.policy : POLICY;   // 2: the policy is a runtime argument (shared code)
     const int nlev = S.nlev;
     const int n = P.n;
     const int jtop = S.level;
@@ -1425,7 +1428,7 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
                 }
                 const StageBound &bj = sb_at(P, S, jtop, bq[P.app[jtop]]);
                 unsigned long long kl;
-                if (POLICY == 0) kl = objkey_maxload(fminf(tq, fminf(bj.maxNT, rT)));
+                if (pol == 0) kl = objkey_maxload(fminf(tq, fminf(bj.maxNT, rT)));
                 else {
                     const int Ulb = Uq + (int)bj.minNP + rU;
                     kl = objkey_minres(max(uq, (Ulb + P.R - 1) / P.R), Ulb);
@@ -1513,14 +1516,14 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
                     // re-check the node against the current bound (it may have tightened)
                     if (S.prune) {
                         unsigned long long kl;
-                        if (POLICY == 0) kl = objkey_maxload(fminf(c.tub, fminf(sb_at(P, S, j, bj).maxNT, c.restT)));
+                        if (pol == 0) kl = objkey_maxload(fminf(c.tub, fminf(sb_at(P, S, j, bj).maxNT, c.restT)));
                         else {
                             const int Ulb = c.U + (int)sb_at(P, S, j, bj).minNP + c.restU;
                             kl = objkey_minres(max(c.u, (Ulb + P.R - 1) / P.R), Ulb);
                         }
                         bool live = can_win(kl, c.x * P.opow[n - j], wb, nlev, S.xshift);
                         // T_i <= fl(N_i thr_i / kappa_i(now)) (kappa only grows): below the load floor -> dead
-                        if (POLICY == 1 && P.A == 1 && c.tub < wb->lmin) live = false;
+                        if (pol == 1 && P.A == 1 && c.tub < wb->lmin) live = false;
                         if (!live) {
                             __syncwarp();
                             if (lane == 0) {
@@ -1592,7 +1595,7 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
                 if (S.prune && go) {
                     // prune only when the subtree cannot hold the answer (ties by index)
                     unsigned long long kl;
-                    if (POLICY == 0) {
+                    if (pol == 0) {
                         const float t = leaf ? fminf(c.tub, r.NT) : fminf(fminf(c.tub, r.NT), c.restT);
                         kl = objkey_maxload(t);
                     } else {
@@ -1636,18 +1639,18 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
                 if (sv && S.prune) {
                     sv &= fe.lsum[0] <= P.qos[0];
                     if (P.A > 1) sv &= fe.lsum[1] <= P.qos[1];
-                    if (sv && POLICY == 0 && wb->bound < 0xFFFFFFFFull) {
+                    if (sv && pol == 0 && wb->bound < 0xFFFFFFFFull) {
                         const float Tbest = __uint_as_float(0xFFFFFFFFu - (unsigned)wb->bound);
                         const int jj = j;
                         auto ntf2 = [&](int i) { return i < jj ? c.nt[i] : r.NT; };
                         if (t_certainly_below<NS>(P, j, fe.kap, ntf2, Tbest)) sv = false;
                     }
-                    if (sv && POLICY == 1 && P.A == 1) {
+                    if (sv && pol == 1 && P.A == 1) {
                         const int jj = j;
                         auto ntf3 = [&](int i) { return i < jj ? c.nt[i] : r.NT; };
                         if (t_certainly_below<NS>(P, j, fe.kap, ntf3, wb->lmin)) sv = false;
                     }
-                    if (sv && POLICY == 1) {
+                    if (sv && pol == 1) {
                         const int Ulb = fe.U + c.restU;
                         sv = (unsigned long long)objkey_minres(max(fe.u, (Ulb + P.R - 1) / P.R), Ulb) <= wb->bound;
                     }
