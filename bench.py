@@ -38,6 +38,18 @@ WORKLOAD = "C4: 5-stage p1-c2-m2-c3-m1 pipeline, 8 modeled V100 (BW 897 GB/s), 1
            "batch 1..128 (pow2), <=4 replicas/stage; max-load then min-resource at 0.3*T*"
 LOW_LOAD = 0.3   # low load = 30% of the peak
 TRAFFIC_CSV = "r02_v10_ncu_search_raw.csv"   # committed ncu --set full capture of the search launches
+FLAT_CSV = "r02_v10_ncu_flat_raw.csv"        # committed ncu --set full capture of the flat sweep (same slice)
+
+
+def ncu_metric(name, key, launch=0):
+    """One metric of one launch of a committed ncu --page raw --csv capture (None if absent)."""
+    import csv
+    try:
+        rows = list(csv.reader(open(os.path.join(ROOT, "profiles", name))))
+        v = rows[2 + launch][rows[0].index(key)]
+        return float(v.replace(",", ""))
+    except (OSError, ValueError, IndexError):
+        return None
 
 
 def ncu_traffic(name, launches_per_step=None):
@@ -472,6 +484,16 @@ def main():
                 "roofline": {"bound": "alu", "achieved": fach, "peak": peak, "unit": "Tops/s",
                              "frac": fach / peak, "ops_per_eval": fops,
                              "note": "per GPU: leaf evaluations x ops_per_eval / sweep kernel time"}}
+        # SURVEY.md 8(d)'s issue-bound fraction: scored/s / (issue peak / measured thread-instructions
+        # per scored leaf), from the committed ncu capture of the same slice
+        ti = ncu_metric(FLAT_CSV, "thread_inst_executed")
+        ia = ncu_metric(FLAT_CSV, "smsp__issue_active.avg.pct_of_peak_sustained_active")
+        if ti and scored_all:
+            ipl = ti / (scored_all / world)
+            flat["issue"] = {"thread_instructions_per_leaf": ipl,
+                             "frac": (scored_all / world) / (kern * 1e-3) * ipl / (peak * 1e12),
+                             "issue_active_pct": ia, "source": "profiles/" + FLAT_CSV,
+                             "note": "leaves/s x measured thread-instructions per leaf / issue peak"}
 
     # further C4 instances, timed like the headline step (median / min):
     #  * C4b: other draws, QoS 0.8x -- pruning is much harder;
