@@ -852,17 +852,22 @@ std::vector<int> coarse_strides(const Ctx &X, int policy) {
 
 // local search (incumbent pass + main pass); leaves keys in X.L.keys (or d_keys) and the
 // exact local best in X.L.result
-int local_search(const Ctx &X, const camelot_exec *ex, int policy, int nlev, long long *d_keys) {
+// prologue_done: the incumbent slots, the Eq. 2 estimates and the cumulative counters
+// were already prepared on the stream (camelot_plan_max_then_min's bridge_kernel)
+int local_search(const Ctx &X, const camelot_exec *ex, int policy, int nlev, long long *d_keys,
+                 bool prologue_done = false) {
     const bool prune = !(X.P.flags & F_NO_FILTER);
     char *ws = X.ws;
     Slot *inc = reinterpret_cast<Slot *>(ws + X.L.inc);
     Slot *result = reinterpret_cast<Slot *>(ws + X.L.result);
     long long *keys = d_keys ? d_keys : reinterpret_cast<long long *>(ws + X.L.keys);
     // incumbent = none: key 0xFFFFFFFF, x = ~0
-    init_slots_kernel<<<1, 64, 0, X.st>>>(inc, nlev);
-    COUNT_LAUNCH();
-    CU(cudaGetLastError());
-    if (policy == 1) {
+    if (!prologue_done) {
+        init_slots_kernel<<<1, 64, 0, X.st>>>(inc, nlev);
+        COUNT_LAUNCH();
+        CU(cudaGetLastError());
+    }
+    if (policy == 1 && !prologue_done) {
         const int nb = X.d.nbc * nlev;
         eq2_kernel<<<(nb + 127) / 128, 128, 0, X.st>>>(X.P, reinterpret_cast<const float *>(ws + X.L.lam), nlev,
                                                       reinterpret_cast<int *>(ws + X.L.y));
@@ -873,7 +878,7 @@ int local_search(const Ctx &X, const camelot_exec *ex, int policy, int nlev, lon
     range_of(X, ex, lo, hi);
     int dev = ex->device;
     int rc;
-    {
+    if (!prologue_done) {
         DevHeader *hdr = reinterpret_cast<DevHeader *>(ws + X.L.hdr);
         CU(cudaMemsetAsync(&hdr->cum_scored, 0, 2 * sizeof(unsigned long long) + 2 * sizeof(unsigned int), X.st));
     }
@@ -1138,8 +1143,6 @@ int camelot_plan_max_then_min(const camelot_problem *p, const camelot_cluster *c
     // max-load search and its winner
     rc = local_search(X, ex, 0, 1, nullptr);
     if (rc) return rc;
-    rc = finalize_enqueue(X, ex, 0, 1, reinterpret_cast<const long long *>(X.ws + X.L.keys), dplans + 1, false);
-    if (rc) return rc;
     std::swap(t_ev, t_ev_spare);   // keep the max-load search's events
     if (t_side.dev != ex->device) {
         if (t_side.s) {
@@ -1157,9 +1160,15 @@ int camelot_plan_max_then_min(const camelot_problem *p, const camelot_cluster *c
     // stream while the min-resource search runs on this one
     Slot *side_w = reinterpret_cast<Slot *>(X.ws + X.L.side_w);
     DevHeader *side_h = reinterpret_cast<DevHeader *>(X.ws + X.L.side_h);
-    low_load_kernel<<<1, 64, 0, X.st>>>(X.P, reinterpret_cast<const Slot *>(X.ws + X.L.winner),
-                                        reinterpret_cast<const DevHeader *>(X.ws + X.L.hdr2), low_load_frac,
-                                        reinterpret_cast<float *>(X.ws + X.L.lam), side_w, side_h);
+    // one launch between the searches: resolve the max-load key, the low load, the snapshot
+    // for the max-load plan, and the min-resource search's prologue (bridge_kernel)
+    bridge_kernel<<<1, 256, 0, X.st>>>(X.P, reinterpret_cast<const long long *>(X.ws + X.L.keys),
+                                       reinterpret_cast<const Slot *>(X.ws + X.L.result),
+                                       reinterpret_cast<Slot *>(X.ws + X.L.winner), low_load_frac,
+                                       reinterpret_cast<float *>(X.ws + X.L.lam), side_w, side_h,
+                                       reinterpret_cast<const DevHeader *>(X.ws + X.L.hdr2),
+                                       reinterpret_cast<Slot *>(X.ws + X.L.inc), reinterpret_cast<int *>(X.ws + X.L.y),
+                                       reinterpret_cast<DevHeader *>(X.ws + X.L.hdr));
     COUNT_LAUNCH();
     CU(cudaGetLastError());
     CU(cudaEventRecord(t_side.fork, X.st));
@@ -1169,7 +1178,7 @@ int camelot_plan_max_then_min(const camelot_problem *p, const camelot_cluster *c
     COUNT_LAUNCH();
     CU(cudaGetLastError());
     CU(cudaEventRecord(t_side.join, t_side.s));
-    rc = local_search(X, ex, 1, 1, nullptr);
+    rc = local_search(X, ex, 1, 1, nullptr, true);
     if (!rc) rc = finalize_enqueue(X, ex, 1, 1, reinterpret_cast<const long long *>(X.ws + X.L.keys), dplans);
     CU(cudaStreamWaitEvent(X.st, t_side.join, 0));   // join the max-load plan (also on an error)
     if (rc) return rc;

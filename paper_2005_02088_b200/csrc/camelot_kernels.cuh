@@ -532,27 +532,59 @@ CAM_GLOBAL void __launch_bounds__(PLAN_THREADS) plan_kernel(const DevProb P, int
     plan_block(P, policy, winner[k], lam + k * P.A, hdr, out + k, ps);
 }
 
-// The low load of camelot_plan_max_then_min (low load = a fraction
-// of the peak): load_a = fl(frac * T*) for every application, T* the max-load
-// optimum (the binary32 rounding of the float64 product, as a host caller computing
-// frac * T* in double and storing it as float); +inf when there is no feasible peak
-// (every min-resource candidate then fails LOAD).  T* is read from the resolved
-// winner's objective key (0xFFFFFFFF - bits(T): the same binary32 T
-// the plan reports), so the min-resource search need not wait for the max-load
-// plan.  The kernel also snapshots the winner and the search counters (side_w,
-// side_h) for the max-load plan_kernel, which runs on a second stream meanwhile.
-CAM_GLOBAL void low_load_kernel(const DevProb P, const Slot *winner, const DevHeader *hdr2, double frac, float *lam,
-                                Slot *side_w, DevHeader *side_h) {
+// camelot_plan_max_then_min, between the two searches, in ONE launch (one CTA):
+//  * resolve the max-load key (world 1: resolve_kernel's rule);
+//  * the low load (low load = a fraction of the peak): load_a =
+//    fl(frac * T*) for every application, T* read from the winner's objective key
+//    (0xFFFFFFFF - bits(T): the same binary32 T the plan reports), the
+//    binary32 rounding of the float64 product (as a host caller computing frac * T* in
+//    double and storing it as float); +inf when there is no feasible peak (every
+//    min-resource candidate then fails LOAD);
+//  * a snapshot of the winner and the search counters for the max-load plan_kernel,
+//    which runs on a second stream while the min-resource search runs;
+//  * the min-resource search's prologue: no incumbent, the Eq. 2 estimates at the low
+//    load, the cumulative counters zeroed (init_slots_kernel, eq2_kernel, a memset).
+CAM_GLOBAL void bridge_kernel(const DevProb P, const long long *keys, const Slot *local, Slot *winner, double frac,
+                              float *lam, Slot *side_w, DevHeader *side_h, const DevHeader *hdr2, Slot *inc, int *y,
+                              DevHeader *hdr) {
+    __shared__ Slot w;
     const int t = threadIdx.x;
-    const Slot w = winner[0];
+    if (t == 0) {
+        const unsigned long long packed = (unsigned long long)keys[0] ^ 0x8000000000000000ull;
+        if (packed == ~0ull) {
+            w.key = 0xFFFFFFFFull;
+            w.x = ~0ull;
+        } else {
+            w.key = packed >> 32;
+            w.x = local[0].x;
+        }
+        winner[0] = w;
+        *side_w = w;
+        inc[0].key = 0xFFFFFFFFull;
+        inc[0].x = ~0ull;
+        hdr->cum_scored = 0;
+        hdr->cum_nodes = 0;
+        hdr->trace_n = 0;
+        hdr->trace_pad = 0;
+    }
+    __syncthreads();
     if (t < P.A) {
         const float T = __uint_as_float(0xFFFFFFFFu - (uint32_t)w.key);
         lam[t] = w.x != ~0ull ? __double2float_rn(frac * (double)T) : __int_as_float(0x7f800000);
     }
-    if (t == 0) *side_w = w;
     const uint32_t *src = reinterpret_cast<const uint32_t *>(hdr2);
     uint32_t *dst = reinterpret_cast<uint32_t *>(side_h);
     for (int q = t; q < (int)(offsetof(DevHeader, trace_n) / 4); q += blockDim.x) dst[q] = src[q];
+    __syncthreads();   // lam before the Eq. 2 estimates
+    for (int bc = t; bc < P.nbc; bc += blockDim.x) {
+        int beta[AMAX];
+        int r = bc;
+        for (int a = P.A - 1; a >= 0; --a) {
+            beta[a] = r % P.nS;
+            r /= P.nS;
+        }
+        y[bc] = eq2_gpus(P, beta, lam);
+    }
 }
 
 // Naive exhaustive search (kernel N5 as a search): one thread scores one
