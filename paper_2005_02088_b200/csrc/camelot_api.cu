@@ -946,7 +946,7 @@ int local_search(const Ctx &X, const camelot_exec *ex, int policy, int nlev, lon
 // resolve the reduced keys (+ chunk re-scan when sharded) and score the winners into
 // dplans[0..nlev) on the device; no host synchronisation when world == 1
 int finalize_enqueue(const Ctx &X, const camelot_exec *ex, int policy, int nlev, const long long *d_keys,
-                     camelot_plan *dplans, bool plan = true) {
+                     camelot_plan *dplans) {
     const bool prune = !(X.P.flags & F_NO_FILTER);
     char *ws = X.ws;
     Slot *winner = reinterpret_cast<Slot *>(ws + X.L.winner);
@@ -959,9 +959,11 @@ int finalize_enqueue(const Ctx &X, const camelot_exec *ex, int policy, int nlev,
     F.local = reinterpret_cast<const Slot *>(ws + X.L.result);
     F.winner = winner;
     F.rescan = rescan;
-    resolve_kernel<<<1, 64, 0, X.st>>>(X.P, F);
-    COUNT_LAUNCH();
-    CU(cudaGetLastError());
+    if (ex->world > 1) {   // (one rank: plan_kernel resolves the key itself)
+        resolve_kernel<<<1, 64, 0, X.st>>>(X.P, F);
+        COUNT_LAUNCH();
+        CU(cudaGetLastError());
+    }
     if (ex->world > 1 && X.d.ntot > (1ull << 32)) {
         std::vector<unsigned long long> rs(nlev);
         CU(cudaMemcpyAsync(rs.data(), rescan, nlev * sizeof(unsigned long long), cudaMemcpyDeviceToHost, X.st));
@@ -974,9 +976,9 @@ int finalize_enqueue(const Ctx &X, const camelot_exec *ex, int policy, int nlev,
             if (rc) return rc;
         }
     }
-    if (!plan) return CAMELOT_OK;
     plan_kernel<<<nlev, PLAN_THREADS, 0, X.st>>>(X.P, policy, nlev, winner, reinterpret_cast<const float *>(ws + X.L.lam),
-                                                   reinterpret_cast<const DevHeader *>(ws + X.L.hdr2), dplans);
+                                                   reinterpret_cast<const DevHeader *>(ws + X.L.hdr2), dplans,
+                                                   ex->world > 1 ? nullptr : d_keys, ex->world > 1 ? nullptr : F.local);
     COUNT_LAUNCH();
     CU(cudaGetLastError());
     return CAMELOT_OK;

@@ -524,12 +524,26 @@ CAM_DEVFN void plan_block(const DevProb &P, int policy, const Slot w, const floa
 }
 
 // One block per load level: plan_block of that level's winner.
-CAM_GLOBAL void __launch_bounds__(PLAN_THREADS) plan_kernel(const DevProb P, int policy, int nlev, const Slot *winner,
-                                                            const float *lam, const DevHeader *hdr, camelot_plan *out) {
+// keys != nullptr (one rank): the level's packed key is resolved here first (resolve_kernel's
+// world-1 rule: objective key from the packed key, index from this rank's exact best
+// `local`) and the winner is written back -- one launch instead of two at the end of a plan.
+CAM_GLOBAL void __launch_bounds__(PLAN_THREADS) plan_kernel(const DevProb P, int policy, int nlev, Slot *winner,
+                                                            const float *lam, const DevHeader *hdr, camelot_plan *out,
+                                                            const long long *keys = nullptr,
+                                                            const Slot *local = nullptr) {
     const int k = blockIdx.x;
     if (k >= nlev) return;
     __shared__ PlanScratch ps;
-    plan_block(P, policy, winner[k], lam + k * P.A, hdr, out + k, ps);
+    Slot w;
+    if (keys) {
+        const unsigned long long packed = (unsigned long long)keys[k] ^ 0x8000000000000000ull;
+        w.key = packed == ~0ull ? 0xFFFFFFFFull : packed >> 32;
+        w.x = packed == ~0ull ? ~0ull : local[k].x;
+        if (threadIdx.x == 0) winner[k] = w;
+    } else {
+        w = winner[k];
+    }
+    plan_block(P, policy, w, lam + k * P.A, hdr, out + k, ps);
 }
 
 // camelot_plan_max_then_min, between the two searches, in ONE launch (one CTA):
