@@ -861,16 +861,11 @@ int local_search(const Ctx &X, const camelot_exec *ex, int policy, int nlev, lon
     Slot *inc = reinterpret_cast<Slot *>(ws + X.L.inc);
     Slot *result = reinterpret_cast<Slot *>(ws + X.L.result);
     long long *keys = d_keys ? d_keys : reinterpret_cast<long long *>(ws + X.L.keys);
-    // incumbent = none: key 0xFFFFFFFF, x = ~0
+    // incumbent = none (key 0xFFFFFFFF, x = ~0), counters zeroed, Eq. 2 estimates: one launch
     if (!prologue_done) {
-        init_slots_kernel<<<1, 64, 0, X.st>>>(inc, nlev);
-        COUNT_LAUNCH();
-        CU(cudaGetLastError());
-    }
-    if (policy == 1 && !prologue_done) {
-        const int nb = X.d.nbc * nlev;
-        eq2_kernel<<<(nb + 127) / 128, 128, 0, X.st>>>(X.P, reinterpret_cast<const float *>(ws + X.L.lam), nlev,
-                                                      reinterpret_cast<int *>(ws + X.L.y));
+        prologue_kernel<<<1, 256, 0, X.st>>>(X.P, inc, nlev, policy, reinterpret_cast<const float *>(ws + X.L.lam),
+                                             reinterpret_cast<int *>(ws + X.L.y),
+                                             reinterpret_cast<DevHeader *>(ws + X.L.hdr));
         COUNT_LAUNCH();
         CU(cudaGetLastError());
     }
@@ -878,10 +873,6 @@ int local_search(const Ctx &X, const camelot_exec *ex, int policy, int nlev, lon
     range_of(X, ex, lo, hi);
     int dev = ex->device;
     int rc;
-    if (!prologue_done) {
-        DevHeader *hdr = reinterpret_cast<DevHeader *>(ws + X.L.hdr);
-        CU(cudaMemsetAsync(&hdr->cum_scored, 0, 2 * sizeof(unsigned long long) + 2 * sizeof(unsigned int), X.st));
-    }
     if (t_ev.dev != dev) {
         if (t_ev.a) {
             cudaEventDestroy(t_ev.a);

@@ -546,6 +546,35 @@ CAM_GLOBAL void __launch_bounds__(PLAN_THREADS) plan_kernel(const DevProb P, int
     plan_block(P, policy, w, lam + k * P.A, hdr, out + k, ps);
 }
 
+// The prologue of a search in ONE launch (one CTA): no incumbent (key 0xFFFFFFFF,
+// x = ~0) at every level, the cumulative counters of the call zeroed, and (min
+// resource) the Eq. 2 estimates y[bc][k] at the levels' loads (eq2_kernel's rule).
+CAM_GLOBAL void prologue_kernel(const DevProb P, Slot *inc, int nlev, int policy, const float *lam, int *y,
+                                DevHeader *hdr) {
+    const int t = threadIdx.x;
+    for (int k = t; k < nlev; k += blockDim.x) {
+        inc[k].key = 0xFFFFFFFFull;
+        inc[k].x = ~0ull;
+    }
+    if (t == 0) {
+        hdr->cum_scored = 0;
+        hdr->cum_nodes = 0;
+        hdr->trace_n = 0;
+        hdr->trace_pad = 0;
+    }
+    if (policy == 1)
+        for (int idx = t; idx < P.nbc * nlev; idx += blockDim.x) {
+            const int bc = idx / nlev, k = idx % nlev;
+            int beta[AMAX];
+            int r = bc;
+            for (int a = P.A - 1; a >= 0; --a) {
+                beta[a] = r % P.nS;
+                r /= P.nS;
+            }
+            y[idx] = eq2_gpus(P, beta, lam + k * P.A);
+        }
+}
+
 // camelot_plan_max_then_min, between the two searches, in ONE launch (one CTA):
 //  * resolve the max-load key (world 1: resolve_kernel's rule);
 //  * the low load (low load = a fraction of the peak): load_a =
