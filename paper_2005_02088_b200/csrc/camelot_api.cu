@@ -855,7 +855,7 @@ std::vector<int> coarse_strides(const Ctx &X, int policy) {
 // prologue_done: the incumbent slots, the Eq. 2 estimates and the cumulative counters
 // were already prepared on the stream (camelot_plan_max_then_min's bridge_kernel)
 int local_search(const Ctx &X, const camelot_exec *ex, int policy, int nlev, long long *d_keys,
-                 bool prologue_done = false) {
+                 bool prologue_done = false, bool snapshot = true) {
     const bool prune = !(X.P.flags & F_NO_FILTER);
     char *ws = X.ws;
     Slot *inc = reinterpret_cast<Slot *>(ws + X.L.inc);
@@ -930,14 +930,16 @@ int local_search(const Ctx &X, const camelot_exec *ex, int policy, int nlev, lon
     }
     CU(cudaEventRecord(t_ev.b, X.st));
     t_ev.armed = true;
-    CU(cudaMemcpyAsync(ws + X.L.hdr2, ws + X.L.hdr, sizeof(DevHeader), cudaMemcpyDeviceToDevice, X.st));
+    // the counters for camelot_finalize, safe from a chunk re-scan (camelot_plan_max_then_min
+    // reads them from the header itself: nothing runs in between)
+    if (snapshot) CU(cudaMemcpyAsync(ws + X.L.hdr2, ws + X.L.hdr, sizeof(DevHeader), cudaMemcpyDeviceToDevice, X.st));
     return CAMELOT_OK;
 }
 
 // resolve the reduced keys (+ chunk re-scan when sharded) and score the winners into
 // dplans[0..nlev) on the device; no host synchronisation when world == 1
 int finalize_enqueue(const Ctx &X, const camelot_exec *ex, int policy, int nlev, const long long *d_keys,
-                     camelot_plan *dplans) {
+                     camelot_plan *dplans, bool from_hdr = false) {
     const bool prune = !(X.P.flags & F_NO_FILTER);
     char *ws = X.ws;
     Slot *winner = reinterpret_cast<Slot *>(ws + X.L.winner);
@@ -968,8 +970,9 @@ int finalize_enqueue(const Ctx &X, const camelot_exec *ex, int policy, int nlev,
         }
     }
     plan_kernel<<<nlev, PLAN_THREADS, 0, X.st>>>(X.P, policy, nlev, winner, reinterpret_cast<const float *>(ws + X.L.lam),
-                                                   reinterpret_cast<const DevHeader *>(ws + X.L.hdr2), dplans,
-                                                   ex->world > 1 ? nullptr : d_keys, ex->world > 1 ? nullptr : F.local);
+                                                   reinterpret_cast<const DevHeader *>(ws + (from_hdr ? X.L.hdr : X.L.hdr2)),
+                                                   dplans, ex->world > 1 ? nullptr : d_keys,
+                                                   ex->world > 1 ? nullptr : F.local);
     COUNT_LAUNCH();
     CU(cudaGetLastError());
     return CAMELOT_OK;
@@ -1134,7 +1137,7 @@ int camelot_plan_max_then_min(const camelot_problem *p, const camelot_cluster *c
     if (rc) return rc;
     camelot_plan *dplans = reinterpret_cast<camelot_plan *>(X.ws + X.L.plans);   // [0] min-resource, [1] max-load
     // max-load search and its winner
-    rc = local_search(X, ex, 0, 1, nullptr);
+    rc = local_search(X, ex, 0, 1, nullptr, false, false);
     if (rc) return rc;
     std::swap(t_ev, t_ev_spare);   // keep the max-load search's events
     if (t_side.dev != ex->device) {
@@ -1159,7 +1162,7 @@ int camelot_plan_max_then_min(const camelot_problem *p, const camelot_cluster *c
                                        reinterpret_cast<const Slot *>(X.ws + X.L.result),
                                        reinterpret_cast<Slot *>(X.ws + X.L.winner), low_load_frac,
                                        reinterpret_cast<float *>(X.ws + X.L.lam), side_w, side_h,
-                                       reinterpret_cast<const DevHeader *>(X.ws + X.L.hdr2),
+                                       reinterpret_cast<const DevHeader *>(X.ws + X.L.hdr),
                                        reinterpret_cast<Slot *>(X.ws + X.L.inc), reinterpret_cast<int *>(X.ws + X.L.y),
                                        reinterpret_cast<DevHeader *>(X.ws + X.L.hdr));
     COUNT_LAUNCH();
@@ -1171,8 +1174,8 @@ int camelot_plan_max_then_min(const camelot_problem *p, const camelot_cluster *c
     COUNT_LAUNCH();
     CU(cudaGetLastError());
     CU(cudaEventRecord(t_side.join, t_side.s));
-    rc = local_search(X, ex, 1, 1, nullptr, true);
-    if (!rc) rc = finalize_enqueue(X, ex, 1, 1, reinterpret_cast<const long long *>(X.ws + X.L.keys), dplans);
+    rc = local_search(X, ex, 1, 1, nullptr, true, false);
+    if (!rc) rc = finalize_enqueue(X, ex, 1, 1, reinterpret_cast<const long long *>(X.ws + X.L.keys), dplans, true);
     CU(cudaStreamWaitEvent(X.st, t_side.join, 0));   // join the max-load plan (also on an error)
     if (rc) return rc;
     camelot_plan both[2];

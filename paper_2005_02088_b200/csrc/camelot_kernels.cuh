@@ -605,20 +605,22 @@ CAM_GLOBAL void bridge_kernel(const DevProb P, const long long *keys, const Slot
         *side_w = w;
         inc[0].key = 0xFFFFFFFFull;
         inc[0].x = ~0ull;
-        hdr->cum_scored = 0;
-        hdr->cum_nodes = 0;
-        hdr->trace_n = 0;
-        hdr->trace_pad = 0;
     }
     __syncthreads();
     if (t < P.A) {
         const float T = __uint_as_float(0xFFFFFFFFu - (uint32_t)w.key);
         lam[t] = w.x != ~0ull ? __double2float_rn(frac * (double)T) : __int_as_float(0x7f800000);
     }
-    const uint32_t *src = reinterpret_cast<const uint32_t *>(hdr2);
+    const uint32_t *src = reinterpret_cast<const uint32_t *>(hdr2);   // (may be hdr itself)
     uint32_t *dst = reinterpret_cast<uint32_t *>(side_h);
     for (int q = t; q < (int)(offsetof(DevHeader, trace_n) / 4); q += blockDim.x) dst[q] = src[q];
-    __syncthreads();   // lam before the Eq. 2 estimates
+    __syncthreads();   // the snapshot before the counters are zeroed; lam before the Eq. 2 estimates
+    if (t == 0) {
+        hdr->cum_scored = 0;
+        hdr->cum_nodes = 0;
+        hdr->trace_n = 0;
+        hdr->trace_pad = 0;
+    }
     for (int bc = t; bc < P.nbc; bc += blockDim.x) {
         int beta[AMAX];
         int r = bc;
