@@ -392,15 +392,30 @@ struct WarpBest {
     unsigned long long bound;       // pruning bound: max over levels of key (conservative)
     unsigned long long gpack;       // device-wide (key << 32 | x >> xshift) best (1 level)
     float lmin;                     // min-resource, one application: the smallest load level
+    int mlev;                       // min-resource, one application, several levels: level-aware bound
+    float lam[LMAX];                // (mlev) the load of each level
 };
 
 // Can a subtree whose keys are >= kl and whose indices are >= xs still hold
 // the answer?  Strictly worse keys cannot; with ONE level, a key equal to the
 // best can only tie and ties go to the smallest index, so a subtree entirely
 // above the best's index cannot either (exact).
+// Min resource with several load levels (one application): a subtree whose completions
+// all have T <= tub cannot be feasible at a level with load > tub, so only the levels
+// it can carry bound it (their best keys are non-decreasing in the load, the bound is
+// the largest of them); no such level: nothing to find.  (wb->bound, the max over all
+// levels, is the plain rule.)
+__device__ __forceinline__ unsigned long long level_bound(const WarpBest *wb, int nlev, float tub) {
+    if (nlev == 1 || !wb->mlev) return wb->bound;
+    unsigned long long m = 0;
+    for (int k = 0; k < nlev; ++k)
+        if (wb->lam[k] <= tub) m = max(m, wb->key[k]);
+    return min(m, wb->bound);
+}
+
 __device__ __forceinline__ bool can_win(unsigned long long kl, unsigned long long xs, const WarpBest *wb, int nlev,
-                                        int xshift) {
-    if (kl > wb->bound) return false;
+                                        int xshift, float tub = __builtin_inff()) {
+    if (kl > level_bound(wb, nlev, tub)) return false;
     if (nlev == 1) {
         if (kl == wb->key[0] && xs > wb->x[0]) return false;
         if (kl == (wb->gpack >> 32) && (xs >> xshift) > (wb->gpack & 0xFFFFFFFFull)) return false;
@@ -1057,6 +1072,9 @@ __device__ __forceinline__ void init_warp_best(const SearchArgs &S, WarpBest *wb
             for (int k = 0; k < nlev; ++k) lm = fminf(lm, S.lam[k * S.lam_stride]);
         }
         wb->lmin = lm;
+        wb->mlev = S.policy == 1 && S.lam && nlev > 1 && S.lam_stride == 1;
+        if (wb->mlev)
+            for (int k = 0; k < nlev; ++k) wb->lam[k] = S.lam[k];
     }
     __syncwarp();
 }
@@ -1098,7 +1116,8 @@ __device__ __forceinline__ void thread_chunk(const DevProb &P, const SearchArgs 
                 const int Ulb = c.U + (int)sb_at(P, S, j, bj).minNP + c.restU;
                 kl = objkey_minres(max(c.u, (Ulb + P.R - 1) / P.R), Ulb);
             }
-            go_node = can_win(kl, c.x * P.opow[n - j], wb, nlev, S.xshift);
+            go_node = can_win(kl, c.x * P.opow[n - j], wb, nlev, S.xshift,
+                              fminf(c.tub, fminf(sb_at(P, S, j, bj).maxNT, c.restT)));
             if (pol == 1 && P.A == 1 && c.tub < wb->lmin) go_node = false;
         }
         const int cnt = go_node ? (int)sb_at(P, S, j, bj).cnt : 0;
@@ -1136,7 +1155,8 @@ __device__ __forceinline__ void thread_chunk(const DevProb &P, const SearchArgs 
                     const int Ulb = c.U + (int)r.NP + c.restU;
                     kl = objkey_minres(max(c.u, (Ulb + P.R - 1) / P.R), Ulb);
                 }
-                go = can_win(kl, x * span, wb, nlev, S.xshift);
+                go = can_win(kl, x * span, wb, nlev, S.xshift,
+                             leaf ? fminf(c.tub, r.NT) : fminf(fminf(c.tub, r.NT), c.restT));
                 if (go && leaf && pol == 0) go = kl < bk || (kl == bk && x < bx);   // the lane's own best
                 if (go && !leaf && c.rqsum - (int)r.NP < c.restU) go = false;
             }
@@ -1217,7 +1237,8 @@ __device__ __forceinline__ void thread_chunk(const DevProb &P, const SearchArgs 
                 if (sv && pol == 1 && P.A == 1 && t_certainly_below<NS>(P, j, fe.kap, ntf, wb->lmin)) sv = false;
                 if (sv && pol == 1) {
                     const int Ulb = fe.U + c.restU;
-                    sv = (unsigned long long)objkey_minres(max(fe.u, (Ulb + P.R - 1) / P.R), Ulb) <= wb->bound;
+                    sv = (unsigned long long)objkey_minres(max(fe.u, (Ulb + P.R - 1) / P.R), Ulb) <=
+                         level_bound(wb, nlev, fminf(fminf(c.tub, r.NT), c.restT));
                 }
             }
             if (sv && j + 1 == S.d0) sv = owns_child<CM>(P, S, nd, j, k);
@@ -1433,7 +1454,7 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
                     const int Ulb = Uq + (int)bj.minNP + rU;
                     kl = objkey_minres(max(uq, (Ulb + P.R - 1) / P.R), Ulb);
                 }
-                lv = can_win(kl, xq * P.opow[n - jtop], wb, nlev, S.xshift);
+                lv = can_win(kl, xq * P.opow[n - jtop], wb, nlev, S.xshift, fminf(tq, fminf(bj.maxNT, rT)));
             }
             live = __ballot_sync(0xffffffffu, lv);
         }
@@ -1521,7 +1542,8 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
                             const int Ulb = c.U + (int)sb_at(P, S, j, bj).minNP + c.restU;
                             kl = objkey_minres(max(c.u, (Ulb + P.R - 1) / P.R), Ulb);
                         }
-                        bool live = can_win(kl, c.x * P.opow[n - j], wb, nlev, S.xshift);
+                        bool live = can_win(kl, c.x * P.opow[n - j], wb, nlev, S.xshift,
+                                            fminf(c.tub, fminf(sb_at(P, S, j, bj).maxNT, c.restT)));
                         // T_i <= fl(N_i thr_i / kappa_i(now)) (kappa only grows): below the load floor -> dead
                         if (pol == 1 && P.A == 1 && c.tub < wb->lmin) live = false;
                         if (!live) {
@@ -1602,7 +1624,8 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
                         const int Ulb = c.U + (int)r.NP + c.restU;
                         kl = objkey_minres(max(c.u, (Ulb + P.R - 1) / P.R), Ulb);
                     }
-                    go = can_win(kl, x * span, wb, nlev, S.xshift);
+                    go = can_win(kl, x * span, wb, nlev, S.xshift,
+                                 leaf ? fminf(c.tub, r.NT) : fminf(fminf(c.tub, r.NT), c.restT));
                     if (go && !leaf && c.rqsum - (int)r.NP < c.restU) go = false;
                 }
                 // QoS lower bound before placement: L_j >= dur, placed stages' L
@@ -1652,7 +1675,8 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
                     }
                     if (sv && pol == 1) {
                         const int Ulb = fe.U + c.restU;
-                        sv = (unsigned long long)objkey_minres(max(fe.u, (Ulb + P.R - 1) / P.R), Ulb) <= wb->bound;
+                        sv = (unsigned long long)objkey_minres(max(fe.u, (Ulb + P.R - 1) / P.R), Ulb) <=
+                             level_bound(wb, nlev, fminf(fminf(c.tub, r.NT), c.restT));
                     }
                 }
                 if (sv && j + 1 == S.d0) sv = owns_child<CM>(P, S, nd, j, opt);
