@@ -1117,7 +1117,7 @@ __device__ __forceinline__ void thread_chunk(const DevProb &P, const SearchArgs 
                 kl = objkey_minres(max(c.u, (Ulb + P.R - 1) / P.R), Ulb);
             }
             go_node = can_win(kl, c.x * P.opow[n - j], wb, nlev, S.xshift,
-                              fminf(c.tub, fminf(sb_at(P, S, j, bj).maxNT, c.restT)));
+                              nlev > 1 ? fminf(c.tub, fminf(sb_at(P, S, j, bj).maxNT, c.restT)) : __builtin_inff());
             if (pol == 1 && P.A == 1 && c.tub < wb->lmin) go_node = false;
         }
         const int cnt = go_node ? (int)sb_at(P, S, j, bj).cnt : 0;
@@ -1156,7 +1156,7 @@ __device__ __forceinline__ void thread_chunk(const DevProb &P, const SearchArgs 
                     kl = objkey_minres(max(c.u, (Ulb + P.R - 1) / P.R), Ulb);
                 }
                 go = can_win(kl, x * span, wb, nlev, S.xshift,
-                             leaf ? fminf(c.tub, r.NT) : fminf(fminf(c.tub, r.NT), c.restT));
+                             nlev == 1 ? __builtin_inff() : leaf ? fminf(c.tub, r.NT) : fminf(fminf(c.tub, r.NT), c.restT));
                 if (go && leaf && pol == 0) go = kl < bk || (kl == bk && x < bx);   // the lane's own best
                 if (go && !leaf && c.rqsum - (int)r.NP < c.restU) go = false;
             }
@@ -1238,7 +1238,7 @@ __device__ __forceinline__ void thread_chunk(const DevProb &P, const SearchArgs 
                 if (sv && pol == 1) {
                     const int Ulb = fe.U + c.restU;
                     sv = (unsigned long long)objkey_minres(max(fe.u, (Ulb + P.R - 1) / P.R), Ulb) <=
-                         level_bound(wb, nlev, fminf(fminf(c.tub, r.NT), c.restT));
+                         (nlev == 1 ? wb->bound : level_bound(wb, nlev, fminf(fminf(c.tub, r.NT), c.restT)));
                 }
             }
             if (sv && j + 1 == S.d0) sv = owns_child<CM>(P, S, nd, j, k);
@@ -1454,7 +1454,7 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
                     const int Ulb = Uq + (int)bj.minNP + rU;
                     kl = objkey_minres(max(uq, (Ulb + P.R - 1) / P.R), Ulb);
                 }
-                lv = can_win(kl, xq * P.opow[n - jtop], wb, nlev, S.xshift, fminf(tq, fminf(bj.maxNT, rT)));
+                lv = can_win(kl, xq * P.opow[n - jtop], wb, nlev, S.xshift, nlev > 1 ? fminf(tq, fminf(bj.maxNT, rT)) : __builtin_inff());
             }
             live = __ballot_sync(0xffffffffu, lv);
         }
@@ -1543,7 +1543,7 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
                             kl = objkey_minres(max(c.u, (Ulb + P.R - 1) / P.R), Ulb);
                         }
                         bool live = can_win(kl, c.x * P.opow[n - j], wb, nlev, S.xshift,
-                                            fminf(c.tub, fminf(sb_at(P, S, j, bj).maxNT, c.restT)));
+                                            nlev > 1 ? fminf(c.tub, fminf(sb_at(P, S, j, bj).maxNT, c.restT)) : __builtin_inff());
                         // T_i <= fl(N_i thr_i / kappa_i(now)) (kappa only grows): below the load floor -> dead
                         if (pol == 1 && P.A == 1 && c.tub < wb->lmin) live = false;
                         if (!live) {
@@ -1625,7 +1625,7 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
                         kl = objkey_minres(max(c.u, (Ulb + P.R - 1) / P.R), Ulb);
                     }
                     go = can_win(kl, x * span, wb, nlev, S.xshift,
-                                 leaf ? fminf(c.tub, r.NT) : fminf(fminf(c.tub, r.NT), c.restT));
+                                 nlev == 1 ? __builtin_inff() : leaf ? fminf(c.tub, r.NT) : fminf(fminf(c.tub, r.NT), c.restT));
                     if (go && !leaf && c.rqsum - (int)r.NP < c.restU) go = false;
                 }
                 // QoS lower bound before placement: L_j >= dur, placed stages' L
@@ -1676,7 +1676,7 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
                     if (sv && pol == 1) {
                         const int Ulb = fe.U + c.restU;
                         sv = (unsigned long long)objkey_minres(max(fe.u, (Ulb + P.R - 1) / P.R), Ulb) <=
-                             level_bound(wb, nlev, fminf(fminf(c.tub, r.NT), c.restT));
+                             (nlev == 1 ? wb->bound : level_bound(wb, nlev, fminf(fminf(c.tub, r.NT), c.restT)));
                     }
                 }
                 if (sv && j + 1 == S.d0) sv = owns_child<CM>(P, S, nd, j, opt);
