@@ -1,10 +1,11 @@
 // camelot_kernels.cuh -- the small kernels around the search (sm_100a):
 //   filter_kernel   (N3) per (batch, stage) option filtering + compaction,
-//   offsets_kernel       item-space prefix offsets per batch combo,
-//   eq2_kernel           Eq. 2 GPU-count estimate per (batch combo, load level),
+//   prologue_kernel      a search's prologue: incumbent slots, counters, Eq. 2 estimates,
+//   bridge_kernel        camelot_plan_max_then_min between the two searches,
 //   reduce_kernel        per-CTA slots -> rank-local best + packed 64-bit keys,
-//   finalize_kernel (N4/N5) keys -> exact index (chunk rescan result) -> plan,
-//   score_range_kernel   (N5) one thread per candidate, full recompute.
+//   resolve_kernel, plan_kernel (N4/N5) keys -> exact index (chunk rescan) -> plan,
+//   level_body / search_level_kernel: filter + passes of one pruned search level,
+//   score_range_kernel, predict_kernel, flat_search_kernel (N5): full recompute.
 #pragma once
 #include "../../include/camelot.h"
 #include "camelot_device.cuh"
@@ -336,19 +337,6 @@ CAM_DEVFN void item_offsets_block(const DevProb &P, const StageBound *sb, int d0
     }
 }
 
-CAM_GLOBAL void eq2_kernel(const DevProb P, const float *lam, int nlev, int *y) {
-    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= P.nbc * nlev) return;
-    const int bc = idx / nlev, k = idx % nlev;
-    int beta[AMAX];
-    int t = bc;
-    for (int a = P.A - 1; a >= 0; --a) {
-        beta[a] = t % P.nS;
-        t /= P.nS;
-    }
-    y[idx] = eq2_gpus(P, beta, lam + k * P.A);
-}
-
 // slots -> result[k] and packed keys (stand-alone kernel: naive path)
 CAM_GLOBAL void reduce_kernel(const DevProb P, const Slot *slots, int nslots, int nlev, Slot *result,
                               long long *keys, const StageBound *sb, const OptRec *rec,
@@ -548,7 +536,7 @@ CAM_GLOBAL void __launch_bounds__(PLAN_THREADS) plan_kernel(const DevProb P, int
 
 // The prologue of a search in ONE launch (one CTA): no incumbent (key 0xFFFFFFFF,
 // x = ~0) at every level, the cumulative counters of the call zeroed, and (min
-// resource) the Eq. 2 estimates y[bc][k] at the levels' loads (eq2_kernel's rule).
+// resource) the Eq. 2 estimates y[bc][k] = eq2_gpus at the levels' loads.
 CAM_GLOBAL void prologue_kernel(const DevProb P, Slot *inc, int nlev, int policy, const float *lam, int *y,
                                 DevHeader *hdr) {
     const int t = threadIdx.x;
@@ -586,7 +574,7 @@ CAM_GLOBAL void prologue_kernel(const DevProb P, Slot *inc, int nlev, int policy
 //  * a snapshot of the winner and the search counters for the max-load plan_kernel,
 //    which runs on a second stream while the min-resource search runs;
 //  * the min-resource search's prologue: no incumbent, the Eq. 2 estimates at the low
-//    load, the cumulative counters zeroed (init_slots_kernel, eq2_kernel, a memset).
+//    load, the cumulative counters zeroed (what prologue_kernel does for a search).
 CAM_GLOBAL void bridge_kernel(const DevProb P, const long long *keys, const Slot *local, Slot *winner, double frac,
                               float *lam, Slot *side_w, DevHeader *side_h, const DevHeader *hdr2, Slot *inc, int *y,
                               DevHeader *hdr) {
