@@ -349,3 +349,16 @@ def test_plan_diagnostics_and_trace(api):
     assert tags.count(0) >= 1 and 16 in tags and 32 in tags      # launch start, pass 0, CTA reduction
     times = [ns for t, ns in tr if t < 64]
     assert times == sorted(times)
+
+
+def test_min_resource_unsorted_levels(api, oracle):
+    """Several load levels in no particular order (the multi-level bound takes, per
+    subtree, the best keys of the levels it can carry -- no ordering assumed)."""
+    for prob in G.config_problems(2)[:4] + G.config_problems(3):
+        bm = oracle.search(prob, threads=8)[0]
+        fr = (0.9, 0.15, 0.6, 1.0, 0.35, 0.05)
+        loads = [[np.float32(f) * np.float32(bm.T)] for f in fr]
+        got = api.Session(prob, n_loads=len(fr)).plan_min_resource(loads)
+        ref = oracle.search(prob, "min_resource", loads=loads, threads=8)
+        for k, (g, r) in enumerate(zip(got, ref)):
+            check_plan(api, prob, g, r, oracle, loads=[loads[k]])
