@@ -123,7 +123,7 @@ CAM_DEVFN void filter_body(const DevProb &P, const FilterArgs &F, int b, FilterS
             if (N > P.C * P.I) k = false;
             const float NT = __fmul_rn((float)N, e.y);
             if (F.policy == 0 && has_inc && NT < Tinc) k = false;   // T <= fl(N thr) < T_inc
-            if (F.policy == 1 && NT < lam_min[P.app[i]]) k = false; // load floor at every level
+            if (F.policy == 1 && NT < (P.app[i] ? lam_min[AMAX - 1] : lam_min[0])) k = false; // load floor at every level
         }
         keep[i][o] = k;
     }
@@ -287,16 +287,17 @@ CAM_DEVFN void item_offsets(const DevProb &P, const StageBound *sb, int d0, unsi
     unsigned long long acc = 0;
     for (int bc = 0; bc < P.nbc; ++bc) {
         item_off[bc] = acc;
-        int bb[AMAX];
-        int t = bc;
-        for (int a = P.A - 1; a >= 0; --a) {
-            bb[a] = t % P.nS;
-            t /= P.nS;
+        int bb[AMAX];   // batch index per application (explicit: no dynamically indexed local array)
+        {
+            int t = bc;
+            bb[AMAX - 1] = t % P.nS;
+            if (P.A > 1) t /= P.nS;
+            bb[0] = t % P.nS;
         }
         unsigned long long it = 1;
         bool empty = false;
         for (int i = 0; i < P.n; ++i) {
-            const unsigned c = sb[(size_t)i * P.nS + bb[P.app[i]]].cnt;
+            const unsigned c = sb[(size_t)i * P.nS + (P.app[i] ? bb[AMAX - 1] : bb[0])].cnt;
             if (c == 0) empty = true;
             if (i < d0) it *= c;
         }
@@ -310,16 +311,17 @@ CAM_DEVFN void item_offsets(const DevProb &P, const StageBound *sb, int d0, unsi
 // memory (nbc <= ITEM_SMEM): per-combo counts in parallel, then an inclusive scan.
 CAM_DEVFN void item_offsets_block(const DevProb &P, const StageBound *sb, int d0, unsigned long long *out) {
     for (int bc = threadIdx.x; bc < P.nbc; bc += blockDim.x) {
-        int bb[AMAX];
-        int t = bc;
-        for (int a = P.A - 1; a >= 0; --a) {
-            bb[a] = t % P.nS;
-            t /= P.nS;
+        int bb[AMAX];   // batch index per application (explicit: no dynamically indexed local array)
+        {
+            int t = bc;
+            bb[AMAX - 1] = t % P.nS;
+            if (P.A > 1) t /= P.nS;
+            bb[0] = t % P.nS;
         }
         unsigned long long it = 1;
         bool empty = false;
         for (int i = 0; i < P.n; ++i) {
-            const unsigned c = sb[(size_t)i * P.nS + bb[P.app[i]]].cnt;
+            const unsigned c = sb[(size_t)i * P.nS + (P.app[i] ? bb[AMAX - 1] : bb[0])].cnt;
             if (c == 0) empty = true;
             if (i < d0) it *= c;
         }

@@ -348,14 +348,12 @@ __device__ void build_child(const DevProb &P, const SearchArgs &S, const Node<CM
 // root node for beta combo bc (no stage placed), built by the warp
 template <int CM>
 __device__ void build_root(const DevProb &P, int bc, Node<CM> &out, int lane) {
-    int b[AMAX];
+    int b[AMAX];   // batch index per application (explicit: no dynamically indexed local array)
     {
         int t = bc;
-        for (int a = P.A - 1; a >= 0; --a) {
-            b[a] = t % P.nS;
-            t /= P.nS;
-        }
-        if (P.A == 1) b[AMAX - 1] = b[0];
+        b[AMAX - 1] = t % P.nS;
+        if (P.A > 1) t /= P.nS;
+        b[0] = t % P.nS;
     }
     __syncwarp();
     if (lane < P.C) {
@@ -363,7 +361,7 @@ __device__ void build_root(const DevProb &P, int bc, Node<CM> &out, int lane) {
         out.pcnt[g] = 0;
         out.prm[g] = P.FM;
         // all GPUs equal: order = index
-        const uint32_t W0 = P.W[0], As0 = P.Am[0] * (uint32_t)P.S[b[P.app[0]]];
+        const uint32_t W0 = P.W[0], As0 = P.Am[0] * (uint32_t)P.S[P.app[0] ? b[AMAX - 1] : b[0]];
         int km = P.Rmax;
         if (P.FM < W0) km = 0;
         else if (As0 > 0) km = (int)min((uint32_t)P.Rmax, (P.FM - W0) / As0);
@@ -1443,11 +1441,11 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
                 float rT = __int_as_float(0x7f800000);
                 int rU = 0;
                 for (int i2 = jtop + 1; i2 < n; ++i2) {
-                    const StageBound &bb = sb_at(P, S, i2, bq[P.app[i2]]);
+                    const StageBound &bb = sb_at(P, S, i2, P.app[i2] ? bq[AMAX - 1] : bq[0]);   // (select: no local array)
                     rT = fminf(rT, bb.maxNT);
                     rU += (int)bb.minNP;
                 }
-                const StageBound &bj = sb_at(P, S, jtop, bq[P.app[jtop]]);
+                const StageBound &bj = sb_at(P, S, jtop, P.app[jtop] ? bq[AMAX - 1] : bq[0]);
                 unsigned long long kl;
                 if (pol == 0) kl = objkey_maxload(fminf(tq, fminf(bj.maxNT, rT)));
                 else {
