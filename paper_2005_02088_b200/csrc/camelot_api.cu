@@ -738,6 +738,7 @@ int search_pass(const Ctx &X, int dev, int policy, int nlev, bool prune, int str
     S.slots = reinterpret_cast<Slot *>(ws + slots_off(X.L));
     S.xshift = xshift_of(X.d.ntot);
     S.tmode_min16 = getenv("CAMELOT_TMODE_MIN16") ? atoi(getenv("CAMELOT_TMODE_MIN16")) : 32;   // (testing knob)
+    S.tmode_inner_gmax = getenv("CAMELOT_TMODE_INNER_G") ? atoi(getenv("CAMELOT_TMODE_INNER_G")) : 8;   // (testing knob)
     S.result = result;
     S.keys = keys;
     S.inc_out = inc_out;
@@ -796,6 +797,7 @@ int rescan_pass(const Ctx &X, int dev, int policy, int nlev, bool prune, int k, 
     S.chunk_hi = chunk + 1;
     S.xshift = xshift_of(X.d.ntot);
     S.tmode_min16 = getenv("CAMELOT_TMODE_MIN16") ? atoi(getenv("CAMELOT_TMODE_MIN16")) : 32;   // (testing knob)
+    S.tmode_inner_gmax = getenv("CAMELOT_TMODE_INNER_G") ? atoi(getenv("CAMELOT_TMODE_INNER_G")) : 8;   // (testing knob)
     CU(cudaMemsetAsync(&hdr->best_obj, 0xFF, sizeof(unsigned int), X.st));
     CU(cudaMemsetAsync(&hdr->best_packed, 0xFF, sizeof(unsigned long long), X.st));
     CU(cudaMemsetAsync(&hdr->done_ctas, 0, sizeof(unsigned int), X.st));

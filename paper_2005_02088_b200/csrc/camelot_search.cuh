@@ -77,6 +77,7 @@ struct SearchArgs {
     unsigned long long *head;   // pop counter of this pass
     int xshift;                 // index >> xshift fits 32 bits (tie pruning key)
     int tmode_min16;            // thread-per-parent mode from count >= tmode_min16 / 16 x resident warps
+    int tmode_inner_gmax;       // inner passes: up to this many lanes per parent (32 children per lane)
     // fused reduction (last pass): the last CTA reduces all slots
     int reduce_last;
     Slot *result;               // [nlev] exact local best
@@ -1355,9 +1356,13 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
     int G = 1;
     while (G < 8 && count * (unsigned long long)(2 * G) <= 32ull * nwarps) G *= 2;
     if (leafp) G = max(G, maxc <= 32 ? 1 : maxc <= 64 ? 2 : 4);
+    // inner passes: G lanes per parent also keep <= 32 children per lane (survivor mask)
+    const int Gin = max(G, maxc <= 32 ? 1 : maxc <= 64 ? 2 : maxc <= 128 ? 4 : 8);
+    const bool inner_t = S.flevel == jtop + 1 && maxc <= 32 * min(Gin, S.tmode_inner_gmax) &&
+                         count * (unsigned long long)maxc <= S.out_cap;
+    if (!leafp && inner_t) G = Gin;
     const bool tmode = S.prune && have_in && split == 1 && 16ull * count >= (unsigned long long)S.tmode_min16 * nwarps && !getenv_tmode_off() &&
-                       ((leafp && maxc <= 128) ||
-                        (S.flevel == jtop + 1 && maxc <= 32 && count * (unsigned long long)maxc <= S.out_cap));
+                       ((leafp && maxc <= 128) || inner_t);
     const unsigned grab = tmode ? 32u / (unsigned)G : screen ? 8u : (unsigned)S.grab;
     const unsigned long long nw = nwarps * grab;
     unsigned long long e0 = ((unsigned long long)blockIdx.x * SEARCH_WARPS + (threadIdx.x >> 5)) * grab;
