@@ -1088,7 +1088,7 @@ __device__ __forceinline__ void thread_chunk(const DevProb &P, const SearchArgs 
                                           const Frontier<CM> &outf, unsigned long long e0, unsigned live, int j,
                                           WarpBest *wb, int lane, Counters &cn, int G) {
     const int pol = POLICY == 2 ? S.policy : POLICY;   // 2: the policy is a runtime argument (shared code)
-    // G lanes per parent (G > 1 only for leaf passes): lane l takes parent e0 + l / G
+    // G lanes per parent (leaf passes, and inner passes with more than 32 options): lane l takes parent e0 + l / G
     // and its children sub, sub + G, ... (sub = l % G)
     const int n = P.n, nlev = S.nlev;
     const bool leaf = j == n - 1;
