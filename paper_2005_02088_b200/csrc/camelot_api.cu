@@ -217,15 +217,17 @@ Layout make_layout(const Dims &d, int nlev) {
     L.side_h = put(sizeof(DevHeader));     // counters, scored on a second stream
     L.slots = put((size_t)MAXSLOTS * L.nlev * sizeof(Slot));
     // frontier of placement-state nodes: as many as there are leaf parents in the
-    // whole space, clamped to [256, 2^21] (overflow falls back to inline DFS).  2^21
-    // (0.9 GB per buffer for 8 GPUs): the thread-per-parent mode needs room for every
-    // child of a pass (measured, C4b: 2^20 forced its 271k-parent pass into the warp
-    // mode, 5.07 ms per step; 2^21: 2.54 ms; C4 unchanged)
+    // whole space, clamped to [256, 2^23] (overflow falls back to inline DFS).  2^23
+    // (3.6 GB per buffer for 8 GPUs, 7 GB per C4 workspace against 180 GB of HBM): the
+    // thread-per-parent mode needs room for every child of a pass (measured: C4b's
+    // 271k-parent pass ran in the warp mode at 2^20, 5.07 ms per step, 2.54 ms at 2^21;
+    // a harder C4-shaped instance (tools/cascade_probe3.py, C4x3) 14.7 ms at 2^21, 5.4 ms
+    // at 2^23; C4 unchanged)
     const size_t nb = d.C > 8 ? sizeof(Node<16>) : d.C > 4 ? sizeof(Node<8>) : sizeof(Node<4>);
     long double parents = (long double)d.ntot / (long double)d.O;
     // (testing knob CAMELOT_FRONTIER_MAX moves the clamp)
     const long double fmax = getenv("CAMELOT_FRONTIER_MAX") ? (long double)atof(getenv("CAMELOT_FRONTIER_MAX"))
-                                                            : (long double)(1u << 21);
+                                                            : (long double)(1u << 23);
     L.fcap = (unsigned long long)std::max(256.0L, std::min(fmax, parents));
     // testing knob: force a small frontier to exercise the inline-descent fallback
     if (const char *cap = getenv("CAMELOT_FRONTIER_CAP")) {

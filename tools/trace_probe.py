@@ -51,9 +51,15 @@ def show(tag, tr, st):
         print("   " + " ".join(line))
 
 
-cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+arg = sys.argv[1] if len(sys.argv) > 1 else "4"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
-p = G.config_problems(cfg)[0]
+if arg.startswith("x"):   # C4-shaped problem of tools/cascade_probe3.py: "x<j>" (seed j, QoS rho)
+    j = int(arg[1:])
+    rho = {2: 1.0, 3: 1.0, 4: 0.8, 5: 0.9, 6: 1.0, 7: 0.8}[j]
+    p = G.build_problem(f"C4x{j}", [["p1", "c2", "m2", "c3", "m1"]], 8, 1, G.POW2_128, 4,
+                        G.config_seed(4, j), rho, "v100-dgx2")
+else:
+    p = G.config_problems(int(arg))[0]
 s = api.Session(p, n_loads=1)
 for rep in range(reps):
     r = s.plan_max_load()
