@@ -741,6 +741,7 @@ int search_pass(const Ctx &X, int dev, int policy, int nlev, bool prune, int str
     S.xshift = xshift_of(X.d.ntot);
     S.tmode_min16 = getenv("CAMELOT_TMODE_MIN16") ? atoi(getenv("CAMELOT_TMODE_MIN16")) : 32;   // (testing knob)
     S.tmode_inner_gmax = getenv("CAMELOT_TMODE_INNER_G") ? atoi(getenv("CAMELOT_TMODE_INNER_G")) : 8;   // (testing knob)
+    S.tmode_slack = 1;   // separate launches have no redo: strict capacity (the cooperative level sets its own)
     S.result = result;
     S.keys = keys;
     S.inc_out = inc_out;
@@ -752,6 +753,9 @@ int search_pass(const Ctx &X, int dev, int policy, int nlev, bool prune, int str
         LA.buf0 = ws + X.L.front0;
         LA.buf1 = ws + X.L.front1;
         LA.fcap = X.L.fcap;
+        // optimistic thread-per-parent inner passes (redone in the warp mode on overflow;
+        // testing knob CAMELOT_TMODE_SLACK)
+        LA.S.tmode_slack = getenv("CAMELOT_TMODE_SLACK") ? std::max(1, atoi(getenv("CAMELOT_TMODE_SLACK"))) : 8;
         if (defer) {   // chained into one cooperative launch by the caller
             defer->push_back(LA);
             return CAMELOT_OK;
@@ -800,6 +804,7 @@ int rescan_pass(const Ctx &X, int dev, int policy, int nlev, bool prune, int k, 
     S.xshift = xshift_of(X.d.ntot);
     S.tmode_min16 = getenv("CAMELOT_TMODE_MIN16") ? atoi(getenv("CAMELOT_TMODE_MIN16")) : 32;   // (testing knob)
     S.tmode_inner_gmax = getenv("CAMELOT_TMODE_INNER_G") ? atoi(getenv("CAMELOT_TMODE_INNER_G")) : 8;   // (testing knob)
+    S.tmode_slack = 1;   // separate launches have no redo: strict capacity (the cooperative level sets its own)
     CU(cudaMemsetAsync(&hdr->best_obj, 0xFF, sizeof(unsigned int), X.st));
     CU(cudaMemsetAsync(&hdr->best_packed, 0xFF, sizeof(unsigned long long), X.st));
     CU(cudaMemsetAsync(&hdr->done_ctas, 0, sizeof(unsigned int), X.st));

@@ -944,7 +944,25 @@ __device__ __forceinline__ void level_body(const DevProb &P, const LevelArgs &LA
         S.out_cap = LA.fcap;
         S.head = &hdr->head[j];
         S.grab = 1;
-        pass_body<CM, NS, POLICY>(P, S, stack, ctl, wb, lane, cn);
+        // (one call site: pass_body is large.)  A thread-per-parent pass that could outgrow
+        // the frontier (optimistic) and did -- children were dropped -- is redone in the
+        // warp mode, which descends inline when the frontier is full.
+        bool redo = false;
+        for (int attempt = 0; attempt < 2; ++attempt) {
+            S.no_tmode = attempt;
+            const bool optimistic = pass_body<CM, NS, POLICY>(P, S, stack, ctl, wb, lane, cn);
+            if (attempt || !optimistic || j == n - 1) break;
+            grid.sync();
+            redo = *(volatile unsigned long long *)&hdr->tail[j + 1] > LA.fcap;   // (same value in every CTA)
+            if (!redo) break;
+            grid.sync();   // every CTA has read the tail
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                hdr->tail[j + 1] = 0;
+                hdr->head[j] = 0;
+            }
+            grid.sync();
+        }
+        S.no_tmode = 0;
         if (j == n - 1) break;   // the last pass ends at the CTA merge below (no grid barrier)
 #ifdef CAMELOT_FTRACE
         if (lane == 0) {

@@ -78,6 +78,9 @@ struct SearchArgs {
     int xshift;                 // index >> xshift fits 32 bits (tie pruning key)
     int tmode_min16;            // thread-per-parent mode from count >= tmode_min16 / 16 x resident warps
     int tmode_inner_gmax;       // inner passes: up to this many lanes per parent (32 children per lane)
+    int tmode_slack;            // inner thread-per-parent passes allowed up to count x maxc <= slack x out_cap
+                                // (> 1: optimistic -- the caller redoes an overflowing pass in the warp mode)
+    int no_tmode;               // the redo: warp mode only
     // fused reduction (last pass): the last CTA reduces all slots
     int reduce_last;
     Slot *result;               // [nlev] exact local best
@@ -1277,7 +1280,9 @@ __device__ __forceinline__ void thread_chunk(const DevProb &P, const SearchArgs 
                     r.dur = __uint_as_float(b.w);
                 }
                 const OptRec &full = list[k];
-                emit_child<CM, NS>(P, nd, c, j, r, full.p, full.W, full.As, k, outf, rbase + __popc(m & ((1u << lane) - 1u)));
+                const unsigned long long slot = rbase + __popc(m & ((1u << lane) - 1u));
+                if (slot < S.out_cap)   // (an optimistic pass may overflow: it is then redone, see pass_body)
+                    emit_child<CM, NS>(P, nd, c, j, r, full.p, full.W, full.As, k, outf, slot);
             }
         }
     }
@@ -1308,7 +1313,11 @@ __device__ __forceinline__ void thread_chunk(const DevProb &P, const SearchArgs 
 // One level-synchronous pass (parents at depth S.level), executed by one warp
 // of a persistent grid until the pass's work is exhausted.
 template <int CM, int NS, int POLICY>
-__device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S, Node<CM> *stack, WarpCtl *ctl,
+// Returns true when the pass ran in the thread-per-parent mode with more possible
+// children than frontier slots (S.tmode_slack > 1): children that found no slot were
+// dropped, so if the frontier overflowed (tail > capacity) the caller must redo the
+// pass in the warp mode (S.no_tmode), which descends inline instead.
+__device__ __forceinline__ bool pass_body(const DevProb &P, const SearchArgs &S, Node<CM> *stack, WarpCtl *ctl,
                                           WarpBest *wb, int lane, Counters &cn) {
     const int pol = POLICY == 2 ? S.policy : POLICY;   // 2: the policy is a runtime argument (shared code)
     const int nlev = S.nlev;
@@ -1359,10 +1368,11 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
     // inner passes: G lanes per parent also keep <= 32 children per lane (survivor mask)
     const int Gin = max(G, maxc <= 32 ? 1 : maxc <= 64 ? 2 : maxc <= 128 ? 4 : 8);
     const bool inner_t = S.flevel == jtop + 1 && maxc <= 32 * min(Gin, S.tmode_inner_gmax) &&
-                         count * (unsigned long long)maxc <= S.out_cap;
+                         count * (unsigned long long)maxc <= S.out_cap * (unsigned long long)max(1, S.tmode_slack);
     if (!leafp && inner_t) G = Gin;
     const bool tmode = S.prune && have_in && split == 1 && 16ull * count >= (unsigned long long)S.tmode_min16 * nwarps && !getenv_tmode_off() &&
-                       ((leafp && maxc <= 128) || inner_t);
+                       !S.no_tmode && ((leafp && maxc <= 128) || inner_t);
+    const bool optimistic = tmode && !leafp && count * (unsigned long long)maxc > S.out_cap;
     const unsigned grab = tmode ? 32u / (unsigned)G : screen ? 8u : (unsigned)S.grab;
     const unsigned long long nw = nwarps * grab;
     unsigned long long e0 = ((unsigned long long)blockIdx.x * SEARCH_WARPS + (threadIdx.x >> 5)) * grab;
@@ -1715,6 +1725,7 @@ __device__ __forceinline__ void pass_body(const DevProb &P, const SearchArgs &S,
         atomicMax(&S.hdr->dbg_maxb[jtop], dbg_nb);
     }
 #endif
+    return optimistic;
 }
 
 // End of a search level for one CTA: merge the warps' bests into the CTA's slot
