@@ -334,3 +334,19 @@ def test_c4_b200_preset_full_golden(api, oracle):
     assert pr.index == g["index"] and (pr.gpus_used, pr.quota_used) == (g["u"], g["U"])
     sc = oracle.score(prob, pr.index, loads=e["min_resource"]["loads"])
     assert sc.level_verdict == [0]
+
+
+@pytest.mark.parametrize("cap", [3000, 30000, 300000])
+def test_optimistic_thread_mode_redo(api, cap, monkeypatch):
+    """Small frontiers make the optimistic thread-per-parent passes overflow, so they
+    are redone in the warp mode (and with the smallest, the warp mode itself falls back
+    to inline descents): the full-C4 and C4b plans stay the O7 goldens'."""
+    monkeypatch.setenv("CAMELOT_FRONTIER_CAP", str(cap))
+    prob, e = c4_golden()
+    pm, pr = api.Session(prob, n_loads=1).plan_max_then_min(0.3)
+    assert pm.index == e["max_load"]["index"] and fb(pm.objective) == fb(e["max_load"]["T"])
+    assert pr.index == e["min_resource"]["index"]
+    eb = json.load(open(os.path.join(GOLD, "expected_C4b-full.json")))
+    pb = G.config_problems(7)[0]
+    bm, br = api.Session(pb, n_loads=1).plan_max_then_min(0.3)
+    assert bm.index == eb["max_load"]["index"] and br.index == eb["min_resource"]["index"]
