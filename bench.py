@@ -204,8 +204,8 @@ def cpu_reference_leg(prob, args, as_main):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="camelot", choices=["camelot", "reference"])
     ap.add_argument("--config", type=int, default=4, help="BASELINE config (default 4 = C4)")
     ap.add_argument("--backend", default=None, choices=["nccl", "gloo"],
