@@ -176,11 +176,12 @@ def cpu_reference_leg(prob, args, as_main):
     t0 = time.perf_counter()
     O.search(prob, lo=lo, hi=lo + 200_000, threads=threads)
     rate0 = 200_000 / max(1e-6, time.perf_counter() - t0)
-    per_step = args.ref_seconds if as_main else args.cpu_seconds
-    n = int(max(100_000, min(5e9, rate0 * per_step)))
-    times = []
     steps = args.steps if as_main else 1
     warm = args.warmup if as_main else 0
+    # the reference arm's whole run stays within ~2.5 minutes for any --steps / --warmup
+    per_step = max(0.5, min(args.ref_seconds, 150.0 / (steps + warm))) if as_main else args.cpu_seconds
+    n = int(max(100_000, min(5e9, rate0 * per_step)))
+    times = []
     for s in range(warm + steps):
         a = lo + s * n
         t0 = time.perf_counter()
