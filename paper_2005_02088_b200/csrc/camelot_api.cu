@@ -741,6 +741,7 @@ int search_pass(const Ctx &X, int dev, int policy, int nlev, bool prune, int str
     S.xshift = xshift_of(X.d.ntot);
     S.tmode_min16 = getenv("CAMELOT_TMODE_MIN16") ? atoi(getenv("CAMELOT_TMODE_MIN16")) : 32;   // (testing knob)
     S.tmode_inner_gmax = getenv("CAMELOT_TMODE_INNER_G") ? atoi(getenv("CAMELOT_TMODE_INNER_G")) : 8;   // (testing knob)
+    S.tmode_leaf_gmax = getenv("CAMELOT_TMODE_LEAF_G") ? atoi(getenv("CAMELOT_TMODE_LEAF_G")) : 8;   // (testing knob)
     S.tmode_slack = 1;   // separate launches have no redo: strict capacity (the cooperative level sets its own)
     S.result = result;
     S.keys = keys;
@@ -804,6 +805,7 @@ int rescan_pass(const Ctx &X, int dev, int policy, int nlev, bool prune, int k, 
     S.xshift = xshift_of(X.d.ntot);
     S.tmode_min16 = getenv("CAMELOT_TMODE_MIN16") ? atoi(getenv("CAMELOT_TMODE_MIN16")) : 32;   // (testing knob)
     S.tmode_inner_gmax = getenv("CAMELOT_TMODE_INNER_G") ? atoi(getenv("CAMELOT_TMODE_INNER_G")) : 8;   // (testing knob)
+    S.tmode_leaf_gmax = getenv("CAMELOT_TMODE_LEAF_G") ? atoi(getenv("CAMELOT_TMODE_LEAF_G")) : 8;   // (testing knob)
     S.tmode_slack = 1;   // separate launches have no redo: strict capacity (the cooperative level sets its own)
     CU(cudaMemsetAsync(&hdr->best_obj, 0xFF, sizeof(unsigned int), X.st));
     CU(cudaMemsetAsync(&hdr->best_packed, 0xFF, sizeof(unsigned long long), X.st));

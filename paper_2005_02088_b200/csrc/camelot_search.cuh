@@ -78,6 +78,7 @@ struct SearchArgs {
     int xshift;                 // index >> xshift fits 32 bits (tie pruning key)
     int tmode_min16;            // thread-per-parent mode from count >= tmode_min16 / 16 x resident warps
     int tmode_inner_gmax;       // inner passes: up to this many lanes per parent (32 children per lane)
+    int tmode_leaf_gmax;        // leaf passes: up to this many lanes per parent (32 children per lane)
     int tmode_slack;            // inner thread-per-parent passes allowed up to count x maxc <= slack x out_cap
                                 // (> 1: optimistic -- the caller redoes an overflowing pass in the warp mode)
     int no_tmode;               // the redo: warp mode only
@@ -1364,14 +1365,14 @@ __device__ __forceinline__ bool pass_body(const DevProb &P, const SearchArgs &S,
     // leaf passes at most 32 children per lane
     int G = 1;
     while (G < 8 && count * (unsigned long long)(2 * G) <= 32ull * nwarps) G *= 2;
-    if (leafp) G = max(G, maxc <= 32 ? 1 : maxc <= 64 ? 2 : 4);
+    if (leafp) G = max(G, maxc <= 32 ? 1 : maxc <= 64 ? 2 : maxc <= 128 ? 4 : 8);
     // inner passes: G lanes per parent also keep <= 32 children per lane (survivor mask)
     const int Gin = max(G, maxc <= 32 ? 1 : maxc <= 64 ? 2 : maxc <= 128 ? 4 : 8);
     const bool inner_t = S.flevel == jtop + 1 && maxc <= 32 * min(Gin, S.tmode_inner_gmax) &&
                          count * (unsigned long long)maxc <= S.out_cap * (unsigned long long)max(1, S.tmode_slack);
     if (!leafp && inner_t) G = Gin;
     const bool tmode = S.prune && have_in && split == 1 && 16ull * count >= (unsigned long long)S.tmode_min16 * nwarps && !getenv_tmode_off() &&
-                       !S.no_tmode && ((leafp && maxc <= 128) || inner_t);
+                       !S.no_tmode && ((leafp && maxc <= 32 * min(8, S.tmode_leaf_gmax)) || inner_t);
     const bool optimistic = tmode && !leafp && count * (unsigned long long)maxc > S.out_cap;
     const unsigned grab = tmode ? 32u / (unsigned)G : screen ? 8u : (unsigned)S.grab;
     const unsigned long long nw = nwarps * grab;
