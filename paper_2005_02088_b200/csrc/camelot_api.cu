@@ -757,6 +757,8 @@ int search_pass(const Ctx &X, int dev, int policy, int nlev, bool prune, int str
         // optimistic thread-per-parent inner passes (redone in the warp mode on overflow;
         // testing knob CAMELOT_TMODE_SLACK)
         LA.S.tmode_slack = getenv("CAMELOT_TMODE_SLACK") ? std::max(1, atoi(getenv("CAMELOT_TMODE_SLACK"))) : 8;
+        // compact depth-1 frontier (testing knob CAMELOT_COMPACT1=0 keeps full nodes)
+        LA.S.compact1 = !(getenv("CAMELOT_COMPACT1") && getenv("CAMELOT_COMPACT1")[0] == '0');
         if (defer) {   // chained into one cooperative launch by the caller
             defer->push_back(LA);
             return CAMELOT_OK;

@@ -933,6 +933,9 @@ __device__ __forceinline__ void level_body(const DevProb &P, const LevelArgs &LA
     init_warp_best(S, wb, lane);
     Counters cn = {0, 0, 0, 0};
     const int n = P.n;
+    // compact depth-1 frontier (2 words per child of the root pass) when depth 1 is an
+    // inner level (testing knob: LevelArgs.S.compact1 = 0 keeps full nodes)
+    S.compact1 = S.compact1 && n >= 3;
     for (int j = 0; j < n; ++j) {
         S.level = j;
         S.flevel = (j + 1 <= n - 1) ? j + 1 : -1;

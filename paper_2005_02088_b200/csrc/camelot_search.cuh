@@ -82,6 +82,8 @@ struct SearchArgs {
     int tmode_slack;            // inner thread-per-parent passes allowed up to count x maxc <= slack x out_cap
                                 // (> 1: optimistic -- the caller redoes an overflowing pass in the warp mode)
     int no_tmode;               // the redo: warp mode only
+    int compact1;               // the depth-1 frontier holds (batch combo, stage-0 option) pairs: the
+                                // root pass writes 2 words per child, the depth-1 pass rebuilds the node
     // fused reduction (last pass): the last CTA reduces all slots
     int reduce_last;
     Slot *result;               // [nlev] exact local best
@@ -1354,7 +1356,8 @@ __device__ __forceinline__ bool pass_body(const DevProb &P, const SearchArgs &S,
     // parents at a time and screens them lane-parallel against the current bound
     // from a few coalesced frontier words before copying any survivor.
     const unsigned long long nwarps = (unsigned long long)gridDim.x * SEARCH_WARPS;
-    const bool screen = S.prune && have_in && split == 1 && count >= 16ull * nwarps;
+    const bool compact_in = S.compact1 && jtop == 1;   // parents are (batch combo, stage-0 option) pairs
+    const bool screen = S.prune && have_in && split == 1 && count >= 16ull * nwarps && !compact_in;
     // thread-per-parent mode: leaf passes with one level, or inner passes whose children
     // all fit in the output frontier (no inline descent possible in this mode)
     // (measured: leaf passes with more than 32 options per parent are faster in the warp mode)
@@ -1372,7 +1375,7 @@ __device__ __forceinline__ bool pass_body(const DevProb &P, const SearchArgs &S,
                          count * (unsigned long long)maxc <= S.out_cap * (unsigned long long)max(1, S.tmode_slack);
     if (!leafp && inner_t) G = Gin;
     const bool tmode = S.prune && have_in && split == 1 && 16ull * count >= (unsigned long long)S.tmode_min16 * nwarps && !getenv_tmode_off() &&
-                       !S.no_tmode && ((leafp && maxc <= 32 * min(8, S.tmode_leaf_gmax)) || inner_t);
+                       !S.no_tmode && !compact_in && ((leafp && maxc <= 32 * min(8, S.tmode_leaf_gmax)) || inner_t);
     const bool optimistic = tmode && !leafp && count * (unsigned long long)maxc > S.out_cap;
     const unsigned grab = tmode ? 32u / (unsigned)G : screen ? 8u : (unsigned)S.grab;
     const unsigned long long nw = nwarps * grab;
@@ -1381,7 +1384,7 @@ __device__ __forceinline__ bool pass_body(const DevProb &P, const SearchArgs &S,
     // parent's node is copied asynchronously (cp.async) into stack[0] while the current
     // one is searched, and the next work item is popped one item ahead, so neither the
     // queue atomic nor the node copy sits on the warp's critical path.
-    const bool pipe = have_in && jtop >= 1 && !tmode;
+    const bool pipe = have_in && jtop >= 1 && !tmode && !compact_in;
     unsigned long long pf_e = ~0ull;    // parent node in stack[0] (copy issued)
     unsigned long long top_e = ~0ull;   // parent node in stack[jtop]
     unsigned long long nx_raw = 0;      // lane 0: the popped-ahead item (nx_state == 1)
@@ -1520,6 +1523,15 @@ __device__ __forceinline__ bool pass_body(const DevProb &P, const SearchArgs &S,
                     if (nx_e < items) e2 = parent_of(nx_e);
                 }
                 if (e2 != ~0ull && e2 != top_e && e2 != pf_e) prefetch(e2);
+            } else if (compact_in) {   // rebuild the depth-1 node: the root, then stage 0's option
+                const int bc = (int)__ldcg(in.base + e);
+                const int k0 = (int)__ldcg(in.base + (size_t)in.cap + e);
+                build_root<CM>(P, bc, stack[0], lane);
+                if (lane < NMAX) stack[0].kidx[lane] = 0;
+                __syncwarp();
+                const OptRec *l0 = list_of(P, S, 0, stack[0].b[P.app[0]]);
+                build_child<CM>(P, S, stack[0], 0, l0[k0], k0, stack[1], lane);
+                __syncwarp();
             } else {
                 copy_node<CM>(stack[jtop], in, e, lane);
             }
@@ -1702,7 +1714,14 @@ __device__ __forceinline__ bool pass_body(const DevProb &P, const SearchArgs &S,
                     fbase = __shfl_sync(0xffffffffu, fbase, 0);
                     const unsigned long long slot = fbase + __popc(m & ((1u << lane) - 1u));
                     const bool fits = sv && slot < S.out_cap;
-                    if (fits) emit_child<CM, NS>(P, nd, c, j, r, cold.x, cold.y, cold.z, opt, outf, slot);
+                    if (fits) {
+                if (S.compact1 && j == 0) {   // compact depth-1 child: (batch combo, option of stage 0)
+                    outf.put(0, slot, (uint32_t)c.bc);
+                    outf.put(1, slot, (uint32_t)opt);
+                } else {
+                    emit_child<CM, NS>(P, nd, c, j, r, cold.x, cold.y, cold.z, opt, outf, slot);
+                }
+            }
                     PTM(5);
                     m = __ballot_sync(0xffffffffu, sv && !fits);   // frontier full: descend inline
                 }
