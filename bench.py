@@ -37,8 +37,8 @@ UNIT = "candidates/s"
 WORKLOAD = "C4: 5-stage p1-c2-m2-c3-m1 pipeline, 8 modeled V100 (BW 897 GB/s), 1% quota grid, " \
            "batch 1..128 (pow2), <=4 replicas/stage; max-load then min-resource at 0.3*T*"
 LOW_LOAD = 0.3   # low load = 30% of the peak
-TRAFFIC_CSV = "r02_v15_ncu_search_raw.csv"   # committed ncu --set full capture of the search launches
-FLAT_CSV = "r02_v15_ncu_flat_raw.csv"        # committed ncu --set full capture of the flat sweep (same slice)
+TRAFFIC_CSV = "r02_v16_ncu_search_raw.csv"   # committed ncu --set full capture of the search launches
+FLAT_CSV = "r02_v16_ncu_flat_raw.csv"        # committed ncu --set full capture of the flat sweep (same slice)
 
 
 def ncu_metric(name, key, launch=0):
